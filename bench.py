@@ -1,0 +1,426 @@
+"""Benchmark of the batched env step (the reference's hot path) on B200.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
+
+A "step" is one BatchEnv.step over every world of the job (envkit.py:625-646):
+dynamics + reward (+ info terms) + obs + truncation + Philox autoreset, with
+synthetic U(-1, 1) actions pre-generated in HBM.  K steps are executed as
+K / --unroll fused rollout launches (one kernel each) cycling through a ring of
+action / output chunks larger than L2.  Rank r owns global worlds
+[r*N, (r+1)*N) -- no collective on the data path ("weak" scaling).
+
+Prints ONE JSON line (rank 0) with the metric, roofline of the rollout kernel,
+the CPU oracle baseline, an end-to-end number through the host-buffer C ABI
+(dk_env_rollout_host) and the clocks seen during the timed region.
+
+--impl reference times the reference's algorithm on the host CPU instead: the
+C restatement in oracle/ (kind "port"; the reference is pure Python and cannot
+be installed on the GPU box), all host threads, same workload and metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import platform
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "physics steps/sec (8192 worlds/GPU) at 1/2/4/8 B200 vs CPU host"
+UNIT = "physics_steps/s"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100_000)
+    ap.add_argument("--warmup", type=int, default=3_000)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--task", default="cartpole-balance")
+    ap.add_argument("--num-envs", type=int, default=8192, help="worlds per GPU")
+    ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--unroll", type=int, default=1000, help="env steps fused per launch")
+    ap.add_argument("--ring", type=int, default=6, help="action/output chunks in the ring")
+    ap.add_argument("--e2e-steps", type=int, default=20_000)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# algorithmic bytes: per world-step and per launch
+
+
+def bytes_per_world_step(A, O, I, esz):
+    # action in; obs, reward, info out; done, trunc, terminal_mask flags out
+    return esz * (A + O + 1 + I) + 3
+
+
+def state_io_bytes(NS, esz):
+    # per world per launch: state read + write, steps/episode/needs_reset read + write
+    return 2 * (NS * esz + 4 + 4 + 1)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (NVML, the library nvidia-smi reads)
+
+
+class ClockSampler:
+    REASONS = {
+        "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+        "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+        "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        "display_clock_setting": 0x100,
+    }
+
+    def __init__(self, device_index: int, period_s: float = 0.002):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._period = period_s
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            self._nv = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - no NVML
+            self._nv = None
+            self.error = str(e)
+
+    def _run(self):
+        nv = self._nv
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                mask = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in self.REASONS.items():
+                    if mask & bit:
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            time.sleep(self._period)
+
+    def __enter__(self):
+        if self._nv is not None:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._nv is not None:
+            self._t.join()
+
+    def summary(self):
+        if self._nv is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "error": self.error}
+        return {"sm_mhz": float(np.median(self.samples)) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons - {"gpu_idle"}),
+                "samples": len(self.samples)}
+
+
+def hbm_peak():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(task, dtype, num_envs, unroll):
+    """dram bytes per launch of the rollout kernel from the committed ncu capture."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            tab = json.load(f)
+        return tab.get(f"{task}/{dtype}/{num_envs}/{unroll}")
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port of the reference algorithm on the host cores
+
+
+def cpu_rate(task, num_envs, seconds, nthreads=0, steps=None):
+    from oracle.oracle import ACTION_DIM, TASK_IDS, OracleBatchEnv, max_threads
+
+    A = ACTION_DIM[TASK_IDS[task]]
+    env = OracleBatchEnv(task, num_envs)
+    env.reset(seed=0)
+    rng = np.random.default_rng(0)
+    threads = nthreads or max_threads()
+    probe = 20
+    acts = rng.uniform(-1, 1, (probe, num_envs, A))
+    t0 = time.perf_counter()
+    env.rollout(acts, nthreads=threads)
+    dt = time.perf_counter() - t0
+    if steps is None:
+        steps = max(probe, int(seconds / max(dt / probe, 1e-9)))
+    acts = rng.uniform(-1, 1, (min(steps, 2000), num_envs, A))
+    done = 0
+    t0 = time.perf_counter()
+    while done < steps:
+        k = min(steps - done, acts.shape[0])
+        env.rollout(acts[:k], nthreads=threads)
+        done += k
+    dt = time.perf_counter() - t0
+    return steps * num_envs / dt, threads, steps, dt
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return platform.processor()
+
+
+# ---------------------------------------------------------------------------
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return
+    from oracle.oracle import build as build_oracle
+
+    build_oracle()
+    # warm-up W steps (bounded), then exactly K steps, each one batched step
+    # of num_envs worlds on all host threads
+    cpu_rate(args.task, args.num_envs, 0.5, steps=max(3, min(args.warmup, 200)))
+    rate, threads, steps, dt = cpu_rate(args.task, args.num_envs, 0, steps=args.steps)
+    cores = threads
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+        "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic U(-1,1) actions",
+        "config": {"workload": f"{args.task} BatchEnv.step, {args.num_envs} worlds, autoreset, "
+                               "episode_length 1000, reward info terms", "num_envs": args.num_envs,
+                   "task": args.task},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
+                         "sample": f"{steps} steps x {args.num_envs} worlds on {cores} threads "
+                                   f"({cpu_model()}); oracle/oracle.c, the bit-exact C "
+                                   "restatement of deskrl BatchEnv.step"},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, world, local_rank, dist):
+    import torch
+
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import _native
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = args.num_envs
+    cfg = dk.EnvConfig(task=args.task)
+    env = dk.DeviceBatchEnv(cfg, n, dtype=args.dtype, device=local_rank,
+                            env_index_offset=rank * n)
+    A, O, I, NS = env.action_dim, env.obs_dim, len(env.info_keys), env.spec.state_dim
+    tdt = env.dtype
+    esz = 8 if tdt == torch.float64 else 4
+    U = min(args.unroll, args.steps)
+    R = max(2, args.ring)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    acts = [torch.rand((U, n, A), generator=gen, device=dev, dtype=tdt) * 2 - 1 for _ in range(R)]
+    outs = [env._outputs((U,), True) for _ in range(R)]
+    env.reset(seed=0)
+    stream = torch.cuda.current_stream(dev)
+
+    def launch(j, k):
+        a = acts[j % R] if k == U else acts[j % R][:k]
+        o = outs[j % R] if k == U else {kk: (v[:k] if v is not None else None)
+                                         for kk, v in outs[j % R].items()}
+        env.rollout(a, with_info=True, out=o)
+
+    # warm-up
+    w_left, j = args.warmup, 0
+    while w_left > 0:
+        k = min(U, w_left)
+        launch(j, k)
+        w_left -= k
+        j += 1
+    env.check()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush.zero_()  # evict L2 before the timed region
+    torch.cuda.synchronize(dev)
+
+    nlaunch = (args.steps + U - 1) // U
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(nlaunch)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = env.kernel_launches
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(local_rank) as clocks:
+        t_start.record(stream)
+        left = args.steps
+        for L in range(nlaunch):
+            k = min(U, left)
+            evs[L][0].record(stream)
+            launch(j + L, k)
+            evs[L][1].record(stream)
+            left -= k
+        t_end.record(stream)
+        torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    env.check()
+    gpu_launches = env.kernel_launches - launches0
+    elapsed_ms = t_start.elapsed_time(t_end)
+    launch_ms = [s.elapsed_time(e) for s, e in evs]
+    full = [t for t, L in zip(launch_ms, range(nlaunch)) if (L + 1) * U <= args.steps] or launch_ms
+    if dist is not None:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    total_steps = args.steps * n * world * cfg.action_repeat
+    value = total_steps / (elapsed_ms / 1e3)
+
+    # roofline of the rollout kernel (the only kernel of a launch)
+    peak, peak_src = hbm_peak()
+    bpw = bytes_per_world_step(A, O, I, esz)
+    alg_bytes_launch = n * U * bpw + n * state_io_bytes(NS, esz) + n * (U // 1000) * O * esz
+    avg_launch_s = float(np.mean(full)) / 1e3
+    achieved = alg_bytes_launch / avg_launch_s / 1e9
+
+    # end-to-end through the C ABI with pinned host buffers (H2D actions,
+    # D2H every output), chunked and pipelined inside dk_env_rollout_host
+    e2e = None
+    if args.e2e_steps > 0:
+        e2e = measure_e2e(env, args, dev, dist, A, O, I, esz, world)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        try:
+            rate, threads, steps, dt = cpu_rate(args.task, n, args.cpu_seconds)
+            cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                   "sample": f"{steps} steps x {n} worlds in {dt:.1f}s on {threads} threads "
+                             f"({cpu_model()}); oracle/oracle.c, bit-exact C restatement of "
+                             "deskrl BatchEnv.step (reference itself is single-threaded Python)"}
+        except Exception as e:  # pragma: no cover
+            cpu = {"value": None, "error": str(e)}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if esz == 4 else "f64",
+            "data": "synthetic U(-1,1) actions pre-generated in HBM",
+            "config": {
+                "workload": f"{args.task} BatchEnv.step (dynamics, reward + info terms, obs, "
+                            "truncation, Philox autoreset), episode_length 1000; BASELINE's Go1 "
+                            "joystick physics does not exist in the reference (SURVEY.md §0)",
+                "task": args.task, "worlds_per_gpu": n, "global_worlds": n * world,
+                "steps_per_launch": U, "parallelism": f"worlds sharded dp{world}",
+                "l2": f"flushed before the timed region; {R}-chunk ring of "
+                      f"{U * n * (bpw + A * esz) / 1e6:.0f} MB chunks > 126 MB L2",
+            },
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "traffic": ncu_traffic(args.task, args.dtype, n, U),
+                         "kernel": "rollout_kernel", "alg_bytes_per_launch": alg_bytes_launch,
+                         "bytes_per_world_step": bpw, "avg_launch_ms": avg_launch_s * 1e3},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": gpu_launches,
+            "clocks": clocks.summary(),
+            "library": _native.LIB_PATH,
+        }
+        print(json.dumps(line), flush=True)
+    env.close()
+
+
+def measure_e2e(env, args, dev, dist, A, O, I, esz, world):
+    import ctypes
+
+    import torch
+
+    n = env.num_envs
+    K = args.e2e_steps
+    chunk = min(args.unroll, K)
+    npdt = np.float64 if esz == 8 else np.float32
+
+    def pinned(shape, dt):
+        tdt = {np.float32: torch.float32, np.float64: torch.float64, np.uint8: torch.uint8}[dt]
+        return torch.empty(shape, dtype=tdt, pin_memory=True).numpy()
+
+    acts = pinned((K, n, A), npdt)
+    acts[:] = np.random.default_rng(7).uniform(-1, 1, (K, n, A))
+    obs, rew = pinned((K, n, O), npdt), pinned((K, n), npdt)
+    done, trunc, mask = pinned((K, n), np.uint8), pinned((K, n), np.uint8), pinned((K, n), np.uint8)
+    term, info = pinned((K, n, O), npdt), pinned((K, n, I), npdt)
+    lib = env._h._lib
+    h = env._h.h
+
+    def call(k):
+        rc = lib.dk_env_rollout_host(h, k, chunk, acts.ctypes.data, obs.ctypes.data,
+                                     rew.ctypes.data, done.ctypes.data, trunc.ctypes.data,
+                                     term.ctypes.data, mask.ctypes.data, info.ctypes.data)
+        if rc != 0:
+            raise RuntimeError(f"dk_env_rollout_host failed: {rc}")
+
+    call(min(K, 2 * chunk))  # warm-up (allocates the scratch ring)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    call(K)
+    dt = time.perf_counter() - t0
+    if dist is not None:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    nterm = int(mask.sum())
+    h2d = n * A * esz
+    d2h = n * (O * esz + esz + 3 + I * esz) + nterm * O * esz / K
+    return {"value": K * n * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
+            "d2h_bytes_per_step": d2h, "api": "dk_env_rollout_host (C ABI, pinned host buffers)",
+            "steps": K, "chunk_steps": chunk}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank)
+        return
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as tdist
+
+        torch.cuda.set_device(local_rank)
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        dist = tdist
+    try:
+        run_b200(args, rank, world, local_rank, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

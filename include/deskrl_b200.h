@@ -1,0 +1,165 @@
+/*
+ * deskrl_b200.h -- C ABI of the B200-native batched env step.
+ *
+ * This is the drop-in boundary for the reference's hot path, the batched
+ * env reset/step of deskrl (/root/reference/pkg/src/deskrl/envkit.py:595-650).
+ * The reference has no native layer; its specified native boundary is the
+ * "bindings" BoundEnvHandle (make_env / reset / step with
+ * contiguous arrays, single-writer handle), realised there as JSON over stdio
+ * (serve.py:48-108).  Each entry point below names the reference interface it
+ * replaces.  INTEGRATION.md shows the ctypes binding a maintainer would add.
+ *
+ * Conventions
+ *  - Plain C types only.  Buffers are caller-owned.  Functions without the
+ *    _host suffix take DEVICE pointers and enqueue work on `stream`
+ *    (a cudaStream_t passed as void*, NULL = legacy default stream) without
+ *    synchronising.  The _host variants take host pointers (pinned for full
+ *    speed), copy in/out internally and return after the results are in the
+ *    host buffers, like the reference's synchronous numpy call.
+ *  - Element type of every floating-point buffer is the env's dtype
+ *    (DK_F32 -> float, DK_F64 -> double).  Flags are uint8 (0/1).
+ *  - Layouts are row-major: actions [N, A]; obs [N, O]; rewards [N];
+ *    info [N, I].  Rollouts are time-major: [K, N, ...].
+ *  - Return value: DK_OK or a DK_ERR_* code; dk_last_error() holds the
+ *    message (thread-local).
+ *  - A handle is single-writer: do not drive one handle from
+ *    two host threads at once.
+ */
+#ifndef DESKRL_B200_H
+#define DESKRL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DK_ABI_VERSION 1
+
+/* Status codes.  The Python host maps them to the reference's exception
+ * classes: ConfigError (randomization.py:19), InvalidInputError
+ * (mathcore.py:22), UsageError (envkit.py:37). */
+enum {
+    DK_OK = 0,
+    DK_ERR_CONFIG = 1,
+    DK_ERR_INVALID_INPUT = 2,
+    DK_ERR_USAGE = 3,
+    DK_ERR_CUDA = 4,
+};
+
+/* Task ids; names as registered_tasks() (envkit.py:456-462). */
+enum {
+    DK_TASK_PENDULUM_SWINGUP = 0, /* "pendulum-swingup"  envkit.py:255-294 */
+    DK_TASK_CARTPOLE_BALANCE = 1, /* "cartpole-balance"  envkit.py:297-349 */
+    DK_TASK_ACROBOT_SWINGUP = 2,  /* "acrobot-swingup"   envkit.py:383-409 */
+    DK_TASK_REACHER_EASY = 3,     /* "reacher-easy"      envkit.py:412-453 */
+};
+
+enum { DK_F32 = 0, DK_F64 = 1 };
+
+/* Model: DynamicsParams (dynamics.py:36-60), same fields, same order.
+ * dt is the effective step (EnvConfig.dt or the task default,
+ * envkit.py:485-487). */
+typedef struct dk_dynamics_params {
+    double dt, gravity;
+    double pend_mass, pend_length, pend_damping, pend_torque_limit;
+    double cart_mass, pole_mass, pole_length, rail_limit, cart_force_limit;
+    double link1_mass, link2_mass, link1_length, link2_length, link_damping;
+    double elbow_torque_limit, reacher_torque_limit;
+} dk_dynamics_params;
+
+/* EnvConfig fields on the step path (envkit.py:56-75). */
+typedef struct dk_env_config {
+    int32_t task;           /* DK_TASK_* */
+    int32_t dtype;          /* DK_F32 or DK_F64: arithmetic and buffer type */
+    int64_t episode_length; /* control steps, 1 .. 2^31-1 */
+    int64_t action_repeat;  /* >= 1 */
+    int32_t wide_init;      /* pendulum full-circle starts (envkit.py:263-268) */
+    int32_t reserved;
+    uint64_t seed;          /* EnvConfig.seed; reset() may replace it */
+} dk_env_config;
+
+typedef struct dk_env dk_env;
+
+/* Task name -> DK_TASK_* (or -1); dimensions of a task. */
+int dk_task_id(const char *name);
+int dk_task_dims(int task, int *action_dim, int *obs_dim, int *info_dim);
+
+/* BatchEnv.__init__ (envkit.py:598-609) + Environment.__init__ (472-495).
+ * Allocates the per-world state (structure of arrays) on `device`.
+ * env_index_offset is the global index of world 0 (multi-GPU sharding:
+ * rank r passes r*num_envs so Philox streams match a single-device run). */
+int dk_env_create(const dk_env_config *cfg, const dk_dynamics_params *params,
+                  int64_t num_envs, int64_t env_index_offset, int device, dk_env **out);
+
+/* BatchEnv.close (envkit.py:648-650); frees device memory. */
+int dk_env_destroy(dk_env *env);
+
+/* BatchEnv.reset (envkit.py:616-623).  has_seed != 0 models reset(seed=s):
+ * seed replaced, episode counters rewound; otherwise every world starts its
+ * next episode.  Clears a pending sticky error.  obs_out: [N, O] device. */
+int dk_env_reset(dk_env *env, int has_seed, uint64_t seed, void *obs_out, void *stream);
+
+/* BatchEnv.step (envkit.py:625-646) on device buffers.
+ *   actions        [N, A]  in
+ *   obs_out        [N, O]  observation after the step (post-reset obs where
+ *                          a world auto-reset), == "state" == "privileged_state"
+ *   reward_out     [N]
+ *   done_out       [N]     u8 (always 0 for these tasks, envkit.py:543)
+ *   trunc_out      [N]     u8
+ *   terminal_obs   [N, O]  written only where terminal_mask is 1 (may be NULL)
+ *   terminal_mask  [N]     u8, infos[i]["terminal_observation"] present (may be NULL)
+ *   info_out       [N, I]  reward terms of infos[i] (may be NULL)
+ * Validation is batch-atomic: a non-finite action or a world that needs a
+ * reset makes the whole call a no-op and leaves a sticky error that
+ * dk_env_check_error() reports (the reference raises after having stepped
+ * the worlds before the offending one, envkit.py:527-531, 630-637). */
+int dk_env_step(dk_env *env, const void *actions, int autoreset, void *obs_out, void *reward_out,
+                uint8_t *done_out, uint8_t *trunc_out, void *terminal_obs_out,
+                uint8_t *terminal_mask_out, void *info_out, void *stream);
+
+/* K consecutive BatchEnv.step(autoreset=True) calls fused into one launch
+ * (the unroll loop of ppo.collect_rollout, ppo.py:308-322, and of
+ * bench.measure_stage, bench.py:122-125).  actions [K, N, A]; outputs
+ * [K, N, ...] time-major, same meaning as dk_env_step. */
+int dk_env_rollout(dk_env *env, int64_t num_steps, const void *actions, void *obs_out,
+                   void *reward_out, uint8_t *done_out, uint8_t *trunc_out,
+                   void *terminal_obs_out, uint8_t *terminal_mask_out, void *info_out,
+                   void *stream);
+
+/* Host-buffer variants (synchronous).  dk_env_rollout_host pipelines the
+ * host<->device copies of chunks of `chunk_steps` steps against the compute
+ * of neighbouring chunks on internal streams. */
+int dk_env_reset_host(dk_env *env, int has_seed, uint64_t seed, void *obs_out);
+int dk_env_step_host(dk_env *env, const void *actions, int autoreset, void *obs_out,
+                     void *reward_out, uint8_t *done_out, uint8_t *trunc_out,
+                     void *terminal_obs_out, uint8_t *terminal_mask_out, void *info_out);
+int dk_env_rollout_host(dk_env *env, int64_t num_steps, int64_t chunk_steps, const void *actions,
+                        void *obs_out, void *reward_out, uint8_t *done_out, uint8_t *trunc_out,
+                        void *terminal_obs_out, uint8_t *terminal_mask_out, void *info_out);
+
+/* Synchronises `stream` and reports (then clears) the sticky error left by
+ * dk_env_step / dk_env_rollout: returns DK_OK, DK_ERR_INVALID_INPUT
+ * (non-finite action) or DK_ERR_USAGE (world needs reset); *step_index and
+ * *env_index locate the first offending (step, world) in reference order. */
+int dk_env_check_error(dk_env *env, void *stream, int64_t *step_index, int64_t *env_index);
+
+/* Per-world state as float64 host arrays (Environment.state / steps /
+ * _episode / _needs_reset / _target, envkit.py:490-513): state [N, 4],
+ * target [N, 2], steps [N], episode [N], needs_reset [N].  Any may be NULL.
+ * Synchronous.  set_state writes them back (tests, render-preview). */
+int dk_env_get_state(dk_env *env, double *state, double *target, int64_t *steps,
+                     int64_t *episode, uint8_t *needs_reset);
+int dk_env_set_state(dk_env *env, const double *state, const double *target,
+                     const int64_t *steps, const int64_t *episode, const uint8_t *needs_reset);
+
+/* Number of kernels this handle has launched (evidence for bench.py). */
+int64_t dk_env_kernel_launches(const dk_env *env);
+
+int dk_abi_version(void);
+const char *dk_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DESKRL_B200_H */

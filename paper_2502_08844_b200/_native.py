@@ -1,0 +1,95 @@
+"""ctypes binding of the C ABI in include/deskrl_b200.h (libdeskrl_b200.so).
+
+There is no fallback: if the sm_100a library is missing this raises at import
+of the env classes, so a GPU run can never silently fall back to CPU code.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdeskrl_b200.so")
+
+DK_OK, DK_ERR_CONFIG, DK_ERR_INVALID_INPUT, DK_ERR_USAGE, DK_ERR_CUDA = range(5)
+DK_F32, DK_F64 = 0, 1
+
+# DynamicsParams field order (dynamics.py:40-60)
+PARAM_FIELDS = (
+    "dt", "gravity", "pend_mass", "pend_length", "pend_damping", "pend_torque_limit",
+    "cart_mass", "pole_mass", "pole_length", "rail_limit", "cart_force_limit",
+    "link1_mass", "link2_mass", "link1_length", "link2_length", "link_damping",
+    "elbow_torque_limit", "reacher_torque_limit",
+)
+
+
+class DynamicsParamsC(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_double) for n in PARAM_FIELDS]
+
+
+class EnvConfigC(ctypes.Structure):
+    _fields_ = [
+        ("task", ctypes.c_int32),
+        ("dtype", ctypes.c_int32),
+        ("episode_length", ctypes.c_int64),
+        ("action_repeat", ctypes.c_int64),
+        ("wide_init", ctypes.c_int32),
+        ("reserved", ctypes.c_int32),
+        ("seed", ctypes.c_uint64),
+    ]
+
+
+_vp = ctypes.c_void_p
+_u8p = ctypes.c_void_p
+_i64 = ctypes.c_int64
+
+_SIGS = {
+    "dk_abi_version": (ctypes.c_int, []),
+    "dk_last_error": (ctypes.c_char_p, []),
+    "dk_task_id": (ctypes.c_int, [ctypes.c_char_p]),
+    "dk_task_dims": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                    ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int)]),
+    "dk_env_create": (ctypes.c_int, [ctypes.POINTER(EnvConfigC), ctypes.POINTER(DynamicsParamsC),
+                                     _i64, _i64, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "dk_env_destroy": (ctypes.c_int, [_vp]),
+    "dk_env_reset": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_uint64, _vp, _vp]),
+    "dk_env_step": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp, _u8p, _u8p, _vp, _u8p, _vp,
+                                   _vp]),
+    "dk_env_rollout": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _u8p, _u8p, _vp, _u8p, _vp, _vp]),
+    "dk_env_reset_host": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_uint64, _vp]),
+    "dk_env_step_host": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _vp, _vp, _u8p, _u8p, _vp, _u8p,
+                                        _vp]),
+    "dk_env_rollout_host": (ctypes.c_int, [_vp, _i64, _i64, _vp, _vp, _vp, _u8p, _u8p, _vp, _u8p,
+                                           _vp]),
+    "dk_env_check_error": (ctypes.c_int, [_vp, _vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "dk_env_get_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _u8p]),
+    "dk_env_set_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _u8p]),
+    "dk_env_kernel_launches": (ctypes.c_int64, [_vp]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libdeskrl_b200.so (raises if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build the sm_100a library first "
+                "(python -m paper_2502_08844_b200.build or __graft_entry__.build())")
+        handle = ctypes.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def last_error() -> str:
+    msg = lib().dk_last_error()
+    return msg.decode() if msg else ""

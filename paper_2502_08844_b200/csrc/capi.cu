@@ -1,0 +1,614 @@
+// capi.cu -- the extern "C" boundary declared in include/deskrl_b200.h.
+//
+// Owns the per-handle device state (structure of arrays) and the streams /
+// scratch of the host-buffer entry points.  No torch types cross this
+// boundary; the Python host (paper_2502_08844_b200/envkit.py) drives it via
+// ctypes with raw device pointers.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/deskrl_b200.h"
+#include "envstep_launch.cuh"
+
+namespace dk {
+DK_DECLARE_LAUNCHERS(float)
+DK_DECLARE_LAUNCHERS(double)
+}  // namespace dk
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    g_last_error = buf;
+    return code;
+}
+
+#define DK_CUDA(expr)                                                                        \
+    do {                                                                                     \
+        cudaError_t e_ = (expr);                                                             \
+        if (e_ != cudaSuccess)                                                               \
+            return fail(DK_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_));        \
+    } while (0)
+
+const char *kTaskNames[4] = {"pendulum-swingup", "cartpole-balance", "acrobot-swingup",
+                             "reacher-easy"};
+const int kA[4] = {1, 1, 1, 2}, kO[4] = {3, 5, 6, 10}, kI[4] = {1, 3, 1, 1}, kNS[4] = {2, 4, 4, 6};
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        cudaGetDevice(&prev);
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        cudaGetDevice(&cur);
+        if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+// Device scratch of the host-buffer entry points: two slots of chunk_steps.
+struct HostScratch {
+    int64_t steps = 0;  // capacity per slot (steps)
+    void *actions[2] = {nullptr, nullptr};
+    void *obs[2] = {nullptr, nullptr};
+    void *reward[2] = {nullptr, nullptr};
+    uint8_t *done[2] = {nullptr, nullptr};
+    uint8_t *trunc[2] = {nullptr, nullptr};
+    void *term[2] = {nullptr, nullptr};
+    uint8_t *mask[2] = {nullptr, nullptr};
+    void *info[2] = {nullptr, nullptr};
+};
+
+}  // namespace
+
+struct dk_env {
+    dk_env_config cfg;
+    dk_dynamics_params params;
+    int64_t n = 0, offset = 0;
+    int device = 0;
+    int A = 0, O = 0, I = 0, NS = 0;
+    size_t esz = 4;  // bytes per real
+    void *state[2] = {nullptr, nullptr};      // double-buffered SoA world state
+    int32_t *steps[2] = {nullptr, nullptr};
+    uint32_t *episode[2] = {nullptr, nullptr};
+    uint8_t *needs_reset[2] = {nullptr, nullptr};
+    int32_t *cur = nullptr;                   // live buffer index (device)
+    uint32_t *blocks_done = nullptr;          // last-block counter (device)
+    unsigned long long *err_dev = nullptr;
+    unsigned long long *err_host = nullptr;  // pinned
+    int64_t launches = 0;
+    cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+    cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
+    HostScratch hs;
+};
+
+namespace {
+
+template <typename T>
+dk::Params<T> to_params(const dk_dynamics_params &p) {
+    dk::Params<T> q;
+    q.dt = (T)p.dt; q.gravity = (T)p.gravity;
+    q.pend_mass = (T)p.pend_mass; q.pend_length = (T)p.pend_length;
+    q.pend_damping = (T)p.pend_damping; q.pend_torque_limit = (T)p.pend_torque_limit;
+    q.cart_mass = (T)p.cart_mass; q.pole_mass = (T)p.pole_mass; q.pole_length = (T)p.pole_length;
+    q.rail_limit = (T)p.rail_limit; q.cart_force_limit = (T)p.cart_force_limit;
+    q.link1_mass = (T)p.link1_mass; q.link2_mass = (T)p.link2_mass;
+    q.link1_length = (T)p.link1_length; q.link2_length = (T)p.link2_length;
+    q.link_damping = (T)p.link_damping; q.elbow_torque_limit = (T)p.elbow_torque_limit;
+    q.reacher_torque_limit = (T)p.reacher_torque_limit;
+    return q;
+}
+
+dk::EnvScalars scalars(const dk_env *e, int autoreset) {
+    dk::EnvScalars sc;
+    sc.seed = e->cfg.seed;
+    sc.n = e->n;
+    sc.env_offset = e->offset;
+    sc.episode_length = (int32_t)e->cfg.episode_length;
+    sc.action_repeat = (int32_t)e->cfg.action_repeat;
+    sc.wide_init = e->cfg.wide_init;
+    sc.autoreset = autoreset ? 1 : 0;
+    return sc;
+}
+
+template <typename T>
+dk::Worlds<T> worlds(const dk_env *e) {
+    dk::Worlds<T> w;
+    for (int b = 0; b < 2; ++b) {
+        w.state[b] = (T *)e->state[b];
+        w.steps[b] = e->steps[b];
+        w.episode[b] = e->episode[b];
+        w.needs_reset[b] = e->needs_reset[b];
+    }
+    w.cur = e->cur;
+    w.blocks_done = e->blocks_done;
+    return w;
+}
+
+int rollout_impl(dk_env *e, int64_t K, const void *actions, int autoreset, void *obs, void *reward,
+                 uint8_t *done, uint8_t *trunc, void *term_obs, uint8_t *term_mask, void *info,
+                 cudaStream_t st) {
+    if (!actions || !obs || !reward || !done || !trunc)
+        return fail(DK_ERR_INVALID_INPUT, "actions, obs, reward, done and trunc are required");
+    if (K < 0) return fail(DK_ERR_INVALID_INPUT, "num_steps must be >= 0");
+    if (K == 0) return DK_OK;
+    const dk::EnvScalars sc = scalars(e, autoreset);
+    cudaError_t rc;
+    if (e->cfg.dtype == DK_F64) {
+        dk::StepOut<double> o{(double *)obs, (double *)reward, done, trunc, (double *)term_obs,
+                              term_mask, (double *)info};
+        rc = dk::launch_rollout<double>(e->cfg.task, (const double *)actions, K, sc,
+                                        to_params<double>(e->params), worlds<double>(e), o,
+                                        e->err_dev, st, &e->launches);
+    } else {
+        dk::StepOut<float> o{(float *)obs, (float *)reward, done, trunc, (float *)term_obs,
+                             term_mask, (float *)info};
+        rc = dk::launch_rollout<float>(e->cfg.task, (const float *)actions, K, sc,
+                                       to_params<float>(e->params), worlds<float>(e), o,
+                                       e->err_dev, st, &e->launches);
+    }
+    if (rc != cudaSuccess) return fail(DK_ERR_CUDA, "rollout launch: %s", cudaGetErrorString(rc));
+    // error word -> pinned host copy (read by dk_env_check_error after a sync)
+    DK_CUDA(cudaMemcpyAsync(e->err_host, e->err_dev, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    return DK_OK;
+}
+
+int decode_error(dk_env *e, unsigned long long key, int64_t *step_index, int64_t *env_index) {
+    if (key == dk::kNoError) return DK_OK;
+    const int code = (int)(key & 3ULL);
+    const int64_t flat = (int64_t)(key >> 2);
+    const int64_t k = flat / e->n, i = flat % e->n;
+    if (step_index) *step_index = k;
+    if (env_index) *env_index = i;
+    if (code == dk::kErrUsage)
+        return fail(DK_ERR_USAGE, "environment must be reset before stepping");
+    return fail(DK_ERR_INVALID_INPUT, "action contains non-finite values");
+}
+
+void free_scratch(dk_env *e) {
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(e->hs.actions[b]); cudaFree(e->hs.obs[b]); cudaFree(e->hs.reward[b]);
+        cudaFree(e->hs.done[b]); cudaFree(e->hs.trunc[b]); cudaFree(e->hs.term[b]);
+        cudaFree(e->hs.mask[b]); cudaFree(e->hs.info[b]);
+    }
+    e->hs = HostScratch();
+}
+
+int ensure_scratch(dk_env *e, int64_t steps) {
+    if (e->hs.steps >= steps) return DK_OK;
+    free_scratch(e);
+    const size_t rows = (size_t)steps * (size_t)e->n;
+    for (int b = 0; b < 2; ++b) {
+        DK_CUDA(cudaMalloc(&e->hs.actions[b], rows * e->A * e->esz));
+        DK_CUDA(cudaMalloc(&e->hs.obs[b], rows * e->O * e->esz));
+        DK_CUDA(cudaMalloc(&e->hs.reward[b], rows * e->esz));
+        DK_CUDA(cudaMalloc((void **)&e->hs.done[b], rows));
+        DK_CUDA(cudaMalloc((void **)&e->hs.trunc[b], rows));
+        DK_CUDA(cudaMalloc(&e->hs.term[b], rows * e->O * e->esz));
+        DK_CUDA(cudaMalloc((void **)&e->hs.mask[b], rows));
+        DK_CUDA(cudaMalloc(&e->hs.info[b], rows * e->I * e->esz));
+    }
+    e->hs.steps = steps;
+    return DK_OK;
+}
+
+int check_env(const dk_env *e) {
+    if (!e) return fail(DK_ERR_USAGE, "null env handle");
+    return DK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int dk_abi_version(void) { return DK_ABI_VERSION; }
+const char *dk_last_error(void) { return g_last_error.c_str(); }
+
+int dk_task_id(const char *name) {
+    if (!name) return -1;
+    for (int t = 0; t < 4; ++t)
+        if (std::strcmp(name, kTaskNames[t]) == 0) return t;
+    return -1;
+}
+
+int dk_task_dims(int task, int *a, int *o, int *i) {
+    if (task < 0 || task > 3) return fail(DK_ERR_CONFIG, "unknown task id %d", task);
+    if (a) *a = kA[task];
+    if (o) *o = kO[task];
+    if (i) *i = kI[task];
+    return DK_OK;
+}
+
+int dk_env_create(const dk_env_config *cfg, const dk_dynamics_params *params, int64_t num_envs,
+                  int64_t env_index_offset, int device, dk_env **out) {
+    if (!cfg || !params || !out) return fail(DK_ERR_CONFIG, "null argument");
+    *out = nullptr;
+    if (cfg->task < 0 || cfg->task > 3) return fail(DK_ERR_CONFIG, "unknown task id %d", cfg->task);
+    if (cfg->dtype != DK_F32 && cfg->dtype != DK_F64)
+        return fail(DK_ERR_CONFIG, "dtype must be DK_F32 or DK_F64");
+    if (num_envs < 1) return fail(DK_ERR_CONFIG, "num_envs and num_workers must be >= 1");
+    if (cfg->episode_length <= 0) return fail(DK_ERR_CONFIG, "episode_length must be positive");
+    if (cfg->episode_length > 0x7fffffffLL)
+        return fail(DK_ERR_CONFIG, "episode_length must be < 2^31 on this backend");
+    if (cfg->action_repeat < 1) return fail(DK_ERR_CONFIG, "action_repeat must be >= 1");
+    if (cfg->action_repeat > 0x7fffffffLL) return fail(DK_ERR_CONFIG, "action_repeat too large");
+    if (env_index_offset < 0 || env_index_offset + num_envs > (1LL << 32))
+        return fail(DK_ERR_CONFIG, "global env indices must fit in 32 bits (Philox key layout)");
+    if (!(params->dt > 0)) return fail(DK_ERR_INVALID_INPUT, "dt must be positive");
+
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev == 0)
+        return fail(DK_ERR_CUDA, "no CUDA device available (%s)",
+                    ce == cudaSuccess ? "0 devices" : cudaGetErrorString(ce));
+    if (device < 0 || device >= ndev) return fail(DK_ERR_CONFIG, "bad device %d", device);
+    DeviceGuard g(device);
+
+    dk_env *e = new dk_env();
+    e->cfg = *cfg;
+    e->params = *params;
+    e->n = num_envs;
+    e->offset = env_index_offset;
+    e->device = device;
+    e->A = kA[cfg->task]; e->O = kO[cfg->task]; e->I = kI[cfg->task]; e->NS = kNS[cfg->task];
+    e->esz = cfg->dtype == DK_F64 ? 8 : 4;
+    auto bail = [&](int code) { dk_env_destroy(e); return code; };
+#define DK_TRY(expr)                                                                          \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return bail(fail(DK_ERR_CUDA, "%s failed: %s", #expr, cudaGetErrorString(e_)));   \
+    } while (0)
+    for (int b = 0; b < 2; ++b) {
+        DK_TRY(cudaMalloc(&e->state[b], (size_t)e->NS * num_envs * e->esz));
+        DK_TRY(cudaMalloc((void **)&e->steps[b], num_envs * sizeof(int32_t)));
+        DK_TRY(cudaMalloc((void **)&e->episode[b], num_envs * sizeof(uint32_t)));
+        DK_TRY(cudaMalloc((void **)&e->needs_reset[b], num_envs));
+        DK_TRY(cudaMemset(e->state[b], 0, (size_t)e->NS * num_envs * e->esz));
+        DK_TRY(cudaMemset(e->steps[b], 0, num_envs * sizeof(int32_t)));
+        DK_TRY(cudaMemset(e->episode[b], 0xff, num_envs * sizeof(uint32_t)));  // _episode = -1
+        DK_TRY(cudaMemset(e->needs_reset[b], 1, num_envs));  // _needs_reset = True
+    }
+    DK_TRY(cudaMalloc((void **)&e->cur, sizeof(int32_t)));
+    DK_TRY(cudaMalloc((void **)&e->blocks_done, sizeof(uint32_t)));
+    DK_TRY(cudaMemset(e->cur, 0, sizeof(int32_t)));
+    DK_TRY(cudaMemset(e->blocks_done, 0, sizeof(uint32_t)));
+    DK_TRY(cudaMalloc((void **)&e->err_dev, sizeof(unsigned long long)));
+    DK_TRY(cudaHostAlloc((void **)&e->err_host, sizeof(unsigned long long), cudaHostAllocDefault));
+    DK_TRY(cudaMemset(e->err_dev, 0xff, sizeof(unsigned long long)));  // kNoError
+    *e->err_host = dk::kNoError;
+    DK_TRY(cudaStreamCreateWithFlags(&e->s_comp, cudaStreamNonBlocking));
+    DK_TRY(cudaStreamCreateWithFlags(&e->s_h2d, cudaStreamNonBlocking));
+    DK_TRY(cudaStreamCreateWithFlags(&e->s_d2h, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        DK_TRY(cudaEventCreateWithFlags(&e->ev_h2d[b], cudaEventDisableTiming));
+        DK_TRY(cudaEventCreateWithFlags(&e->ev_comp[b], cudaEventDisableTiming));
+        DK_TRY(cudaEventCreateWithFlags(&e->ev_d2h[b], cudaEventDisableTiming));
+    }
+    DK_TRY(cudaDeviceSynchronize());
+#undef DK_TRY
+    *out = e;
+    return DK_OK;
+}
+
+int dk_env_destroy(dk_env *e) {
+    if (!e) return DK_OK;
+    DeviceGuard g(e->device);
+    if (e->s_comp) cudaStreamSynchronize(e->s_comp);
+    if (e->s_h2d) cudaStreamSynchronize(e->s_h2d);
+    if (e->s_d2h) cudaStreamSynchronize(e->s_d2h);
+    free_scratch(e);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(e->state[b]);
+        cudaFree(e->steps[b]);
+        cudaFree(e->episode[b]);
+        cudaFree(e->needs_reset[b]);
+    }
+    cudaFree(e->cur);
+    cudaFree(e->blocks_done);
+    cudaFree(e->err_dev);
+    if (e->err_host) cudaFreeHost(e->err_host);
+    for (int b = 0; b < 2; ++b) {
+        if (e->ev_h2d[b]) cudaEventDestroy(e->ev_h2d[b]);
+        if (e->ev_comp[b]) cudaEventDestroy(e->ev_comp[b]);
+        if (e->ev_d2h[b]) cudaEventDestroy(e->ev_d2h[b]);
+    }
+    if (e->s_comp) cudaStreamDestroy(e->s_comp);
+    if (e->s_h2d) cudaStreamDestroy(e->s_h2d);
+    if (e->s_d2h) cudaStreamDestroy(e->s_d2h);
+    delete e;
+    return DK_OK;
+}
+
+int dk_env_reset(dk_env *e, int has_seed, uint64_t seed, void *obs_out, void *stream) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (has_seed) e->cfg.seed = seed;
+    DK_CUDA(cudaMemsetAsync(e->err_dev, 0xff, sizeof(unsigned long long), st));
+    DK_CUDA(cudaMemcpyAsync(e->err_host, e->err_dev, sizeof(unsigned long long),
+                            cudaMemcpyDeviceToHost, st));
+    const dk::EnvScalars sc = scalars(e, 1);
+    cudaError_t rc;
+    if (e->cfg.dtype == DK_F64)
+        rc = dk::launch_reset<double>(e->cfg.task, sc, to_params<double>(e->params),
+                                      worlds<double>(e), has_seed ? 1 : 0, (double *)obs_out, st,
+                                      &e->launches);
+    else
+        rc = dk::launch_reset<float>(e->cfg.task, sc, to_params<float>(e->params),
+                                     worlds<float>(e), has_seed ? 1 : 0, (float *)obs_out, st,
+                                     &e->launches);
+    if (rc != cudaSuccess) return fail(DK_ERR_CUDA, "reset launch: %s", cudaGetErrorString(rc));
+    return DK_OK;
+}
+
+int dk_env_step(dk_env *e, const void *actions, int autoreset, void *obs, void *reward,
+                uint8_t *done, uint8_t *trunc, void *term_obs, uint8_t *term_mask, void *info,
+                void *stream) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    return rollout_impl(e, 1, actions, autoreset, obs, reward, done, trunc, term_obs, term_mask,
+                        info, (cudaStream_t)stream);
+}
+
+int dk_env_rollout(dk_env *e, int64_t K, const void *actions, void *obs, void *reward,
+                   uint8_t *done, uint8_t *trunc, void *term_obs, uint8_t *term_mask, void *info,
+                   void *stream) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    return rollout_impl(e, K, actions, 1, obs, reward, done, trunc, term_obs, term_mask, info,
+                        (cudaStream_t)stream);
+}
+
+int dk_env_check_error(dk_env *e, void *stream, int64_t *step_index, int64_t *env_index) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    DK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    DK_CUDA(cudaStreamSynchronize(e->s_comp));
+    const unsigned long long key = *e->err_host;
+    if (key == dk::kNoError) return DK_OK;
+    *e->err_host = dk::kNoError;
+    DK_CUDA(cudaMemset(e->err_dev, 0xff, sizeof(unsigned long long)));
+    return decode_error(e, key, step_index, env_index);
+}
+
+int dk_env_reset_host(dk_env *e, int has_seed, uint64_t seed, void *obs_out) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    if (int rc = ensure_scratch(e, 1)) return rc;
+    if (int rc = dk_env_reset(e, has_seed, seed, e->hs.obs[0], e->s_comp)) return rc;
+    if (obs_out)
+        DK_CUDA(cudaMemcpyAsync(obs_out, e->hs.obs[0], (size_t)e->n * e->O * e->esz,
+                                cudaMemcpyDeviceToHost, e->s_comp));
+    DK_CUDA(cudaStreamSynchronize(e->s_comp));
+    return DK_OK;
+}
+
+int dk_env_step_host(dk_env *e, const void *actions, int autoreset, void *obs, void *reward,
+                     uint8_t *done, uint8_t *trunc, void *term_obs, uint8_t *term_mask,
+                     void *info) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    if (int rc = ensure_scratch(e, 1)) return rc;
+    cudaStream_t st = e->s_comp;
+    const size_t n = (size_t)e->n;
+    DK_CUDA(cudaMemcpyAsync(e->hs.actions[0], actions, n * e->A * e->esz, cudaMemcpyHostToDevice,
+                            st));
+    if (int rc = rollout_impl(e, 1, e->hs.actions[0], autoreset, e->hs.obs[0], e->hs.reward[0],
+                              e->hs.done[0], e->hs.trunc[0], e->hs.term[0], e->hs.mask[0],
+                              info ? e->hs.info[0] : nullptr, st))
+        return rc;
+    DK_CUDA(cudaMemcpyAsync(obs, e->hs.obs[0], n * e->O * e->esz, cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaMemcpyAsync(reward, e->hs.reward[0], n * e->esz, cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaMemcpyAsync(done, e->hs.done[0], n, cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaMemcpyAsync(trunc, e->hs.trunc[0], n, cudaMemcpyDeviceToHost, st));
+    if (info)
+        DK_CUDA(cudaMemcpyAsync(info, e->hs.info[0], n * e->I * e->esz, cudaMemcpyDeviceToHost,
+                                st));
+    std::vector<uint8_t> mask_local;
+    uint8_t *mask = term_mask;
+    if (term_obs && !mask) {
+        mask_local.resize(n);
+        mask = mask_local.data();
+    }
+    if (mask) DK_CUDA(cudaMemcpyAsync(mask, e->hs.mask[0], n, cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaStreamSynchronize(st));
+    int64_t ks, ki;
+    if (int rc = dk_env_check_error(e, st, &ks, &ki)) return rc;
+    if (term_obs) {
+        bool any = false;
+        for (size_t i = 0; i < n && !any; ++i) any = mask[i] != 0;
+        if (any) {
+            DK_CUDA(cudaMemcpy(term_obs, e->hs.term[0], n * e->O * e->esz,
+                               cudaMemcpyDeviceToHost));
+        }
+    }
+    return DK_OK;
+}
+
+int dk_env_rollout_host(dk_env *e, int64_t K, int64_t chunk, const void *actions, void *obs,
+                        void *reward, uint8_t *done, uint8_t *trunc, void *term_obs,
+                        uint8_t *term_mask, void *info) {
+    if (int rc = check_env(e)) return rc;
+    if (!actions || !obs || !reward || !done || !trunc)
+        return fail(DK_ERR_INVALID_INPUT, "actions, obs, reward, done and trunc are required");
+    if (K <= 0) return K == 0 ? DK_OK : fail(DK_ERR_INVALID_INPUT, "num_steps must be >= 0");
+    DeviceGuard g(e->device);
+    if (chunk <= 0 || chunk > K) chunk = K;
+    if (int rc = ensure_scratch(e, chunk)) return rc;
+    const size_t n = (size_t)e->n, es = e->esz;
+    const int64_t nchunks = (K + chunk - 1) / chunk;
+    std::vector<uint8_t> mask_local;
+    uint8_t *mask_host = term_mask;
+    if (term_obs && !mask_host) {
+        mask_local.resize((size_t)K * n);
+        mask_host = mask_local.data();
+    }
+    auto off = [&](int64_t j) { return (size_t)(j * chunk) * n; };  // rows before chunk j
+    auto steps_in = [&](int64_t j) { return (size_t)std::min<int64_t>(chunk, K - j * chunk); };
+
+    // Chunk j's term obs rows are fetched after the host has seen its mask.
+    auto finish_chunk = [&](int64_t j) -> int {
+        const int b = (int)(j & 1);
+        DK_CUDA(cudaEventSynchronize(e->ev_d2h[b]));
+        if (*e->err_host != dk::kNoError) return DK_OK;  // reported below
+        if (term_obs) {
+            const size_t rows = steps_in(j) * n;
+            const uint8_t *m = mask_host + off(j);
+            for (size_t k = 0; k < steps_in(j); ++k) {
+                bool any = false;
+                for (size_t i = 0; i < n && !any; ++i) any = m[k * n + i] != 0;
+                if (any)
+                    DK_CUDA(cudaMemcpyAsync((char *)term_obs + (off(j) + k * n) * e->O * es,
+                                            (char *)e->hs.term[b] + k * n * e->O * es,
+                                            n * e->O * es, cudaMemcpyDeviceToHost, e->s_d2h));
+            }
+            (void)rows;
+            DK_CUDA(cudaEventRecord(e->ev_d2h[b], e->s_d2h));
+        }
+        return DK_OK;
+    };
+
+    for (int64_t j = 0; j < nchunks; ++j) {
+        const int b = (int)(j & 1);
+        const size_t kj = steps_in(j), rows = kj * n;
+        if (j >= 2) {
+            if (int rc = finish_chunk(j - 2)) return rc;
+        }
+        // H2D of this chunk's actions once compute of chunk j-2 released the slot
+        if (j >= 2) DK_CUDA(cudaStreamWaitEvent(e->s_h2d, e->ev_comp[b], 0));
+        DK_CUDA(cudaMemcpyAsync(e->hs.actions[b], (const char *)actions + off(j) * e->A * es,
+                                rows * e->A * es, cudaMemcpyHostToDevice, e->s_h2d));
+        DK_CUDA(cudaEventRecord(e->ev_h2d[b], e->s_h2d));
+        // compute once the actions landed and the output slot was drained
+        DK_CUDA(cudaStreamWaitEvent(e->s_comp, e->ev_h2d[b], 0));
+        if (j >= 2) DK_CUDA(cudaStreamWaitEvent(e->s_comp, e->ev_d2h[b], 0));
+        if (int rc = rollout_impl(e, (int64_t)kj, e->hs.actions[b], 1, e->hs.obs[b],
+                                  e->hs.reward[b], e->hs.done[b], e->hs.trunc[b],
+                                  term_obs ? e->hs.term[b] : nullptr, e->hs.mask[b],
+                                  info ? e->hs.info[b] : nullptr, e->s_comp))
+            return rc;
+        DK_CUDA(cudaEventRecord(e->ev_comp[b], e->s_comp));
+        // D2H of the outputs
+        DK_CUDA(cudaStreamWaitEvent(e->s_d2h, e->ev_comp[b], 0));
+        DK_CUDA(cudaMemcpyAsync((char *)obs + off(j) * e->O * es, e->hs.obs[b], rows * e->O * es,
+                                cudaMemcpyDeviceToHost, e->s_d2h));
+        DK_CUDA(cudaMemcpyAsync((char *)reward + off(j) * es, e->hs.reward[b], rows * es,
+                                cudaMemcpyDeviceToHost, e->s_d2h));
+        DK_CUDA(cudaMemcpyAsync(done + off(j), e->hs.done[b], rows, cudaMemcpyDeviceToHost,
+                                e->s_d2h));
+        DK_CUDA(cudaMemcpyAsync(trunc + off(j), e->hs.trunc[b], rows, cudaMemcpyDeviceToHost,
+                                e->s_d2h));
+        if (mask_host)
+            DK_CUDA(cudaMemcpyAsync(mask_host + off(j), e->hs.mask[b], rows,
+                                    cudaMemcpyDeviceToHost, e->s_d2h));
+        if (info)
+            DK_CUDA(cudaMemcpyAsync((char *)info + off(j) * e->I * es, e->hs.info[b],
+                                    rows * e->I * es, cudaMemcpyDeviceToHost, e->s_d2h));
+        DK_CUDA(cudaEventRecord(e->ev_d2h[b], e->s_d2h));
+    }
+    for (int64_t j = std::max<int64_t>(0, nchunks - 2); j < nchunks; ++j)
+        if (int rc = finish_chunk(j)) return rc;
+    DK_CUDA(cudaStreamSynchronize(e->s_d2h));
+    int64_t ks = 0, ki = 0;
+    return dk_env_check_error(e, e->s_comp, &ks, &ki);
+}
+
+int dk_env_get_state(dk_env *e, double *state, double *target, int64_t *steps, int64_t *episode,
+                     uint8_t *needs_reset) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    cudaStream_t st = e->s_comp;
+    const size_t n = (size_t)e->n;
+    double *d_s = nullptr, *d_t = nullptr;
+    DK_CUDA(cudaMallocAsync((void **)&d_s, n * 4 * sizeof(double), st));
+    DK_CUDA(cudaMallocAsync((void **)&d_t, n * 2 * sizeof(double), st));
+    const dk::EnvScalars sc = scalars(e, 1);
+    cudaError_t rc = e->cfg.dtype == DK_F64
+                         ? dk::launch_get_state<double>(e->cfg.task, sc, worlds<double>(e), d_s,
+                                                        d_t, st)
+                         : dk::launch_get_state<float>(e->cfg.task, sc, worlds<float>(e), d_s,
+                                                       d_t, st);
+    if (rc != cudaSuccess) return fail(DK_ERR_CUDA, "get_state: %s", cudaGetErrorString(rc));
+    int32_t c = 0;
+    DK_CUDA(cudaMemcpyAsync(&c, e->cur, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaStreamSynchronize(st));
+    std::vector<int32_t> st32(n);
+    std::vector<uint32_t> ep32(n);
+    if (state) DK_CUDA(cudaMemcpyAsync(state, d_s, n * 4 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (target) DK_CUDA(cudaMemcpyAsync(target, d_t, n * 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaMemcpyAsync(st32.data(), e->steps[c], n * 4, cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaMemcpyAsync(ep32.data(), e->episode[c], n * 4, cudaMemcpyDeviceToHost, st));
+    if (needs_reset)
+        DK_CUDA(cudaMemcpyAsync(needs_reset, e->needs_reset[c], n, cudaMemcpyDeviceToHost, st));
+    DK_CUDA(cudaFreeAsync(d_s, st));
+    DK_CUDA(cudaFreeAsync(d_t, st));
+    DK_CUDA(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < n; ++i) {
+        if (steps) steps[i] = st32[i];
+        if (episode) episode[i] = ep32[i] == 0xffffffffu ? -1 : (int64_t)ep32[i];
+    }
+    return DK_OK;
+}
+
+int dk_env_set_state(dk_env *e, const double *state, const double *target, const int64_t *steps,
+                     const int64_t *episode, const uint8_t *needs_reset) {
+    if (int rc = check_env(e)) return rc;
+    DeviceGuard g(e->device);
+    cudaStream_t st = e->s_comp;
+    const size_t n = (size_t)e->n;
+    if (state || target) {
+        std::vector<double> s4(n * 4, 0.0), t2(n * 2, 0.0);
+        if (!state || !target) {  // keep the half that was not given
+            if (int rc = dk_env_get_state(e, s4.data(), t2.data(), nullptr, nullptr, nullptr))
+                return rc;
+        }
+        if (state) std::memcpy(s4.data(), state, n * 4 * sizeof(double));
+        if (target) std::memcpy(t2.data(), target, n * 2 * sizeof(double));
+        double *d_s = nullptr, *d_t = nullptr;
+        DK_CUDA(cudaMallocAsync((void **)&d_s, n * 4 * sizeof(double), st));
+        DK_CUDA(cudaMallocAsync((void **)&d_t, n * 2 * sizeof(double), st));
+        DK_CUDA(cudaMemcpyAsync(d_s, s4.data(), n * 4 * sizeof(double), cudaMemcpyHostToDevice, st));
+        DK_CUDA(cudaMemcpyAsync(d_t, t2.data(), n * 2 * sizeof(double), cudaMemcpyHostToDevice, st));
+        const dk::EnvScalars sc = scalars(e, 1);
+        cudaError_t rc = e->cfg.dtype == DK_F64
+                             ? dk::launch_set_state<double>(e->cfg.task, sc, worlds<double>(e),
+                                                            d_s, d_t, st)
+                             : dk::launch_set_state<float>(e->cfg.task, sc, worlds<float>(e), d_s,
+                                                           d_t, st);
+        if (rc != cudaSuccess) return fail(DK_ERR_CUDA, "set_state: %s", cudaGetErrorString(rc));
+        DK_CUDA(cudaFreeAsync(d_s, st));
+        DK_CUDA(cudaFreeAsync(d_t, st));
+        DK_CUDA(cudaStreamSynchronize(st));
+    }
+    int32_t c = 0;
+    DK_CUDA(cudaMemcpy(&c, e->cur, sizeof(int32_t), cudaMemcpyDeviceToHost));
+    if (steps) {
+        std::vector<int32_t> v(n);
+        for (size_t i = 0; i < n; ++i) v[i] = (int32_t)steps[i];
+        DK_CUDA(cudaMemcpy(e->steps[c], v.data(), n * 4, cudaMemcpyHostToDevice));
+    }
+    if (episode) {
+        std::vector<uint32_t> v(n);
+        for (size_t i = 0; i < n; ++i) v[i] = (uint32_t)(episode[i] & 0xffffffffLL);
+        DK_CUDA(cudaMemcpy(e->episode[c], v.data(), n * 4, cudaMemcpyHostToDevice));
+    }
+    if (needs_reset)
+        DK_CUDA(cudaMemcpy(e->needs_reset[c], needs_reset, n, cudaMemcpyHostToDevice));
+    return DK_OK;
+}
+
+int64_t dk_env_kernel_launches(const dk_env *e) { return e ? e->launches : 0; }
+
+}  // extern "C"

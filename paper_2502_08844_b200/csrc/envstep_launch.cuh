@@ -1,0 +1,122 @@
+// envstep_launch.cuh -- host-side launchers, explicitly instantiated per real
+// type in envstep_f32.cu / envstep_f64.cu (the f64 TU is compiled with
+// --fmad=false to keep the reference's two-rounding arithmetic).
+#pragma once
+#include "envstep_kernels.cuh"
+
+namespace dk {
+
+constexpr int kSms = 148;  // B200
+
+inline int pick_block(int64_t n) {
+    // Few worlds per GPU (1K-8K) is a latency-bound regime: spread warps over
+    // all 148 SMs before stacking them on one SM.
+    int bs = 256;
+    while (bs > 32 && (n + bs - 1) / bs < 2 * kSms) bs /= 2;
+    return bs;
+}
+
+template <class Task, typename T>
+inline cudaError_t launch_task_rollout(const T *actions, int64_t K, const EnvScalars &sc,
+                                       const Params<T> &p, const Worlds<T> &w,
+                                       const StepOut<T> &out, unsigned long long *err,
+                                       cudaStream_t st, int64_t *launches) {
+    const int bs = pick_block(sc.n);
+    const int64_t grid = (sc.n + bs - 1) / bs;
+    constexpr int R = Task::O > Task::I ? Task::O : Task::I;
+    constexpr int CH = Task::A > 1 ? 4 : 8;
+    rollout_kernel<Task, T, CH><<<(unsigned)grid, bs, bs * R * sizeof(T), st>>>(
+        actions, K, sc, p, w, out, err);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_rollout(int task, const T *actions, int64_t K, const EnvScalars &sc,
+                           const Params<T> &p, const Worlds<T> &w, const StepOut<T> &out,
+                           unsigned long long *err, cudaStream_t st, int64_t *launches) {
+    switch (task) {
+    case 0: return launch_task_rollout<Pendulum<T>, T>(actions, K, sc, p, w, out, err, st, launches);
+    case 1: return launch_task_rollout<Cartpole<T>, T>(actions, K, sc, p, w, out, err, st, launches);
+    case 2: return launch_task_rollout<Acrobot<T>, T>(actions, K, sc, p, w, out, err, st, launches);
+    default: return launch_task_rollout<Reacher<T>, T>(actions, K, sc, p, w, out, err, st, launches);
+    }
+}
+
+template <class Task, typename T>
+inline cudaError_t launch_task_reset(const EnvScalars &sc, const Params<T> &p, const Worlds<T> &w,
+                                     int rewind, T *obs, cudaStream_t st, int64_t *launches) {
+    const int bs = pick_block(sc.n);
+    const int64_t grid = (sc.n + bs - 1) / bs;
+    reset_kernel<Task, T><<<(unsigned)grid, bs, bs * Task::O * sizeof(T), st>>>(sc, p, w, rewind,
+                                                                               obs);
+    *launches += 1;
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_reset(int task, const EnvScalars &sc, const Params<T> &p, const Worlds<T> &w,
+                         int rewind, T *obs, cudaStream_t st, int64_t *launches) {
+    switch (task) {
+    case 0: return launch_task_reset<Pendulum<T>, T>(sc, p, w, rewind, obs, st, launches);
+    case 1: return launch_task_reset<Cartpole<T>, T>(sc, p, w, rewind, obs, st, launches);
+    case 2: return launch_task_reset<Acrobot<T>, T>(sc, p, w, rewind, obs, st, launches);
+    default: return launch_task_reset<Reacher<T>, T>(sc, p, w, rewind, obs, st, launches);
+    }
+}
+
+template <typename T>
+cudaError_t launch_get_state(int task, const EnvScalars &sc, const Worlds<T> &w, double *s4,
+                             double *t2, cudaStream_t st) {
+    const int bs = 128;
+    const unsigned grid = (unsigned)((sc.n + bs - 1) / bs);
+    switch (task) {
+    case 0: get_state_kernel<Pendulum<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    case 1: get_state_kernel<Cartpole<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    case 2: get_state_kernel<Acrobot<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    default: get_state_kernel<Reacher<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    }
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_set_state(int task, const EnvScalars &sc, const Worlds<T> &w, const double *s4,
+                             const double *t2, cudaStream_t st) {
+    const int bs = 128;
+    const unsigned grid = (unsigned)((sc.n + bs - 1) / bs);
+    switch (task) {
+    case 0: set_state_kernel<Pendulum<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    case 1: set_state_kernel<Cartpole<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    case 2: set_state_kernel<Acrobot<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    default: set_state_kernel<Reacher<T>, T><<<grid, bs, 0, st>>>(sc, w, s4, t2); break;
+    }
+    return cudaGetLastError();
+}
+
+// Explicit instantiation declarations (definitions in envstep_f32.cu / _f64.cu).
+#define DK_DECLARE_LAUNCHERS(T)                                                                  \
+    extern template cudaError_t launch_rollout<T>(int, const T *, int64_t, const EnvScalars &,   \
+                                                  const Params<T> &, const Worlds<T> &,          \
+                                                  const StepOut<T> &, unsigned long long *,      \
+                                                  cudaStream_t, int64_t *);                      \
+    extern template cudaError_t launch_reset<T>(int, const EnvScalars &, const Params<T> &,      \
+                                                const Worlds<T> &, int, T *, cudaStream_t,       \
+                                                int64_t *);                                      \
+    extern template cudaError_t launch_get_state<T>(int, const EnvScalars &, const Worlds<T> &,  \
+                                                    double *, double *, cudaStream_t);           \
+    extern template cudaError_t launch_set_state<T>(int, const EnvScalars &, const Worlds<T> &,  \
+                                                    const double *, const double *, cudaStream_t);
+
+#define DK_INSTANTIATE_LAUNCHERS(T)                                                              \
+    template cudaError_t launch_rollout<T>(int, const T *, int64_t, const EnvScalars &,          \
+                                           const Params<T> &, const Worlds<T> &,                 \
+                                           const StepOut<T> &, unsigned long long *,             \
+                                           cudaStream_t, int64_t *);                             \
+    template cudaError_t launch_reset<T>(int, const EnvScalars &, const Params<T> &,             \
+                                         const Worlds<T> &, int, T *, cudaStream_t, int64_t *);  \
+    template cudaError_t launch_get_state<T>(int, const EnvScalars &, const Worlds<T> &,         \
+                                             double *, double *, cudaStream_t);                  \
+    template cudaError_t launch_set_state<T>(int, const EnvScalars &, const Worlds<T> &,         \
+                                             const double *, const double *, cudaStream_t);
+
+}  // namespace dk

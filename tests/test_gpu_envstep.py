@@ -1,0 +1,259 @@
+"""GPU parity of the B200 env step against the reference (golden fixtures) and
+the C oracle, through the C ABI (libdeskrl_b200.so).
+
+Tolerances (BASELINE.md "Parity"):
+  * flags, step / episode counters, truncation and autoreset placement: exact;
+  * float64 build: reset states bit-exact; trajectories within 1e-9 relative
+    (the only differences are CUDA vs glibc sin/cos/exp ulps, amplified by the
+    chaotic dynamics over the horizon);
+  * float32 build: 1 step within 1e-5 relative, <=100 steps within 1e-3
+    relative, both with an absolute floor of 1e-3 (chaotic divergence beyond
+    ~200 steps is checked statistically instead).
+"""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+TASKS = ["pendulum-swingup", "cartpole-balance", "acrobot-swingup", "reacher-easy"]
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_08844_b200 as p
+
+    return p
+
+
+def _close(got, want, rtol, floor):
+    got = np.asarray(got, dtype=np.float64)
+    want = np.asarray(want, dtype=np.float64)
+    err = np.abs(got - want) / np.maximum(np.abs(want), floor)
+    return float(err.max()) if err.size else 0.0
+
+
+def _traj_names(golden):
+    return sorted({k.split("/")[1] for k in golden.files if k.startswith("traj/")})
+
+
+def _make_params(pkg, kind):
+    if kind == "damped":
+        return pkg.DynamicsParams(link_damping=0.1, link2_mass=1.3, elbow_torque_limit=6.0)
+    return None
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_golden_trajectories(golden, pkg, dtype):
+    """BatchEnv (drop-in numpy API) replays the reference's own trajectories."""
+    tol_step = 1e-9 if dtype == "float64" else 1e-3
+    for name in _traj_names(golden):
+        g = lambda k: golden[f"traj/{name}/{k}"]  # noqa: E731
+        dt = float(g("meta_dt"))
+        cfg = pkg.EnvConfig(task=str(g("meta_task")), episode_length=int(g("meta_ep_len")),
+                            action_repeat=int(g("meta_rep")), dt=None if dt < 0 else dt,
+                            wide_init=bool(g("meta_wide")))
+        env = pkg.BatchEnv(cfg, int(g("meta_n")), params=_make_params(pkg, str(g("meta_params"))),
+                           dtype=dtype)
+        obs0 = env.reset(seed=int(g("meta_seed")))
+        assert _close(obs0["state"], g("obs0"), 0, 1e-3) < (1e-12 if dtype == "float64" else 1e-6)
+        acts = g("acts")
+        for k in range(acts.shape[0]):
+            if k == int(g("mid_reset_step")):
+                o = env.reset()
+                assert _close(o["state"], g("obs_mid_reset"), 0, 1e-3) < tol_step
+            obs, rew, done, trunc, infos = env.step(acts[k])
+            assert obs["state"].dtype == np.float64 and obs["state"].shape == g("obs")[k].shape
+            np.testing.assert_array_equal(obs["state"], obs["privileged_state"])
+            assert _close(obs["state"], g("obs")[k], 0, 1e-3) < tol_step, (name, k)
+            assert _close(rew, g("rew")[k], 0, 1e-3) < tol_step, (name, k)
+            np.testing.assert_array_equal(done, g("done")[k])
+            np.testing.assert_array_equal(trunc, g("trunc")[k])
+            mask = np.array(["terminal_observation" in inf for inf in infos])
+            np.testing.assert_array_equal(mask, g("term_mask")[k])
+            for i in np.nonzero(mask)[0]:
+                t = infos[i]["terminal_observation"]
+                assert _close(t["state"], g("term_obs")[k][i], 0, 1e-3) < tol_step
+            info = np.array([[v for kk, v in inf.items() if kk != "terminal_observation"]
+                             for inf in infos])
+            assert _close(info, g("info")[k], 0, 1e-3) < tol_step
+        s, t, steps, ep, nr = env._h.get_state()
+        np.testing.assert_array_equal(steps, g("final_steps"))
+        np.testing.assert_array_equal(ep, g("final_episode"))
+        assert _close(s, g("final_state"), 0, 1e-3) < tol_step
+        env.close()
+
+
+@pytest.mark.parametrize("task", TASKS)
+def test_reset_states_match_philox_oracle(pkg, oracle, task):
+    n = 4096
+    env = pkg.DeviceBatchEnv(pkg.EnvConfig(task=task, wide_init=task == "pendulum-swingup"), n,
+                             dtype="float64", env_index_offset=12345)
+    env.reset(seed=987654321)
+    s, t, steps, ep, nr = env.state()
+    ref = oracle.OracleBatchEnv(task, n, wide_init=task == "pendulum-swingup", env_offset=12345)
+    ref.reset(seed=987654321)
+    np.testing.assert_array_equal(s, ref.state)  # Philox + uniform: bit-exact
+    if task == "reacher-easy":  # target = radius * (cos, sin): CUDA vs glibc trig ulp
+        np.testing.assert_allclose(t, ref.target, rtol=0, atol=4e-16)
+    assert (steps == 0).all() and (ep == 0).all() and not nr.any()
+    # float32: exactly the float64 draw rounded to nearest
+    env32 = pkg.DeviceBatchEnv(pkg.EnvConfig(task=task, wide_init=task == "pendulum-swingup"), n,
+                               dtype="float32", env_index_offset=12345)
+    env32.reset(seed=987654321)
+    s32, *_ = env32.state()
+    np.testing.assert_array_equal(s32, ref.state.astype(np.float32).astype(np.float64))
+
+
+def _oracle_rollout(oracle, task, n, K, seed, acts, **kw):
+    ref = oracle.OracleBatchEnv(task, n, **kw)
+    ref.reset(seed=seed)
+    return ref, ref.rollout(acts)
+
+
+@pytest.mark.parametrize("task", TASKS)
+def test_rollout_vs_oracle_f64(pkg, oracle, task):
+    n, K, seed = 8192, 100, 3
+    rng = np.random.default_rng(5)
+    acts = rng.uniform(-1.2, 1.2, (K, n, 2 if task == "reacher-easy" else 1))
+    ref, (obs, rew, done, trunc, term, mask, info) = _oracle_rollout(
+        oracle, task, n, K, seed, acts, episode_length=37, action_repeat=2)
+    env = pkg.DeviceBatchEnv(pkg.EnvConfig(task=task, episode_length=37, action_repeat=2), n,
+                             dtype="float64")
+    env.reset(seed=seed)
+    out = env.rollout(torch.as_tensor(acts, device="cuda"), with_info=True)
+    env.check()
+    np.testing.assert_array_equal(out["trunc"].cpu().numpy(), trunc)
+    np.testing.assert_array_equal(out["done"].cpu().numpy(), done)
+    np.testing.assert_array_equal(out["terminal_mask"].cpu().numpy(), mask)
+    assert _close(out["obs"].cpu().numpy(), obs, 0, 1e-3) < 1e-9
+    assert _close(out["reward"].cpu().numpy(), rew, 0, 1e-3) < 1e-9
+    assert _close(out["info"].cpu().numpy(), info, 0, 1e-3) < 1e-9
+    m = mask
+    assert _close(out["terminal_obs"].cpu().numpy()[m], term[m], 0, 1e-3) < 1e-9
+    s, t, steps, ep, nr = env.state()
+    np.testing.assert_array_equal(steps, ref.steps)
+    np.testing.assert_array_equal(ep, ref.episode)
+
+
+@pytest.mark.parametrize("task", TASKS)
+def test_rollout_vs_oracle_f32(pkg, oracle, task):
+    n, K, seed = 8192, 100, 11
+    rng = np.random.default_rng(6)
+    acts = rng.uniform(-1, 1, (K, n, 2 if task == "reacher-easy" else 1))
+    ref, (obs, rew, done, trunc, term, mask, info) = _oracle_rollout(
+        oracle, task, n, K, seed, acts, episode_length=1000)
+    env = pkg.DeviceBatchEnv(pkg.EnvConfig(task=task), n, dtype="float32")
+    env.reset(seed=seed)
+    out = env.rollout(torch.as_tensor(acts, device="cuda", dtype=torch.float32), with_info=True)
+    env.check()
+    got = out["obs"].cpu().numpy()
+    e1 = _close(got[0], obs[0], 0, 1e-3)
+    e100 = _close(got, obs, 0, 1e-3)
+    assert e1 < 1e-5, e1
+    assert e100 < 1e-3, e100
+    assert _close(out["reward"].cpu().numpy(), rew, 0, 1e-3) < 1e-3
+    np.testing.assert_array_equal(out["trunc"].cpu().numpy(), trunc)
+
+
+def test_full_episode_statistics_f32(pkg, oracle):
+    """1000 steps (one full episode + autoreset) at 8192 worlds, float32:
+    counters exact, trajectories compared statistically after chaos sets in."""
+    n, K = 8192, 1001
+    acts = np.random.default_rng(0).uniform(-1, 1, (K, n, 1))
+    ref, (obs, rew, done, trunc, term, mask, info) = _oracle_rollout(
+        oracle, "cartpole-balance", n, K, 0, acts)
+    env = pkg.DeviceBatchEnv(pkg.EnvConfig(), n, dtype="float32")
+    env.reset(seed=0)
+    out = env.rollout(torch.as_tensor(acts, device="cuda", dtype=torch.float32))
+    env.check()
+    tr = out["trunc"].cpu().numpy()
+    np.testing.assert_array_equal(tr, trunc)
+    assert tr[999].all() and tr.sum() == n
+    # reset obs after the autoreset is a fresh Philox draw: matches again
+    got = out["obs"].cpu().numpy()
+    assert _close(got[999], obs[999], 0, 1e-3) < 1e-5
+    r = out["reward"].cpu().numpy()
+    assert abs(r.mean() - rew.mean()) < 2e-3 * max(1.0, abs(rew.mean()))
+    s, t, steps, ep, nr = env.state()
+    np.testing.assert_array_equal(steps, ref.steps)
+    np.testing.assert_array_equal(ep, ref.episode)
+
+
+def test_step_equals_rollout_and_sharding(pkg):
+    """K single steps == one K-step rollout; two shards == one device run."""
+    n, K = 1000, 25
+    acts = torch.rand((K, n, 1), device="cuda", dtype=torch.float64) * 2 - 1
+    cfg = pkg.EnvConfig(task="cartpole-balance", episode_length=10)
+    a = pkg.DeviceBatchEnv(cfg, n, dtype="float64")
+    a.reset(seed=4)
+    ro = a.rollout(acts, with_info=True)
+    b = pkg.DeviceBatchEnv(cfg, n, dtype="float64")
+    b.reset(seed=4)
+    for k in range(K):
+        o = b.step(acts[k])
+        assert torch.equal(o["obs"], ro["obs"][k])
+        assert torch.equal(o["reward"], ro["reward"][k])
+        assert torch.equal(o["trunc"], ro["trunc"][k])
+        assert torch.equal(o["info"], ro["info"][k])
+    shards = [pkg.DeviceBatchEnv(cfg, n // 2, dtype="float64", env_index_offset=r * (n // 2))
+              for r in range(2)]
+    for s in shards:
+        s.reset(seed=4)
+    parts = [s.rollout(acts[:, r * (n // 2):(r + 1) * (n // 2)].contiguous())
+             for r, s in enumerate(shards)]
+    assert torch.equal(torch.cat([p["obs"] for p in parts], 1), ro["obs"])
+    assert torch.equal(torch.cat([p["reward"] for p in parts], 1), ro["reward"])
+
+
+def test_errors_are_batch_atomic(pkg):
+    env = pkg.BatchEnv(pkg.EnvConfig(task="cartpole-balance", episode_length=2), 64)
+    with pytest.raises(pkg.UsageError, match="environment must be reset before stepping"):
+        env.step(np.zeros((64, 1)))
+    env.reset(seed=0)
+    before = env._h.get_state()
+    a = np.zeros((64, 1))
+    a[17, 0] = np.nan
+    with pytest.raises(pkg.InvalidInputError, match="action contains non-finite values"):
+        env.step(a)
+    after = env._h.get_state()
+    for x, y in zip(before, after):
+        np.testing.assert_array_equal(x, y)  # nothing was stepped
+    with pytest.raises(pkg.InvalidInputError, match="actions batch size mismatch"):
+        env.step(np.zeros((63, 1)))
+    env.step(np.zeros((64, 1)), autoreset=False)
+    _, _, _, tr, infos = env.step(np.zeros((64, 1)), autoreset=False)
+    assert tr.all() and all("terminal_observation" not in i for i in infos)
+    with pytest.raises(pkg.UsageError):
+        env.step(np.zeros((64, 1)), autoreset=False)
+    env.reset()
+    env.step(np.zeros((64, 1)))  # usable again after reset
+    # device API: the error surfaces at check(), the worlds stay untouched
+    d = pkg.DeviceBatchEnv(pkg.EnvConfig(), 256, dtype="float32")
+    d.reset(seed=1)
+    bad = torch.zeros((8, 256, 1), device="cuda")
+    bad[5, 200, 0] = float("inf")
+    d.rollout(bad)
+    with pytest.raises(pkg.InvalidInputError) as e:
+        d.check()
+    assert (e.value.step_index, e.value.env_index) == (5, 200)
+    s, t, steps, ep, nr = d.state()
+    assert (steps == 0).all()
+
+
+def test_drop_in_surface(pkg):
+    env = pkg.BatchEnv(pkg.EnvConfig(task="reacher-easy"), 8, num_workers=4)
+    assert env.num_envs == 8 and env.action_dim == 2
+    obs = env.reset(seed=3)
+    assert set(obs) == {"state", "privileged_state"} and obs["state"].shape == (8, 10)
+    assert env.envs[0].observation_shapes() == {"state": (10,), "privileged_state": (10,)}
+    assert len(env.envs[3].state) == 4
+    o, r, d, t, infos = env.step(np.zeros((8, 2)))
+    assert r.dtype == np.float64 and d.dtype == bool and t.dtype == bool
+    assert set(infos[0]) == {"distance"}
+    assert env.kernel_launches > 0
+    env.close()
