@@ -21,12 +21,17 @@ inline cudaError_t launch_task_rollout(const T *actions, int64_t K, const EnvSca
                                        const Params<T> &p, const Worlds<T> &w,
                                        const StepOut<T> &out, unsigned long long *err,
                                        cudaStream_t st, int64_t *launches) {
-    const int bs = pick_block(sc.n);
-    const int64_t grid = (sc.n + bs - 1) / bs;
-    constexpr int R = Task::O > Task::I ? Task::O : Task::I;
-    constexpr int CH = Task::A > 1 ? 4 : 8;
-    rollout_kernel<Task, T, CH><<<(unsigned)grid, bs, bs * R * sizeof(T), st>>>(
-        actions, K, sc, p, w, out, err);
+    using S = RolloutShape<Task, T>;
+    auto kern = rollout_kernel<Task, T>;
+    static bool attr_set = false;  // per instantiation; opt in above 48 KB once
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)S::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int64_t grid = (sc.n + 31) / 32;  // one block per tile of 32 worlds
+    kern<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(actions, K, sc, p, w, out, err);
     *launches += 1;
     return cudaGetLastError();
 }

@@ -49,7 +49,8 @@ struct Pendulum {
     static __device__ __forceinline__ void step(W &w, const T *a, const Params<T> &p) {
         const T torque = clip_sym(a[0] * p.pend_torque_limit, p.pend_torque_limit);
         const T m = p.pend_mass, l = p.pend_length;
-        const T accel = (torque - p.pend_damping * w.om - m * p.gravity * l * w.s) / (m * l * l);
+        const T accel =
+            RealOps<T>::div_(torque - p.pend_damping * w.om - m * p.gravity * l * w.s, m * l * l);
         w.om = w.om + p.dt * accel;
         w.th = w.th + p.dt * w.om;
         refresh(w);
@@ -60,7 +61,7 @@ struct Pendulum {
         return r;
     }
     static __device__ __forceinline__ void obs(const W &w, const Params<T> &, T *o) {
-        o[0] = w.c; o[1] = w.s; o[2] = w.om / T(10.0);
+        o[0] = w.c; o[1] = w.s; o[2] = RealOps<T>::div_(w.om, T(10.0));
     }
     static __device__ __forceinline__ void sample(W &w, Philox4x64 &rng, const Params<T> &,
                                                   bool wide) {
@@ -105,8 +106,8 @@ struct Cartpole {
         const T r1 = force + mp * l * w.thd * w.thd * w.s;
         const T r2 = mp * g * l * w.s;
         const T det = m11 * m22 - m12 * m12;
-        const T xddot = (m22 * r1 - m12 * r2) / det;
-        const T thetaddot = (m11 * r2 - m12 * r1) / det;
+        const T xddot = RealOps<T>::div_(m22 * r1 - m12 * r2, det);
+        const T thetaddot = RealOps<T>::div_(m11 * r2 - m12 * r1, det);
         w.xd = w.xd + p.dt * xddot;
         w.thd = w.thd + p.dt * thetaddot;
         w.x = w.x + p.dt * w.xd;
@@ -176,8 +177,8 @@ __device__ __forceinline__ void twolink_advance(TwoLinkW<T> &w, T tau1, T tau2, 
     const T rhs1 = tau1 - cor1 - g1 - p.link_damping * d1;
     const T rhs2 = tau2 - cor2 - g2 - p.link_damping * d2;
     const T det = m11 * m22 - m12 * m12;
-    const T a1 = (m22 * rhs1 - m12 * rhs2) / det;
-    const T a2 = (m11 * rhs2 - m12 * rhs1) / det;
+    const T a1 = RealOps<T>::div_(m22 * rhs1 - m12 * rhs2, det);
+    const T a2 = RealOps<T>::div_(m11 * rhs2 - m12 * rhs1, det);
     w.d1 = d1 + p.dt * a1;
     w.d2 = d2 + p.dt * a2;
     w.t1 = w.t1 + p.dt * w.d1;
@@ -205,13 +206,13 @@ struct Acrobot {
     }
     static __device__ __forceinline__ T reward(const W &w, const Params<T> &p, T *info) {
         const T tip_y = -(p.link1_length * w.c1 + p.link2_length * w.c12);
-        const T height = tip_y / (p.link1_length + p.link2_length);
+        const T height = RealOps<T>::div_(tip_y, p.link1_length + p.link2_length);
         info[0] = height;
         return tol<T>(height, T(0.95), T(1.0), T(1.0));
     }
     static __device__ __forceinline__ void obs(const W &w, const Params<T> &, T *o) {
         o[0] = w.c1; o[1] = w.s1; o[2] = w.c2; o[3] = w.s2;
-        o[4] = w.d1 / T(10.0); o[5] = w.d2 / T(10.0);
+        o[4] = RealOps<T>::div_(w.d1, T(10.0)); o[5] = RealOps<T>::div_(w.d2, T(10.0));
     }
     static __device__ __forceinline__ void sample(W &w, Philox4x64 &rng, const Params<T> &, bool) {
         w.t1 = (T)rng.uniform(-0.1, 0.1);
@@ -263,7 +264,7 @@ struct Reacher {
         T x, y;
         tip(w, p, x, y);
         o[0] = w.c1; o[1] = w.s1; o[2] = w.c2; o[3] = w.s2;
-        o[4] = w.d1 / T(10.0); o[5] = w.d2 / T(10.0);
+        o[4] = RealOps<T>::div_(w.d1, T(10.0)); o[5] = RealOps<T>::div_(w.d2, T(10.0));
         o[6] = w.tx; o[7] = w.ty; o[8] = w.tx - x; o[9] = w.ty - y;
     }
     static __device__ __forceinline__ void sample(W &w, Philox4x64 &rng, const Params<T> &, bool) {

@@ -1,8 +1,5 @@
-set -x
 cd $GRAFT_REPO_ROOT
-nvidia-smi > gpurun_out/smi.txt 2>&1
-nproc > gpurun_out/nproc.txt
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
-timeout 900 python -m pytest tests -m gpu -q -x > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --steps 20000 --warmup 2000 --cpu-seconds 5 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
-timeout 600 python bench.py --dtype float64 --steps 20000 --warmup 2000 --no-cpu > gpurun_out/bench64.json 2> gpurun_out/bench64.err
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 20000 --warmup 2000 --cpu-seconds 3 > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?" >> gpurun_out/bench.err
+timeout 600 python bench.py --dtype float64 --steps 20000 --warmup 2000 --no-cpu --e2e-steps 0 > gpurun_out/bench64.json 2> gpurun_out/bench64.err
