@@ -141,6 +141,7 @@ int rollout_impl(dk_env *e, int64_t K, const void *actions, int autoreset, void 
     if (!actions || !obs || !reward || !done || !trunc)
         return fail(DK_ERR_INVALID_INPUT, "actions, obs, reward, done and trunc are required");
     if (K < 0) return fail(DK_ERR_INVALID_INPUT, "num_steps must be >= 0");
+    if (K > 0x7fffffffLL) return fail(DK_ERR_INVALID_INPUT, "num_steps must be < 2^31 per call");
     if (K == 0) return DK_OK;
     const dk::EnvScalars sc = scalars(e, autoreset);
     cudaError_t rc;

@@ -101,8 +101,8 @@ __device__ __forceinline__ void finish_launch(int32_t *cur, uint32_t *blocks_don
     }
 }
 
-__device__ __forceinline__ void record_error(unsigned long long *err, int64_t k, int64_t n,
-                                             int64_t i, int code) {
+static __device__ __noinline__ void record_error(unsigned long long *err, int64_t k, int64_t n,
+                                          int64_t i, int code) {
     const unsigned long long key = ((unsigned long long)(k * n + i) << 2) | (unsigned long long)code;
     atomicMin(err, key);
 }
@@ -194,6 +194,24 @@ struct RolloutShape {
 };
 
 template <class Task, typename T>
+__device__ __forceinline__ void world_to_slot(const typename Task::W &w, T *slot, int lane);
+
+// Environment.reset (envkit.py:502-519) of one world inside a rollout: the
+// next Philox stream of (seed, env, episode) -> sample_initial.  Out of line:
+// taken once per episode_length steps.
+template <class Task, typename T>
+__device__ __noinline__ typename Task::W autoreset_world(uint64_t seed, uint64_t gidx,
+                                                         uint32_t episode, Params<T> p, int wide,
+                                                         T *post_slot, int lane) {
+    typename Task::W wd;
+    Philox4x64 rng;
+    rng.init(seed, gidx, episode, 0);
+    Task::sample(wd, rng, p, wide != 0);
+    world_to_slot<Task, T>(wd, post_slot, lane);
+    return wd;
+}
+
+template <class Task, typename T>
 __device__ __forceinline__ void world_to_slot(const typename Task::W &w, T *slot, int lane) {
     constexpr int WF = RolloutShape<Task, T>::WF;
     const T *f = reinterpret_cast<const T *>(&w);
@@ -209,7 +227,7 @@ __device__ __forceinline__ void slot_to_world(typename Task::W &w, const T *slot
     for (int j = 0; j < WF; ++j) f[j] = slot[j * 32 + lane];
 }
 
-template <class Task, typename T>
+template <class Task, typename T, bool R1>
 __global__ void __launch_bounds__(RolloutShape<Task, T>::THREADS)
 rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T> p, Worlds<T> w,
                StepOut<T> out, unsigned long long *err) {
@@ -238,7 +256,7 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
 #pragma unroll
         for (int d = 0; d < D; ++d) {
             mbar_init(&full[d], 32);
-            mbar_init(&empty[d], 32);
+            mbar_init(&empty[d], 32);  // consumer warp 0 pre-arms every slot once (below)
         }
     }
     __syncthreads();
@@ -284,56 +302,62 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         // I-cache footprint) and the dependent chain never waits on HBM
         constexpr int P = S::P;
         T *aring = reinterpret_cast<T *>(smem + S::OFF_ACT);  // [P][32][A]
-        auto issue = [&](int64_t k) {
-            const bool v = in_range && k < K;
-            cp_async_ca<A * sizeof(T)>(aring + ((int)(k % P) * 32 + lane) * A,
-                                       actions + (v ? (k * n + i) * A : 0), v);
-            cp_async_commit();
-        };
+        const int K32 = (int)K;  // host guarantees K < 2^31
+        const T *aptr = actions + (in_range ? i * A : 0);
+        const int64_t astep = in_range ? n * A : 0;
 #pragma unroll 1
-        for (int64_t k = 0; k < P; ++k) issue(k);
+        for (int k = 0; k < P; ++k) {
+            cp_async_ca<A * sizeof(T)>(aring + (k * 32 + lane) * A, aptr + k * astep,
+                                       in_range && k < K32);
+            cp_async_commit();
+        }
+        const T *anext = aptr + P * astep;
+        const int ku = k_usage < K ? (int)k_usage : K32;
+        uint32_t phase_bits = 0;  // bit d: parity of the next empty[d] completion to wait for
 
 #pragma unroll 1
-        for (int64_t k = 0; k < K; ++k) {
-            const int slot = (int)(k % D);
-            const uint32_t use = (uint32_t)(k / D);
+        for (int k = 0; k < K32; ++k) {
+            const int slot = k & (D - 1);
+            const int ar = k & (P - 1);
             cp_async_wait<P - 1>();  // this lane's copy for step k has landed
             T a[A];
             bool fin = true;
 #pragma unroll
             for (int j = 0; j < A; ++j) {  // min(max(float(a), -1.0), 1.0)  (envkit.py:532)
-                T v = aring[((int)(k % P) * 32 + lane) * A + j];
+                T v = aring[(ar * 32 + lane) * A + j];
                 fin &= RealOps<T>::finite_(v);
-                if (T(-1) > v) v = T(-1);
-                if (T(1) < v) v = T(1);
-                a[j] = v;
+                a[j] = fmin(fmax(v, T(-1)), T(1));
             }
-            issue(k + P);
-            if (__builtin_expect(!fin && ok && in_range && k < k_usage, 0)) {  // envkit.py:529-531
+            cp_async_ca<A * sizeof(T)>(aring + (ar * 32 + lane) * A, anext,
+                                       in_range && k + P < K32);
+            cp_async_commit();
+            anext += astep;
+            if (__builtin_expect(!fin && ok && in_range && k < ku, 0)) {  // envkit.py:529-531
                 ok = false;
                 record_error(err, k, n, i, kErrInvalid);
             }
             T rp = T(0);
             Task::step(wd, a, p);
-            for (int rep = 1; rep < sc.action_repeat; ++rep) {
-                T inf[I];
-                rp += Task::reward(wd, p, inf);
-                Task::step(wd, a, p);
+            if (!R1) {
+                for (int rep = 1; rep < sc.action_repeat; ++rep) {
+                    T inf[I];
+                    rp += Task::reward(wd, p, inf);
+                    Task::step(wd, a, p);
+                }
             }
             steps += 1;
             const bool truncated = steps >= sc.episode_length;
             const bool reset = truncated && sc.autoreset && in_range;
-            if (use > 0) mbar_wait(&empty[slot], (use - 1) & 1u);
+            mbar_wait(&empty[slot], (phase_bits >> slot) & 1u);
+            phase_bits ^= 1u << slot;
             world_to_slot<Task, T>(wd, ring + (size_t)slot * WF * 32, lane);
-            rpart[slot * 32 + lane] = rp;
+            if (!R1) rpart[slot * 32 + lane] = rp;
             flags[slot * 32 + lane] = (uint8_t)((truncated ? 1 : 0) | (reset ? 2 : 0));
             if (__builtin_expect(reset, 0)) {
-                episode += 1;  // Environment.reset (envkit.py:502-519)
-                Philox4x64 rng;
-                rng.init(sc.seed, gidx, episode, 0);
-                Task::sample(wd, rng, p, sc.wide_init != 0);
+                episode += 1;
                 steps = 0;
-                world_to_slot<Task, T>(wd, post + (size_t)slot * WF * 32, lane);
+                wd = autoreset_world<Task, T>(sc.seed, gidx, episode, p, sc.wide_init,
+                                              post + (size_t)slot * WF * 32, lane);
             }
             mbar_arrive(&full[slot]);
         }
@@ -350,19 +374,24 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         const int c = warp - 1;
         T *tile = reinterpret_cast<T *>(smem + S::OFF_TILE) + (size_t)c * 32 * S::R;
         const T inv_rep = T(sc.action_repeat);
+        if (c == 0) {
+#pragma unroll
+            for (int d = 0; d < D; ++d) mbar_arrive(&empty[d]);  // slots start free
+        }
         for (int64_t k = c; k < K; k += M) {
             const int slot = (int)(k % D);
             mbar_wait(&full[slot], (uint32_t)(k / D) & 1u);
             typename Task::W wd, wp;
             slot_to_world<Task, T>(wd, ring + (size_t)slot * WF * 32, lane);
-            const T rp = rpart[slot * 32 + lane];
+            const T rp = R1 ? T(0) : rpart[slot * 32 + lane];
             const uint8_t fl = flags[slot * 32 + lane];
             const bool reset = (fl & 2) != 0;
             if (reset) slot_to_world<Task, T>(wp, post + (size_t)slot * WF * 32, lane);
             mbar_arrive(&empty[slot]);
 
             T info[I];
-            const T r = (rp + Task::reward(wd, p, info)) / inv_rep;
+            const T r = R1 ? (T(0) + Task::reward(wd, p, info))
+                           : (rp + Task::reward(wd, p, info)) / inv_rep;
             T o[O];
             Task::obs(wd, p, o);
             const int64_t ko = k * n;

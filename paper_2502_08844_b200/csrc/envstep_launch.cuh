@@ -22,12 +22,14 @@ inline cudaError_t launch_task_rollout(const T *actions, int64_t K, const EnvSca
                                        const StepOut<T> &out, unsigned long long *err,
                                        cudaStream_t st, int64_t *launches) {
     using S = RolloutShape<Task, T>;
-    auto kern = rollout_kernel<Task, T>;
+    auto kern = sc.action_repeat == 1 ? rollout_kernel<Task, T, true> : rollout_kernel<Task, T, false>;
     static bool attr_set = false;  // per instantiation; opt in above 48 KB once
     if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)S::SMEM);
-        if (e != cudaSuccess) return e;
+        for (auto kk : {rollout_kernel<Task, T, true>, rollout_kernel<Task, T, false>}) {
+            cudaError_t e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)S::SMEM);
+            if (e != cudaSuccess) return e;
+        }
         attr_set = true;
     }
     const int64_t grid = (sc.n + 31) / 32;  // one block per tile of 32 worlds

@@ -112,11 +112,10 @@ struct Cartpole {
         w.thd = w.thd + p.dt * thetaddot;
         w.x = w.x + p.dt * w.xd;
         w.th = w.th + p.dt * w.thd;
-        if (w.x < -p.rail_limit) {  // inelastic rail stop (envkit.py:330-333)
-            w.x = -p.rail_limit; w.xd = T(0);
-        } else if (w.x > p.rail_limit) {
-            w.x = p.rail_limit; w.xd = T(0);
-        }
+        // inelastic rail stop (envkit.py:330-333), branch-free
+        const bool lo = w.x < -p.rail_limit, hi = w.x > p.rail_limit;
+        w.x = lo ? -p.rail_limit : (hi ? p.rail_limit : w.x);
+        w.xd = (lo || hi) ? T(0) : w.xd;
         refresh(w);
     }
     static __device__ __forceinline__ T reward(const W &w, const Params<T> &, T *info) {
