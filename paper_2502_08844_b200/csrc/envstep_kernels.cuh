@@ -154,62 +154,65 @@ __device__ __forceinline__ void cp_async_wait() {
 // Fused K-step rollout (K == 1 is BatchEnv.step), warp-specialised.
 //
 // A block owns a tile of 32 worlds.  With only 8192 worlds per GPU there are
-// fewer warps than the 592 SM sub-partitions, so a monolithic thread-per-world
-// step is bound by the latency of one serial instruction stream.  The work is
-// therefore split by dependency:
-//   warp 0 (producer):   the serial chain only -- action clip/validation,
-//                        dynamics (+ trig refresh), step counter, Philox
-//                        autoreset; writes each post-step world state into a
-//                        D-deep shared-memory ring (slot layout [field][lane],
-//                        conflict-free) and arrives on full[slot].
-//   warps 1..M (consumers): control step k is handled by consumer k % M:
-//                        wait full[slot], pull the state into registers,
-//                        release empty[slot], then reward + info terms,
-//                        observation, flags and all global stores (rows
-//                        transposed through a per-warp tile so every store is
-//                        a coalesced 128 B line).
-// Rewards of the first action_repeat-1 substeps are summed by the producer in
-// the reference's order (reward = 0.0; reward += r, envkit.py:533-540), the
-// consumer adds the last one, so the arithmetic is unchanged.
+// fewer warps than the 592 SM sub-partitions, so the step rate is set by the
+// latency of one world's serial dependency chain.  The block's warps split the
+// work by dependency so that the chain runs alone in its warp:
+//   stager   (1 warp): streams the actions of G-step groups into a
+//            shared-memory ring (coalesced loads issued a group at a time),
+//            validates them (non-finite -> sticky error, envkit.py:529-531)
+//            and clips them to [-1, 1] (envkit.py:532).
+//   producer (1 warp): the serial chain only -- dynamics + trig refresh,
+//            step counter / truncation, Philox autoreset (out of line; it
+//            also writes the post-reset observation row itself).  Each
+//            post-step state goes into a group ring in shared memory
+//            (layout [field][lane], conflict-free).
+//   consumers (M warps): group g is handled by consumer g % M: reward + info
+//            terms, observation, flags and every global store (rows
+//            transposed through a per-warp tile into full 128 B lines).
+// Hand-offs are mbarrier phases, one per G-step group, so the chain pays
+// for synchronisation once per group.  Rewards of the first action_repeat-1
+// substeps are summed by the producer in the reference's order
+// (reward = 0.0; reward += r, envkit.py:533-540) and the consumer adds the last.
+
+__device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(addr), "r"(parity)
+            : "memory");
+    } while (!done);
+}
 
 template <class Task, typename T>
 struct RolloutShape {
-    static constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));  // floats per world
-    static constexpr int SLOT_BYTES = 32 * WF * (int)sizeof(T);
-    static constexpr int D = SLOT_BYTES <= 1024 ? 16 : 8;                    // ring depth
+    static constexpr int A = Task::A, O = Task::O, I = Task::I;
+    static constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));  // reals per world
+    static constexpr int G = WF * (int)sizeof(T) <= 24 ? 8 : 4;            // steps per group
     static constexpr int M = 4;                                              // consumer warps
-    static constexpr int R = Task::O > Task::I ? Task::O : Task::I;
-    static constexpr int THREADS = 32 * (1 + M);
-    static constexpr int P = 16;                                             // action prefetch depth
+    static constexpr int NG = M + 2;                                         // state ring (groups)
+    static constexpr int NA = 4;                                             // action ring (groups)
+    static constexpr int R = O > I ? O : I;
+    static constexpr int STAGER = M + 1;                                     // warp index
+    static constexpr int THREADS = 32 * (M + 2);
     // shared memory carve-up
-    static constexpr size_t OFF_BAR = 0;                                     // full[D], empty[D]
-    static constexpr size_t OFF_RING = 16 * D;
-    static constexpr size_t OFF_POST = OFF_RING + (size_t)D * WF * 32 * sizeof(T);
-    static constexpr size_t OFF_RPART = OFF_POST + (size_t)D * WF * 32 * sizeof(T);
-    static constexpr size_t OFF_FLAGS = OFF_RPART + (size_t)D * 32 * sizeof(T);
-    static constexpr size_t OFF_TILE = (OFF_FLAGS + (size_t)D * 32 + 15) / 16 * 16;
-    static constexpr size_t OFF_ACT = OFF_TILE + (size_t)M * 32 * R * sizeof(T);  // [P][32][A]
-    static constexpr size_t OFF_CTRL = OFF_ACT + (size_t)P * 32 * Task::A * sizeof(T);
+    static constexpr size_t OFF_BAR = 0;  // full[NG] empty[NG] afull[NA] aempty[NA]
+    static constexpr size_t OFF_RING = 8 * (2 * NG + 2 * NA);
+    static constexpr size_t RING_G = (size_t)G * WF * 32 * sizeof(T);       // bytes per group
+    static constexpr size_t OFF_RPART = OFF_RING + NG * RING_G;
+    static constexpr size_t OFF_ACT = OFF_RPART + (size_t)NG * G * 32 * sizeof(T);
+    static constexpr size_t ACT_G = (size_t)G * A * 32 * sizeof(T);
+    static constexpr size_t OFF_TILE = OFF_ACT + NA * ACT_G;
+    static constexpr size_t OFF_FLAGS = OFF_TILE + (size_t)M * 32 * R * sizeof(T);
+    static constexpr size_t OFF_CTRL = (OFF_FLAGS + (size_t)NG * G * 32 + 15) / 16 * 16;
     static constexpr size_t SMEM = OFF_CTRL + 16;
 };
-
-template <class Task, typename T>
-__device__ __forceinline__ void world_to_slot(const typename Task::W &w, T *slot, int lane);
-
-// Environment.reset (envkit.py:502-519) of one world inside a rollout: the
-// next Philox stream of (seed, env, episode) -> sample_initial.  Out of line:
-// taken once per episode_length steps.
-template <class Task, typename T>
-__device__ __noinline__ typename Task::W autoreset_world(uint64_t seed, uint64_t gidx,
-                                                         uint32_t episode, Params<T> p, int wide,
-                                                         T *post_slot, int lane) {
-    typename Task::W wd;
-    Philox4x64 rng;
-    rng.init(seed, gidx, episode, 0);
-    Task::sample(wd, rng, p, wide != 0);
-    world_to_slot<Task, T>(wd, post_slot, lane);
-    return wd;
-}
 
 template <class Task, typename T>
 __device__ __forceinline__ void world_to_slot(const typename Task::W &w, T *slot, int lane) {
@@ -227,115 +230,124 @@ __device__ __forceinline__ void slot_to_world(typename Task::W &w, const T *slot
     for (int j = 0; j < WF; ++j) f[j] = slot[j * 32 + lane];
 }
 
+// Environment.reset (envkit.py:502-519) of one world inside a rollout: the
+// next Philox stream of (seed, env, episode) -> sample_initial; writes the
+// post-reset observation row (the step's returned obs, envkit.py:634).  Out of
+// line: taken once per episode_length steps.
+template <class Task, typename T>
+__device__ __noinline__ typename Task::W autoreset_world(uint64_t seed, uint64_t gidx,
+                                                         uint32_t episode, Params<T> p, int wide,
+                                                         T *obs_row) {
+    typename Task::W wd;
+    Philox4x64 rng;
+    rng.init(seed, gidx, episode, 0);
+    Task::sample(wd, rng, p, wide != 0);
+    T o[Task::O];
+    Task::obs(wd, p, o);
+#pragma unroll
+    for (int j = 0; j < Task::O; ++j) obs_row[j] = o[j];
+    return wd;
+}
+
+// warp_store_rows, skipping the rows of lanes set in `skip`.
+template <typename T, int R>
+__device__ __forceinline__ void warp_store_rows_skip(T *__restrict__ out, int64_t row0,
+                                                     int64_t nrows, const T (&v)[R], T *tile,
+                                                     int lane, uint32_t skip) {
+#pragma unroll
+    for (int j = 0; j < R; ++j) tile[lane * R + j] = v[j];
+    __syncwarp();
+    const int64_t valid = nrows - row0 < 32 ? (nrows - row0) * R : 32 * R;
+    T *dst = out + row0 * R;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        const int e = j * 32 + lane;
+        if (e < valid && !((skip >> (e / R)) & 1u)) dst[e] = tile[e];
+    }
+    __syncwarp();
+}
+
 template <class Task, typename T, bool R1>
 __global__ void __launch_bounds__(RolloutShape<Task, T>::THREADS)
 rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T> p, Worlds<T> w,
                StepOut<T> out, unsigned long long *err) {
     using S = RolloutShape<Task, T>;
-    constexpr int A = Task::A, O = Task::O, I = Task::I, WF = S::WF, D = S::D, M = S::M;
+    constexpr int A = Task::A, O = Task::O, I = Task::I, WF = S::WF, G = S::G, M = S::M;
+    constexpr int NG = S::NG, NA = S::NA;
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem + S::OFF_BAR);
-    uint64_t *empty = full + D;
-    T *ring = reinterpret_cast<T *>(smem + S::OFF_RING);    // [D][WF][32]
-    T *post = reinterpret_cast<T *>(smem + S::OFF_POST);    // [D][WF][32] post-reset state
-    T *rpart = reinterpret_cast<T *>(smem + S::OFF_RPART);  // [D][32]
-    uint8_t *flags = smem + S::OFF_FLAGS;                   // [D][32] bit0 trunc, bit1 reset
+    T *ring = reinterpret_cast<T *>(smem + S::OFF_RING);    // [NG][G][WF][32]
+    T *rpart = reinterpret_cast<T *>(smem + S::OFF_RPART);  // [NG][G][32]
+    T *aring = reinterpret_cast<T *>(smem + S::OFF_ACT);    // [NA][G][A][32]
+    uint8_t *flags = smem + S::OFF_FLAGS;                   // [NG][G][32] bit0 trunc, bit1 reset
     int *ctrl = reinterpret_cast<int *>(smem + S::OFF_CTRL);
+    const uint32_t bar = smem_u32(smem + S::OFF_BAR);
+    const uint32_t full_b = bar, empty_b = bar + 8 * NG, afull_b = bar + 16 * NG,
+                   aempty_b = bar + 16 * NG + 8 * NA;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n = sc.n;
     const int64_t i = (int64_t)blockIdx.x * 32 + lane;
     const int64_t row0 = (int64_t)blockIdx.x * 32;
     const bool in_range = i < n;
+    const int K32 = (int)K;  // host guarantees K < 2^31
+    const int ngroups = (K32 + G - 1) / G;
 
     if (threadIdx.x == 0) {
         // a pending (sticky) error from an earlier call: the batch is not
         // stepped.  Read once so the whole block takes the same branch.
         ctrl[0] = *(volatile const unsigned long long *)err != kNoError;
         ctrl[1] = *w.cur;
+        uint64_t *b = reinterpret_cast<uint64_t *>(smem + S::OFF_BAR);
 #pragma unroll
-        for (int d = 0; d < D; ++d) {
-            mbar_init(&full[d], 32);
-            mbar_init(&empty[d], 32);  // consumer warp 0 pre-arms every slot once (below)
-        }
+        for (int d = 0; d < 2 * NG + 2 * NA; ++d) mbar_init(&b[d], 32);
     }
     __syncthreads();
     const bool blocked = ctrl[0] != 0;
     const int src = ctrl[1];
+    // buffer selection by ternary: runtime-indexing the by-value param arrays
+    // would spill the whole struct to local memory
+    const int32_t *steps_src = src ? w.steps[1] : w.steps[0];
+    const uint8_t *nr_src = src ? w.needs_reset[1] : w.needs_reset[0];
 
-    if (!blocked && warp == 0) {
+    // step at which this world would need a reset (UsageError, envkit.py:527-528)
+    auto usage_step = [&](int32_t steps) -> int {
+        if (!in_range) return K32;
+        if (nr_src[i]) return 0;
+        if (!sc.autoreset && (int64_t)sc.episode_length - steps < K)
+            return (int)((int64_t)sc.episode_length - steps);
+        return K32;
+    };
+
+    if (blocked) {
+        // nothing
+    } else if (warp == 0) {
         // ------------------------------------------------------------ producer
-        // buffer selection by ternary: runtime-indexing the by-value param
-        // arrays would spill the whole struct to local memory
         const T *st_src = src ? w.state[1] : w.state[0];
         T *st_dst = src ? w.state[0] : w.state[1];
-        const int32_t *steps_src = src ? w.steps[1] : w.steps[0];
         int32_t *steps_dst = src ? w.steps[0] : w.steps[1];
         const uint32_t *ep_src = src ? w.episode[1] : w.episode[0];
         uint32_t *ep_dst = src ? w.episode[0] : w.episode[1];
-        const uint8_t *nr_src = src ? w.needs_reset[1] : w.needs_reset[0];
         uint8_t *nr_dst = src ? w.needs_reset[0] : w.needs_reset[1];
 
         typename Task::W wd;
         int32_t steps = 0;
         uint32_t episode = 0;
-        int64_t k_usage = K;  // step at which this world would need a reset (UsageError)
         if (in_range) {
             Task::load(wd, st_src, i, n);
             steps = steps_src[i];
             episode = ep_src[i];
-            if (nr_src[i]) {
-                k_usage = 0;
-            } else if (!sc.autoreset && (int64_t)sc.episode_length - steps < K) {
-                k_usage = (int64_t)sc.episode_length - steps;
-            }
-            if (k_usage < K) record_error(err, k_usage, n, i, kErrUsage);
         } else {
             Task::zero(wd);
         }
+        const int ku = usage_step(steps);
+        if (ku < K32) record_error(err, ku, n, i, kErrUsage);
         Task::refresh(wd);
         const uint64_t gidx = (uint64_t)(sc.env_offset + i);
-        bool ok = true;
 
-        // actions stream through a P-deep shared-memory ring filled by
-        // cp.async P steps ahead: the loop body stays one step long (small
-        // I-cache footprint) and the dependent chain never waits on HBM
-        constexpr int P = S::P;
-        T *aring = reinterpret_cast<T *>(smem + S::OFF_ACT);  // [P][32][A]
-        const int K32 = (int)K;  // host guarantees K < 2^31
-        const T *aptr = actions + (in_range ? i * A : 0);
-        const int64_t astep = in_range ? n * A : 0;
-#pragma unroll 1
-        for (int k = 0; k < P; ++k) {
-            cp_async_ca<A * sizeof(T)>(aring + (k * 32 + lane) * A, aptr + k * astep,
-                                       in_range && k < K32);
-            cp_async_commit();
-        }
-        const T *anext = aptr + P * astep;
-        const int ku = k_usage < K ? (int)k_usage : K32;
-        uint32_t phase_bits = 0;  // bit d: parity of the next empty[d] completion to wait for
-
-#pragma unroll 1
-        for (int k = 0; k < K32; ++k) {
-            const int slot = k & (D - 1);
-            const int ar = k & (P - 1);
-            cp_async_wait<P - 1>();  // this lane's copy for step k has landed
+        auto step_body = [&](int s, int k, T *ring_g, T *rp_g, uint8_t *fl_g, const T *act_g) {
             T a[A];
-            bool fin = true;
 #pragma unroll
-            for (int j = 0; j < A; ++j) {  // min(max(float(a), -1.0), 1.0)  (envkit.py:532)
-                T v = aring[(ar * 32 + lane) * A + j];
-                fin &= RealOps<T>::finite_(v);
-                a[j] = fmin(fmax(v, T(-1)), T(1));
-            }
-            cp_async_ca<A * sizeof(T)>(aring + (ar * 32 + lane) * A, anext,
-                                       in_range && k + P < K32);
-            cp_async_commit();
-            anext += astep;
-            if (__builtin_expect(!fin && ok && in_range && k < ku, 0)) {  // envkit.py:529-531
-                ok = false;
-                record_error(err, k, n, i, kErrInvalid);
-            }
+            for (int j = 0; j < A; ++j) a[j] = act_g[(s * A + j) * 32 + lane];
             T rp = T(0);
             Task::step(wd, a, p);
             if (!R1) {
@@ -348,20 +360,37 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             steps += 1;
             const bool truncated = steps >= sc.episode_length;
             const bool reset = truncated && sc.autoreset && in_range;
-            mbar_wait(&empty[slot], (phase_bits >> slot) & 1u);
-            phase_bits ^= 1u << slot;
-            world_to_slot<Task, T>(wd, ring + (size_t)slot * WF * 32, lane);
-            if (!R1) rpart[slot * 32 + lane] = rp;
-            flags[slot * 32 + lane] = (uint8_t)((truncated ? 1 : 0) | (reset ? 2 : 0));
+            world_to_slot<Task, T>(wd, ring_g + s * WF * 32, lane);
+            if (!R1) rp_g[s * 32 + lane] = rp;
+            fl_g[s * 32 + lane] = (uint8_t)((truncated ? 1 : 0) | (reset ? 2 : 0));
             if (__builtin_expect(reset, 0)) {
                 episode += 1;
                 steps = 0;
                 wd = autoreset_world<Task, T>(sc.seed, gidx, episode, p, sc.wide_init,
-                                              post + (size_t)slot * WF * 32, lane);
+                                              out.obs + ((int64_t)k * n + i) * O);
             }
-            mbar_arrive(&full[slot]);
+        };
+
+#pragma unroll 1
+        for (int g = 0; g < ngroups; ++g) {
+            const int sb = g % NG, ab = g % NA;
+            mbar_wait_u32(afull_b + 8 * ab, (uint32_t)(g / NA) & 1u);
+            mbar_wait_u32(empty_b + 8 * sb, (uint32_t)(g / NG) & 1u);  // phase 0 pre-armed
+            T *ring_g = ring + (size_t)sb * G * WF * 32;
+            T *rp_g = rpart + (size_t)sb * G * 32;
+            uint8_t *fl_g = flags + sb * G * 32;
+            const T *act_g = aring + (size_t)ab * G * A * 32;
+            const int k0 = g * G;
+            if (k0 + G <= K32) {
+#pragma unroll
+                for (int s = 0; s < G; ++s) step_body(s, k0 + s, ring_g, rp_g, fl_g, act_g);
+            } else {
+#pragma unroll 1
+                for (int s = 0; s < K32 - k0; ++s) step_body(s, k0 + s, ring_g, rp_g, fl_g, act_g);
+            }
+            mbar_arrive_u32(aempty_b + 8 * ab);
+            mbar_arrive_u32(full_b + 8 * sb);
         }
-        cp_async_wait<0>();
         if (in_range) {
             Task::store(wd, st_dst, i, n);
             steps_dst[i] = steps;
@@ -369,47 +398,87 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             // without autoreset a world that truncated in this window needs a reset
             nr_dst[i] = (!sc.autoreset && steps >= sc.episode_length) ? 1 : 0;
         }
-    } else if (!blocked) {
+    } else if (warp == S::STAGER) {
+        // ------------------------------------------------------------ stager
+        const int ku = usage_step(in_range ? steps_src[i] : 0);
+        bool ok = true;
+        const T *arow = actions + (in_range ? i * A : 0);
+        const int64_t astep = in_range ? n * A : 0;
+#pragma unroll 1
+        for (int g = 0; g < ngroups; ++g) {
+            const int ab = g % NA;
+            const int k0 = g * G;
+            T v[G][A];
+#pragma unroll
+            for (int s = 0; s < G; ++s)  // issue the whole group's loads first
+#pragma unroll
+                for (int j = 0; j < A; ++j)
+                    v[s][j] = (in_range && k0 + s < K32) ? __ldg(arow + (k0 + s) * astep + j)
+                                                         : T(0);
+            if (g >= NA) mbar_wait_u32(aempty_b + 8 * ab, (uint32_t)(g / NA - 1) & 1u);
+            T *act_g = aring + (size_t)ab * G * A * 32;
+#pragma unroll
+            for (int s = 0; s < G; ++s) {
+                bool fin = true;
+#pragma unroll
+                for (int j = 0; j < A; ++j) {
+                    fin &= RealOps<T>::finite_(v[s][j]);
+                    // min(max(float(a), -1.0), 1.0)  (envkit.py:532)
+                    act_g[(s * A + j) * 32 + lane] = fmin(fmax(v[s][j], T(-1)), T(1));
+                }
+                if (__builtin_expect(!fin && ok && in_range && k0 + s < ku && k0 + s < K32, 0)) {
+                    ok = false;  // envkit.py:529-531
+                    record_error(err, k0 + s, n, i, kErrInvalid);
+                }
+            }
+            mbar_arrive_u32(afull_b + 8 * ab);
+        }
+    } else {
         // ------------------------------------------------------------ consumers
         const int c = warp - 1;
         T *tile = reinterpret_cast<T *>(smem + S::OFF_TILE) + (size_t)c * 32 * S::R;
         const T inv_rep = T(sc.action_repeat);
         if (c == 0) {
-#pragma unroll
-            for (int d = 0; d < D; ++d) mbar_arrive(&empty[d]);  // slots start free
+#pragma unroll 1
+            for (int d = 0; d < NG; ++d) mbar_arrive_u32(empty_b + 8 * d);  // slots start free
         }
-        for (int64_t k = c; k < K; k += M) {
-            const int slot = (int)(k % D);
-            mbar_wait(&full[slot], (uint32_t)(k / D) & 1u);
-            typename Task::W wd, wp;
-            slot_to_world<Task, T>(wd, ring + (size_t)slot * WF * 32, lane);
-            const T rp = R1 ? T(0) : rpart[slot * 32 + lane];
-            const uint8_t fl = flags[slot * 32 + lane];
-            const bool reset = (fl & 2) != 0;
-            if (reset) slot_to_world<Task, T>(wp, post + (size_t)slot * WF * 32, lane);
-            mbar_arrive(&empty[slot]);
-
-            T info[I];
-            const T r = R1 ? (T(0) + Task::reward(wd, p, info))
-                           : (rp + Task::reward(wd, p, info)) / inv_rep;
-            T o[O];
-            Task::obs(wd, p, o);
-            const int64_t ko = k * n;
-            if (reset) {
-                if (out.term_obs) {
+#pragma unroll 1
+        for (int g = c; g < ngroups; g += M) {
+            const int sb = g % NG;
+            mbar_wait_u32(full_b + 8 * sb, (uint32_t)(g / NG) & 1u);
+            const T *ring_g = ring + (size_t)sb * G * WF * 32;
+            const T *rp_g = rpart + (size_t)sb * G * 32;
+            const uint8_t *fl_g = flags + sb * G * 32;
+            const int kend = min(G, K32 - g * G);
+#pragma unroll 1
+            for (int s = 0; s < kend; ++s) {
+                const int64_t k = (int64_t)g * G + s;
+                typename Task::W wd;
+                slot_to_world<Task, T>(wd, ring_g + s * WF * 32, lane);
+                const uint8_t fl = fl_g[s * 32 + lane];
+                const bool reset = (fl & 2) != 0;
+                T info[I];
+                const T r = R1 ? (T(0) + Task::reward(wd, p, info))
+                               : (rp_g[s * 32 + lane] + Task::reward(wd, p, info)) / inv_rep;
+                T o[O];
+                Task::obs(wd, p, o);
+                const int64_t ko = k * n;
+                if (reset && out.term_obs) {
 #pragma unroll
                     for (int j = 0; j < O; ++j) out.term_obs[(ko + i) * O + j] = o[j];
                 }
-                Task::obs(wp, p, o);
+                // the producer wrote the post-reset observation of reset worlds
+                const uint32_t skip = __ballot_sync(0xffffffffu, reset);
+                warp_store_rows_skip<T, O>(out.obs + ko * O, row0, n, o, tile, lane, skip);
+                if (out.info) warp_store_rows<T, I>(out.info + ko * I, row0, n, info, tile, lane);
+                if (in_range) {
+                    out.reward[ko + i] = r;
+                    out.done[ko + i] = 0;
+                    out.trunc[ko + i] = fl & 1;
+                    if (out.term_mask) out.term_mask[ko + i] = reset ? 1 : 0;
+                }
             }
-            warp_store_rows<T, O>(out.obs + ko * O, row0, n, o, tile, lane);
-            if (out.info) warp_store_rows<T, I>(out.info + ko * I, row0, n, info, tile, lane);
-            if (in_range) {
-                out.reward[ko + i] = r;
-                out.done[ko + i] = 0;
-                out.trunc[ko + i] = fl & 1;
-                if (out.term_mask) out.term_mask[ko + i] = reset ? 1 : 0;
-            }
+            mbar_arrive_u32(empty_b + 8 * sb);
         }
     }
     finish_launch(w.cur, w.blocks_done, err, !blocked);
