@@ -344,22 +344,20 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         Task::refresh(wd);
         const uint64_t gidx = (uint64_t)(sc.env_offset + i);
 
-        auto step_body = [&](int s, int k, T *ring_g, T *rp_g, uint8_t *fl_g, const T *act_g) {
-            T a[A];
-#pragma unroll
-            for (int j = 0; j < A; ++j) a[j] = act_g[(s * A + j) * 32 + lane];
+        const bool can_reset = sc.autoreset && in_range;
+        auto step_body = [&](int s, int k, T *ring_g, T *rp_g, uint8_t *fl_g, const T *u) {
             T rp = T(0);
-            Task::step(wd, a, p);
+            Task::step_u(wd, u, p);
             if (!R1) {
                 for (int rep = 1; rep < sc.action_repeat; ++rep) {
                     T inf[I];
                     rp += Task::reward(wd, p, inf);
-                    Task::step(wd, a, p);
+                    Task::step_u(wd, u, p);
                 }
             }
             steps += 1;
             const bool truncated = steps >= sc.episode_length;
-            const bool reset = truncated && sc.autoreset && in_range;
+            const bool reset = truncated && can_reset;
             world_to_slot<Task, T>(wd, ring_g + s * WF * 32, lane);
             if (!R1) rp_g[s * 32 + lane] = rp;
             fl_g[s * 32 + lane] = (uint8_t)((truncated ? 1 : 0) | (reset ? 2 : 0));
@@ -382,11 +380,21 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             const T *act_g = aring + (size_t)ab * G * A * 32;
             const int k0 = g * G;
             if (k0 + G <= K32) {
+                T u[G][A];  // the whole group's controls, loaded ahead of the chain
 #pragma unroll
-                for (int s = 0; s < G; ++s) step_body(s, k0 + s, ring_g, rp_g, fl_g, act_g);
+                for (int s = 0; s < G; ++s)
+#pragma unroll
+                    for (int j = 0; j < A; ++j) u[s][j] = act_g[(s * A + j) * 32 + lane];
+#pragma unroll
+                for (int s = 0; s < G; ++s) step_body(s, k0 + s, ring_g, rp_g, fl_g, u[s]);
             } else {
 #pragma unroll 1
-                for (int s = 0; s < K32 - k0; ++s) step_body(s, k0 + s, ring_g, rp_g, fl_g, act_g);
+                for (int s = 0; s < K32 - k0; ++s) {
+                    T u[A];
+#pragma unroll
+                    for (int j = 0; j < A; ++j) u[j] = act_g[(s * A + j) * 32 + lane];
+                    step_body(s, k0 + s, ring_g, rp_g, fl_g, u);
+                }
             }
             mbar_arrive_u32(aempty_b + 8 * ab);
             mbar_arrive_u32(full_b + 8 * sb);
@@ -420,12 +428,16 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
 #pragma unroll
             for (int s = 0; s < G; ++s) {
                 bool fin = true;
+                T a[A], u[A];
 #pragma unroll
                 for (int j = 0; j < A; ++j) {
                     fin &= RealOps<T>::finite_(v[s][j]);
-                    // min(max(float(a), -1.0), 1.0)  (envkit.py:532)
-                    act_g[(s * A + j) * 32 + lane] = fmin(fmax(v[s][j], T(-1)), T(1));
+                    a[j] = fmin(fmax(v[s][j], T(-1)), T(1));  // envkit.py:532
                 }
+                // the force / torque clip of step_dynamics, off the producer's chain
+                Task::control(a, p, u);
+#pragma unroll
+                for (int j = 0; j < A; ++j) act_g[(s * A + j) * 32 + lane] = u[j];
                 if (__builtin_expect(!fin && ok && in_range && k0 + s < ku && k0 + s < K32, 0)) {
                     ok = false;  // envkit.py:529-531
                     record_error(err, k0 + s, n, i, kErrInvalid);
@@ -469,7 +481,10 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
                 }
                 // the producer wrote the post-reset observation of reset worlds
                 const uint32_t skip = __ballot_sync(0xffffffffu, reset);
-                warp_store_rows_skip<T, O>(out.obs + ko * O, row0, n, o, tile, lane, skip);
+                if (__builtin_expect(skip == 0u, 1))
+                    warp_store_rows<T, O>(out.obs + ko * O, row0, n, o, tile, lane);
+                else
+                    warp_store_rows_skip<T, O>(out.obs + ko * O, row0, n, o, tile, lane, skip);
                 if (out.info) warp_store_rows<T, I>(out.info + ko * I, row0, n, info, tile, lane);
                 if (in_range) {
                     out.reward[ko + i] = r;

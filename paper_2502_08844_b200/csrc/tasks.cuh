@@ -12,7 +12,10 @@
 //   struct W                 registers of one world
 //   load/store(W&, soa, i, N)  structure-of-arrays state in HBM
 //   refresh(W&)              trig of the current state
-//   step(W&, a[A], P)        step_dynamics + refresh
+//   control(a[A], P, u[A])   clipped action -> clipped force/torque (the
+//                            min(max(a * limit, -limit), limit) of step_dynamics)
+//   step_u(W&, u[A], P)      step_dynamics given u, + refresh
+//   step(W&, a[A], P)        control + step_u
 //   reward(W&, P, info[I])   reward + info terms of the current state
 //   obs(W&, P, o[O])         state_obs of the current state
 //   sample(W&, Philox&, P, wide)  sample_initial + refresh
@@ -46,8 +49,16 @@ struct Pendulum {
     }
     static __device__ __forceinline__ void zero(W &w) { w.th = T(0); w.om = T(0); }
     static __device__ __forceinline__ void refresh(W &w) { RealOps<T>::sincos_(w.th, &w.s, &w.c); }
+    static __device__ __forceinline__ void control(const T *a, const Params<T> &p, T *u) {
+        u[0] = clip_sym(a[0] * p.pend_torque_limit, p.pend_torque_limit);
+    }
     static __device__ __forceinline__ void step(W &w, const T *a, const Params<T> &p) {
-        const T torque = clip_sym(a[0] * p.pend_torque_limit, p.pend_torque_limit);
+        T u[A];
+        control(a, p, u);
+        step_u(w, u, p);
+    }
+    static __device__ __forceinline__ void step_u(W &w, const T *u, const Params<T> &p) {
+        const T torque = u[0];
         const T m = p.pend_mass, l = p.pend_length;
         const T accel =
             RealOps<T>::div_(torque - p.pend_damping * w.om - m * p.gravity * l * w.s, m * l * l);
@@ -97,8 +108,16 @@ struct Cartpole {
     }
     static __device__ __forceinline__ void zero(W &w) { w.x = w.th = w.xd = w.thd = T(0); }
     static __device__ __forceinline__ void refresh(W &w) { RealOps<T>::sincos_(w.th, &w.s, &w.c); }
+    static __device__ __forceinline__ void control(const T *a, const Params<T> &p, T *u) {
+        u[0] = clip_sym(a[0] * p.cart_force_limit, p.cart_force_limit);
+    }
     static __device__ __forceinline__ void step(W &w, const T *a, const Params<T> &p) {
-        const T force = clip_sym(a[0] * p.cart_force_limit, p.cart_force_limit);
+        T u[A];
+        control(a, p, u);
+        step_u(w, u, p);
+    }
+    static __device__ __forceinline__ void step_u(W &w, const T *u, const Params<T> &p) {
+        const T force = u[0];
         const T mc = p.cart_mass, mp = p.pole_mass, l = p.pole_length, g = p.gravity;
         const T m11 = mc + mp;
         const T m12 = mp * l * w.c;
@@ -199,9 +218,16 @@ struct Acrobot {
     }
     static __device__ __forceinline__ void zero(W &w) { w.t1 = w.t2 = w.d1 = w.d2 = w.tx = w.ty = T(0); }
     static __device__ __forceinline__ void refresh(W &w) { twolink_refresh(w); }
+    static __device__ __forceinline__ void control(const T *a, const Params<T> &p, T *u) {
+        u[0] = clip_sym(a[0] * p.elbow_torque_limit, p.elbow_torque_limit);
+    }
+    static __device__ __forceinline__ void step_u(W &w, const T *u, const Params<T> &p) {
+        twolink_advance(w, T(0), u[0], p.gravity, p);
+    }
     static __device__ __forceinline__ void step(W &w, const T *a, const Params<T> &p) {
-        const T torque = clip_sym(a[0] * p.elbow_torque_limit, p.elbow_torque_limit);
-        twolink_advance(w, T(0), torque, p.gravity, p);
+        T u[A];
+        control(a, p, u);
+        step_u(w, u, p);
     }
     static __device__ __forceinline__ T reward(const W &w, const Params<T> &p, T *info) {
         const T tip_y = -(p.link1_length * w.c1 + p.link2_length * w.c12);
@@ -244,9 +270,18 @@ struct Reacher {
     }
     static __device__ __forceinline__ void zero(W &w) { w.t1 = w.t2 = w.d1 = w.d2 = w.tx = w.ty = T(0); }
     static __device__ __forceinline__ void refresh(W &w) { twolink_refresh(w); }
-    static __device__ __forceinline__ void step(W &w, const T *a, const Params<T> &p) {
+    static __device__ __forceinline__ void control(const T *a, const Params<T> &p, T *u) {
         const T lim = p.reacher_torque_limit;
-        twolink_advance(w, clip_sym(a[0] * lim, lim), clip_sym(a[1] * lim, lim), T(0), p);
+        u[0] = clip_sym(a[0] * lim, lim);
+        u[1] = clip_sym(a[1] * lim, lim);
+    }
+    static __device__ __forceinline__ void step_u(W &w, const T *u, const Params<T> &p) {
+        twolink_advance(w, u[0], u[1], T(0), p);
+    }
+    static __device__ __forceinline__ void step(W &w, const T *a, const Params<T> &p) {
+        T u[A];
+        control(a, p, u);
+        step_u(w, u, p);
     }
     static __device__ __forceinline__ void tip(const W &w, const Params<T> &p, T &x, T &y) {
         x = p.link1_length * w.c1 + p.link2_length * w.c12;
