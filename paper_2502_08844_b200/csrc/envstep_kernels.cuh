@@ -412,17 +412,20 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         bool ok = true;
         const T *arow = actions + (in_range ? i * A : 0);
         const int64_t astep = in_range ? n * A : 0;
-#pragma unroll 1
-        for (int g = 0; g < ngroups; ++g) {
-            const int ab = g % NA;
+        // two groups of loads in flight ahead of the group being processed
+        T v0[G][A], v1[G][A];
+        auto load = [&](T (&v)[G][A], int g) {
             const int k0 = g * G;
-            T v[G][A];
 #pragma unroll
-            for (int s = 0; s < G; ++s)  // issue the whole group's loads first
+            for (int s = 0; s < G; ++s)
 #pragma unroll
                 for (int j = 0; j < A; ++j)
                     v[s][j] = (in_range && k0 + s < K32) ? __ldg(arow + (k0 + s) * astep + j)
                                                          : T(0);
+        };
+        auto process = [&](const T (&v)[G][A], int g) {
+            const int ab = g % NA;
+            const int k0 = g * G;
             if (g >= NA) mbar_wait_u32(aempty_b + 8 * ab, (uint32_t)(g / NA - 1) & 1u);
             T *act_g = aring + (size_t)ab * G * A * 32;
 #pragma unroll
@@ -444,6 +447,17 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
                 }
             }
             mbar_arrive_u32(afull_b + 8 * ab);
+        };
+        load(v0, 0);
+        load(v1, 1);
+#pragma unroll 1
+        for (int g = 0; g < ngroups; g += 2) {
+            process(v0, g);
+            load(v0, g + 2);
+            if (g + 1 < ngroups) {
+                process(v1, g + 1);
+                load(v1, g + 3);
+            }
         }
     } else {
         // ------------------------------------------------------------ consumers
