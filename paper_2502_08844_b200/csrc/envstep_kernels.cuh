@@ -199,7 +199,9 @@ struct RolloutShape {
     static constexpr int NG = M + 2;                                         // state ring (groups)
     static constexpr int NA = 4;                                             // action ring (groups)
     static constexpr int R = O > I ? O : I;
-    static constexpr int STAGER = M + 1;                                     // warp index
+    // warp w runs on SM sub-partition w % 4: the light stager shares the
+    // producer's (warp 0) scheduler, consumers are warps 1, 2, 3, 5, ...
+    static constexpr int STAGER = 4;                                         // warp index
     static constexpr int THREADS = 32 * (M + 2);
     // shared memory carve-up
     static constexpr size_t OFF_BAR = 0;  // full[NG] empty[NG] afull[NA] aempty[NA]
@@ -210,7 +212,8 @@ struct RolloutShape {
     static constexpr size_t ACT_G = (size_t)G * A * 32 * sizeof(T);
     static constexpr size_t OFF_TILE = OFF_ACT + NA * ACT_G;
     static constexpr size_t OFF_FLAGS = OFF_TILE + (size_t)M * 32 * R * sizeof(T);
-    static constexpr size_t OFF_CTRL = (OFF_FLAGS + (size_t)NG * G * 32 + 15) / 16 * 16;
+    static constexpr size_t OFF_GFLAG = OFF_FLAGS + (size_t)NG * G * 32;   // [NG] u8: fast group
+    static constexpr size_t OFF_CTRL = (OFF_GFLAG + NG + 15) / 16 * 16;
     static constexpr size_t SMEM = OFF_CTRL + 16;
 };
 
@@ -279,6 +282,7 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
     T *rpart = reinterpret_cast<T *>(smem + S::OFF_RPART);  // [NG][G][32]
     T *aring = reinterpret_cast<T *>(smem + S::OFF_ACT);    // [NA][G][A][32]
     uint8_t *flags = smem + S::OFF_FLAGS;                   // [NG][G][32] bit0 trunc, bit1 reset
+    uint8_t *gflag = smem + S::OFF_GFLAG;                   // [NG] 1: no world truncated in the group
     int *ctrl = reinterpret_cast<int *>(smem + S::OFF_CTRL);
     const uint32_t bar = smem_u32(smem + S::OFF_BAR);
     const uint32_t full_b = bar, empty_b = bar + 8 * NG, afull_b = bar + 16 * NG,
@@ -379,23 +383,42 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             uint8_t *fl_g = flags + sb * G * 32;
             const T *act_g = aring + (size_t)ab * G * A * 32;
             const int k0 = g * G;
-            if (k0 + G <= K32) {
+            // fast group: no world of this warp reaches episode_length inside
+            // it (124 of 125 groups at episode_length 1000), so the chain
+            // carries no step counting, flags or reset branch
+            const bool fast = (k0 + G <= K32) &&
+                              !__any_sync(0xffffffffu, in_range && steps + G >= sc.episode_length);
+            if (fast) {
                 T u[G][A];  // the whole group's controls, loaded ahead of the chain
 #pragma unroll
                 for (int s = 0; s < G; ++s)
 #pragma unroll
                     for (int j = 0; j < A; ++j) u[s][j] = act_g[(s * A + j) * 32 + lane];
 #pragma unroll
-                for (int s = 0; s < G; ++s) step_body(s, k0 + s, ring_g, rp_g, fl_g, u[s]);
+                for (int s = 0; s < G; ++s) {
+                    T rp = T(0);
+                    Task::step_u(wd, u[s], p);
+                    if (!R1) {
+                        for (int rep = 1; rep < sc.action_repeat; ++rep) {
+                            T inf[I];
+                            rp += Task::reward(wd, p, inf);
+                            Task::step_u(wd, u[s], p);
+                        }
+                        rp_g[s * 32 + lane] = rp;
+                    }
+                    world_to_slot<Task, T>(wd, ring_g + s * WF * 32, lane);
+                }
+                steps += G;
             } else {
 #pragma unroll 1
-                for (int s = 0; s < K32 - k0; ++s) {
+                for (int s = 0; s < min(G, K32 - k0); ++s) {
                     T u[A];
 #pragma unroll
                     for (int j = 0; j < A; ++j) u[j] = act_g[(s * A + j) * 32 + lane];
                     step_body(s, k0 + s, ring_g, rp_g, fl_g, u);
                 }
             }
+            if (lane == 0) gflag[sb] = fast ? 1 : 0;
             mbar_arrive_u32(aempty_b + 8 * ab);
             mbar_arrive_u32(full_b + 8 * sb);
         }
@@ -461,7 +484,7 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         }
     } else {
         // ------------------------------------------------------------ consumers
-        const int c = warp - 1;
+        const int c = warp < S::STAGER ? warp - 1 : warp - 2;  // consumer index 0..M-1
         T *tile = reinterpret_cast<T *>(smem + S::OFF_TILE) + (size_t)c * 32 * S::R;
         const T inv_rep = T(sc.action_repeat);
         if (c == 0) {
@@ -475,13 +498,14 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             const T *ring_g = ring + (size_t)sb * G * WF * 32;
             const T *rp_g = rpart + (size_t)sb * G * 32;
             const uint8_t *fl_g = flags + sb * G * 32;
+            const bool fast = gflag[sb] != 0;
             const int kend = min(G, K32 - g * G);
 #pragma unroll 1
             for (int s = 0; s < kend; ++s) {
                 const int64_t k = (int64_t)g * G + s;
                 typename Task::W wd;
                 slot_to_world<Task, T>(wd, ring_g + s * WF * 32, lane);
-                const uint8_t fl = fl_g[s * 32 + lane];
+                const uint8_t fl = fast ? 0 : fl_g[s * 32 + lane];
                 const bool reset = (fl & 2) != 0;
                 T info[I];
                 const T r = R1 ? (T(0) + Task::reward(wd, p, info))

@@ -131,10 +131,11 @@ struct Cartpole {
         w.thd = w.thd + p.dt * thetaddot;
         w.x = w.x + p.dt * w.xd;
         w.th = w.th + p.dt * w.thd;
-        // inelastic rail stop (envkit.py:330-333), branch-free
-        const bool lo = w.x < -p.rail_limit, hi = w.x > p.rail_limit;
-        w.x = lo ? -p.rail_limit : (hi ? p.rail_limit : w.x);
-        w.xd = (lo || hi) ? T(0) : w.xd;
+        // inelastic rail stop (envkit.py:330-333), branch-free; NaN passes
+        // through unchanged as in the reference's if/elif
+        const bool hit = fabs(w.x) > p.rail_limit;
+        w.x = clamp_nan(w.x, -p.rail_limit, p.rail_limit);
+        w.xd = hit ? T(0) : w.xd;
         refresh(w);
     }
     static __device__ __forceinline__ T reward(const W &w, const Params<T> &, T *info) {
