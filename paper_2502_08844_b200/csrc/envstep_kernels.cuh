@@ -210,7 +210,9 @@ struct RolloutShape {
     static constexpr size_t OFF_RPART = OFF_RING + NG * RING_G;
     static constexpr size_t OFF_ACT = OFF_RPART + (size_t)NG * G * 32 * sizeof(T);
     static constexpr size_t ACT_G = (size_t)G * A * 32 * sizeof(T);
-    static constexpr size_t OFF_TILE = OFF_ACT + NA * ACT_G;
+    static constexpr int NR = 8;                                             // raw action ring (groups)
+    static constexpr size_t OFF_RAW = OFF_ACT + NA * ACT_G;                  // [NR][G][A][32]
+    static constexpr size_t OFF_TILE = OFF_RAW + NR * ACT_G;
     static constexpr size_t OFF_FLAGS = OFF_TILE + (size_t)M * 32 * R * sizeof(T);
     static constexpr size_t OFF_GFLAG = OFF_FLAGS + (size_t)NG * G * 32;   // [NG] u8: fast group
     static constexpr size_t OFF_CTRL = (OFF_GFLAG + NG + 15) / 16 * 16;
@@ -435,20 +437,37 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         bool ok = true;
         const T *arow = actions + (in_range ? i * A : 0);
         const int64_t astep = in_range ? n * A : 0;
-        // two groups of loads in flight ahead of the group being processed
-        T v0[G][A], v1[G][A];
-        auto load = [&](T (&v)[G][A], int g) {
+        // raw actions stream into an NR-group shared-memory ring through
+        // cp.async (each lane copies its own world's row), NR-1 groups ahead
+        constexpr int NR = S::NR;
+        T *raw = reinterpret_cast<T *>(smem + S::OFF_RAW);  // [NR][G][A][32]
+        auto issue = [&](int g) {
+            T *dst = raw + (size_t)(g % NR) * G * A * 32;
             const int k0 = g * G;
+#pragma unroll
+            for (int s = 0; s < G; ++s) {
+                const bool v = in_range && k0 + s < K32;
+#pragma unroll
+                for (int j = 0; j < A; ++j)
+                    cp_async_ca<sizeof(T)>(dst + (s * A + j) * 32 + lane,
+                                           v ? arow + (int64_t)(k0 + s) * astep + j : actions, v);
+            }
+            cp_async_commit();  // one group per call (empty groups past K keep the count)
+        };
+#pragma unroll 1
+        for (int g = 0; g < NR - 1; ++g) issue(g);
+#pragma unroll 1
+        for (int g = 0; g < ngroups; ++g) {
+            issue(g + NR - 1);       // into the slot read in the previous iteration
+            cp_async_wait<NR - 1>();  // this lane's copies of group g have landed
+            const int ab = g % NA;
+            const int k0 = g * G;
+            const T *src_g = raw + (size_t)(g % NR) * G * A * 32;
+            T v[G][A];
 #pragma unroll
             for (int s = 0; s < G; ++s)
 #pragma unroll
-                for (int j = 0; j < A; ++j)
-                    v[s][j] = (in_range && k0 + s < K32) ? __ldg(arow + (k0 + s) * astep + j)
-                                                         : T(0);
-        };
-        auto process = [&](const T (&v)[G][A], int g) {
-            const int ab = g % NA;
-            const int k0 = g * G;
+                for (int j = 0; j < A; ++j) v[s][j] = src_g[(s * A + j) * 32 + lane];
             if (g >= NA) mbar_wait_u32(aempty_b + 8 * ab, (uint32_t)(g / NA - 1) & 1u);
             T *act_g = aring + (size_t)ab * G * A * 32;
 #pragma unroll
@@ -470,18 +489,8 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
                 }
             }
             mbar_arrive_u32(afull_b + 8 * ab);
-        };
-        load(v0, 0);
-        load(v1, 1);
-#pragma unroll 1
-        for (int g = 0; g < ngroups; g += 2) {
-            process(v0, g);
-            load(v0, g + 2);
-            if (g + 1 < ngroups) {
-                process(v1, g + 1);
-                load(v1, g + 3);
-            }
         }
+        cp_async_wait<0>();
     } else {
         // ------------------------------------------------------------ consumers
         const int c = warp < S::STAGER ? warp - 1 : warp - 2;  // consumer index 0..M-1
