@@ -260,3 +260,35 @@ def test_drop_in_surface(pkg):
     assert set(infos[0]) == {"distance"}
     assert env.kernel_launches > 0
     env.close()
+
+
+@pytest.mark.parametrize("n", [1, 37, 1000, 4097])
+@pytest.mark.parametrize("task", ["cartpole-balance", "reacher-easy"])
+def test_ragged_world_counts(pkg, oracle, n, task):
+    """Partial 32-world tiles and unaligned action rows (the cp.async path
+    instead of TMA bulk copies) give the same results as aligned ones."""
+    K = 23
+    A = 2 if task == "reacher-easy" else 1
+    acts = np.random.default_rng(n).uniform(-1.1, 1.1, (K, n, A))
+    ref, (obs, rew, done, trunc, term, mask, info) = _oracle_rollout(
+        oracle, task, n, K, 2, acts, episode_length=9)
+    for dtype, tol, floor in (("float64", 1e-9, 1e-3), ("float32", 1e-3, 0.1)):
+        env = pkg.DeviceBatchEnv(pkg.EnvConfig(task=task, episode_length=9), n, dtype=dtype)
+        env.reset(seed=2)
+        out = env.rollout(torch.as_tensor(acts, device="cuda", dtype=env.dtype), with_info=True)
+        env.check()
+        assert _close(out["obs"].double().cpu().numpy(), obs, 0, floor) < tol
+        assert _close(out["reward"].double().cpu().numpy(), rew, 0, floor) < tol
+        assert _close(out["info"].double().cpu().numpy(), info, 0, floor) < tol
+        np.testing.assert_array_equal(out["trunc"].cpu().numpy(), trunc)
+        np.testing.assert_array_equal(out["terminal_mask"].cpu().numpy(), mask)
+        m = mask
+        assert _close(out["terminal_obs"].double().cpu().numpy()[m], term[m], 0, floor) < tol
+        # an unaligned view of the actions (offset by one element) as well
+        big = torch.zeros(K * n * A + 1, device="cuda", dtype=env.dtype)
+        view = big[1:].view(K, n, A)
+        view.copy_(torch.as_tensor(acts, device="cuda", dtype=env.dtype))
+        env.reset(seed=2)
+        out2 = env.rollout(view, with_info=True)
+        env.check()
+        assert torch.equal(out2["obs"], out["obs"]) and torch.equal(out2["reward"], out["reward"])
