@@ -156,6 +156,97 @@ int dk_env_set_state(dk_env *env, const double *state, const double *target,
 /* Number of kernels this handle has launched (evidence for bench.py). */
 int64_t dk_env_kernel_launches(const dk_env *env);
 
+/* ------------------------------------------------------------------------ */
+/* Locomotion step tail.  These replace per-frame */
+/* pure functions of the reference that the north_star fuses into the step  */
+/* tail; all pointers are DEVICE pointers, element type = dtype (DK_F32 /    */
+/* DK_F64), rows row-major.  Noise draws come from the Philox stream         */
+/* stream_rng(key.seed, key.env_index_offset + world, episode[world], step)  */
+/* (envkit.py:41-49), so they are bit-compatible with the reference given    */
+/* the same generator.                                                       */
+
+/* RewardTermConfig (rewards.py:51-75), same fields, same order. */
+typedef struct dk_reward_config {
+    double w_lin_vel, sigma_lin_vel, w_ang_vel, sigma_ang_vel, w_airtime, airtime_min,
+        airtime_max, w_clearance, w_phase, sigma_phase, swing_height, w_slip, w_orientation,
+        w_torque, w_joint_pos, w_action_rate, w_energy, w_pose, w_termination, w_standstill,
+        w_lin_vel_z, w_ang_vel_xy;
+    int32_t standstill_gated;
+    int32_t reserved;
+} dk_reward_config;
+
+/* A batch of LocomotionFrame (rewards.py:17-44): every field [R, dim] with
+ * R = num_steps * num_worlds rows (step-major).  Flags are uint8.
+ * joint_nominal / joint_default may be one broadcast [J] row (stride 0). */
+typedef struct dk_loco_frames {
+    const void *base_orientation, *base_lin_vel, *base_ang_vel, *joint_pos, *joint_vel,
+        *joint_torque, *foot_height, *foot_height_des, *foot_vel_xy;
+    const uint8_t *foot_contact;
+    const void *airtime;
+    const uint8_t *touchdown;
+    const void *phase, *command, *action, *prev_action, *joint_nominal, *joint_default;
+    const uint8_t *done;
+    int64_t nominal_stride, default_stride;
+} dk_loco_frames;
+
+/* total_reward's RewardBreakdown (rewards.py:84-89, 201-211) and the two
+ * observation slots of build_locomotion_observation (envkit.py:147-193).
+ * terms [R,16] (TERM_REGISTRY order), state_obs [R, 9+3J+3+2F],
+ * privileged_obs [R, 9+3J+3+2F + F+J+3]; terms / obs pointers may be NULL. */
+typedef struct dk_loco_outputs {
+    void *total, *unclipped, *terms, *state_obs, *privileged_obs;
+} dk_loco_outputs;
+
+typedef struct dk_noise_key {
+    uint64_t seed;
+    int64_t env_index_offset;
+    const uint32_t *episode; /* [num_worlds] device, or NULL for episode 0 */
+    uint64_t step;           /* step of row block 0; block k uses step + k */
+} dk_noise_key;
+
+/* rewards.total_reward + envkit.build_locomotion_observation fused.
+ * prev_action [R,J] / command [R,3] default to the frame's fields when NULL;
+ * obs_noise: host double[5] ObservationNoise (gravity, lin_vel, ang_vel,
+ * joint_pos, joint_vel) or NULL; perturbation [R,3] or NULL.
+ * bad_row: device u64 the caller initialises to ~0; receives the first row
+ * whose quaternion is not unit (InvalidInputError, mathcore.py:46-47). */
+int dk_loco_tail(int dtype, int64_t num_steps, int64_t num_worlds, int num_joints, int num_feet,
+                 const dk_reward_config *cfg, const dk_loco_frames *frames,
+                 const void *prev_action, const void *command, const double *obs_noise,
+                 const dk_noise_key *key, const void *perturbation, const dk_loco_outputs *out,
+                 unsigned long long *bad_row, void *stream);
+
+/* action_to_target + pd_torque (envkit.py:111-131).  pd_params (host):
+ * kp, kd, action_scale, torque_limit, range_lo, range_hi, relative(0/1). */
+int dk_loco_pd(int dtype, int64_t n, int num_joints, const double *pd_params,
+               const void *q_default, const void *action, const void *prev_target, const void *q,
+               const void *qd, void *target, void *torque, void *stream);
+
+/* advance_phase + phase_encode (mathcore.py:143-177): phi [n,F], freq/dt [n];
+ * phi_out [n,F] and/or cos_sin_out [n,F,2]. */
+int dk_loco_phase(int dtype, int64_t n, int num_feet, const void *phi, const void *freq,
+                  const void *dt, void *phi_out, void *cos_sin_out, void *stream);
+
+/* progress_clip_reward (envkit.py:196-202); history_max updated in place. */
+int dk_loco_progress_clip(int dtype, int64_t n, const void *raw, void *history_max, void *reward,
+                          void *stream);
+
+/* apply_sensor_noise, uniform kind (randomization.py:88-108), in place on obs
+ * [n, dim]; specs as device arrays (offset, length, scale) in spec order. */
+int dk_dr_sensor_noise(int dtype, int64_t n, int dim, void *obs, int num_specs,
+                       const int32_t *spec_offset, const int32_t *spec_length,
+                       const double *spec_scale, const dk_noise_key *key, void *stream);
+
+/* pose_injection (randomization.py:188-199), in place on pose [n, dim];
+ * bounds device double [dim, 2]; injected [n] u8 (may be NULL). */
+int dk_dr_pose_injection(int dtype, int64_t n, int dim, void *pose, const double *bounds,
+                         double prob, const dk_noise_key *key, uint8_t *injected, void *stream);
+
+/* curriculum_update (randomization.py:224-238), in place on state [n,4] i64 =
+ * (level, successes_at_level, episodes, total_successes). */
+int dk_dr_curriculum(int64_t n, int64_t *state, const uint8_t *success, int64_t max_level,
+                     int64_t promotion_threshold, void *stream);
+
 int dk_abi_version(void);
 const char *dk_last_error(void);
 

@@ -1,0 +1,359 @@
+/*
+ * locomotion.c -- CPU restatement of the reference's locomotion step tail.
+ *
+ * TEST INFRASTRUCTURE ONLY (see oracle.c).  Restates, in float64:
+ *   rewards.py:92-211      swing_height_profile, the 16 reward terms, total_reward
+ *   envkit.py:111-131      action_to_target, pd_torque
+ *   envkit.py:147-193      build_locomotion_observation (+ Philox-keyed uniform noise)
+ *   envkit.py:196-202      progress_clip_reward
+ *   mathcore.py:42-97      quat_check_unit, quat_mul/conj/rotate, project_gravity
+ *   mathcore.py:143-177    wrap_angle, advance_phase, phase_encode
+ *   randomization.py:88-108, 188-199, 224-238  uniform sensor noise, pose injection,
+ *                          curriculum_update
+ * Parity: pinned against tests/golden/loco_golden.npz (generated from the reference
+ * by tests/golden/make_golden_loco.py).  Integer / selection logic is bit-exact;
+ * sums of products are sequential here, where NumPy uses BLAS dot / pairwise sums
+ * and SIMD sin/cos, so those agree to a few ulps (tolerance in the tests).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+/* from oracle.c */
+typedef struct {
+    uint64_t ctr[4];
+    uint64_t key[2];
+    uint64_t buf[4];
+    int pos;
+} orc_philox_state;
+void orc_philox_block(const uint64_t ctr_in[4], const uint64_t key_in[2], uint64_t out[4]);
+
+static void px_init(orc_philox_state *p, uint64_t seed, uint64_t env, int64_t ep, uint64_t step) {
+    p->key[0] = seed;
+    p->key[1] = (env << 32) | ((uint64_t)ep & 0xFFFFFFFFULL);
+    p->ctr[0] = step; p->ctr[1] = p->ctr[2] = p->ctr[3] = 0;
+    p->pos = 4;
+}
+static uint64_t px_next(orc_philox_state *p) {
+    if (p->pos < 4) return p->buf[p->pos++];
+    if (++p->ctr[0] == 0)
+        if (++p->ctr[1] == 0)
+            if (++p->ctr[2] == 0) ++p->ctr[3];
+    orc_philox_block(p->ctr, p->key, p->buf);
+    p->pos = 1;
+    return p->buf[0];
+}
+static double px_uniform(orc_philox_state *p, double lo, double hi) {
+    double range = hi - lo;
+    return lo + range * ((double)(px_next(p) >> 11) * (1.0 / 9007199254740992.0));
+}
+
+/* RewardTermConfig, rewards.py:51-75, field order preserved */
+typedef struct {
+    double w_lin_vel, sigma_lin_vel, w_ang_vel, sigma_ang_vel, w_airtime, airtime_min,
+        airtime_max, w_clearance, w_phase, sigma_phase, swing_height, w_slip, w_orientation,
+        w_torque, w_joint_pos, w_action_rate, w_energy, w_pose, w_termination, w_standstill,
+        w_lin_vel_z, w_ang_vel_xy;
+    int32_t standstill_gated;
+} orc_reward_cfg;
+
+/* Batched frames: every field row-major [N, dim]; nominal / default may be
+ * broadcast ([dim], stride 0). */
+typedef struct {
+    const double *base_orientation, *base_lin_vel, *base_ang_vel, *joint_pos, *joint_vel,
+        *joint_torque, *foot_height, *foot_height_des, *foot_vel_xy;
+    const uint8_t *foot_contact;
+    const double *airtime;
+    const uint8_t *touchdown;
+    const double *phase, *command, *action, *prev_action, *joint_nominal, *joint_default;
+    const uint8_t *done;
+    int64_t nominal_stride, default_stride;
+} orc_frames;
+
+/* mathcore.py:42-48 + 51-61 + 64-66 + 76-79 + 93-97 */
+static int project_gravity(const double *q, double *out) {
+    double n = sqrt(q[0] * q[0] + q[1] * q[1] + q[2] * q[2] + q[3] * q[3]);
+    if (fabs(n - 1.0) > 1e-6) return 0; /* quaternion is not unit length */
+    double c[4] = {q[0], -q[1], -q[2], -q[3]};        /* quat_conj(q) */
+    double p[4] = {0.0, 0.0, 0.0, -1.0};              /* [0, GRAVITY_DIR] */
+    double a[4], r[4];
+    /* quat_mul(c, p) */
+    a[0] = c[0] * p[0] - c[1] * p[1] - c[2] * p[2] - c[3] * p[3];
+    a[1] = c[0] * p[1] + c[1] * p[0] + c[2] * p[3] - c[3] * p[2];
+    a[2] = c[0] * p[2] - c[1] * p[3] + c[2] * p[0] + c[3] * p[1];
+    a[3] = c[0] * p[3] + c[1] * p[2] - c[2] * p[1] + c[3] * p[0];
+    double cc[4] = {c[0], -c[1], -c[2], -c[3]};       /* quat_conj(c) */
+    r[0] = a[0] * cc[0] - a[1] * cc[1] - a[2] * cc[2] - a[3] * cc[3];
+    r[1] = a[0] * cc[1] + a[1] * cc[0] + a[2] * cc[3] - a[3] * cc[2];
+    r[2] = a[0] * cc[2] - a[1] * cc[3] + a[2] * cc[0] + a[3] * cc[1];
+    r[3] = a[0] * cc[3] + a[1] * cc[2] - a[2] * cc[1] + a[3] * cc[0];
+    double m = sqrt(r[1] * r[1] + r[2] * r[2] + r[3] * r[3]);
+    out[0] = r[1] / m; out[1] = r[2] / m; out[2] = r[3] / m;
+    return 1;
+}
+
+int orc_project_gravity(int64_t n, const double *q, double *out, uint8_t *ok) {
+    int bad = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        ok[i] = (uint8_t)project_gravity(q + 4 * i, out + 3 * i);
+        bad += !ok[i];
+    }
+    return bad;
+}
+
+/* rewards.py:97-211.  terms [N,16] in TERM_REGISTRY order; returns the index of the
+ * first frame with a non-unit quaternion, or -1. */
+int64_t orc_total_reward(int64_t n, int nj, int nf, const orc_reward_cfg *c,
+                         const orc_frames *f, double *terms, double *unclipped, double *total) {
+    int64_t first_bad = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        const double *lin = f->base_lin_vel + 3 * i, *ang = f->base_ang_vel + 3 * i;
+        const double *cmd = f->command + 3 * i;
+        const double *jp = f->joint_pos + nj * i, *jv = f->joint_vel + nj * i;
+        const double *jt = f->joint_torque + nj * i;
+        const double *fh = f->foot_height + nf * i, *fhd = f->foot_height_des + nf * i;
+        const double *fv = f->foot_vel_xy + 2 * nf * i, *air = f->airtime + nf * i;
+        const double *ph = f->phase + nf * i;
+        const uint8_t *con = f->foot_contact + nf * i, *td = f->touchdown + nf * i;
+        const double *act = f->action + nj * i, *pact = f->prev_action + nj * i;
+        const double *nom = f->joint_nominal + f->nominal_stride * i;
+        const double *def = f->joint_default + f->default_stride * i;
+        double t[16];
+        double e0 = cmd[0] - lin[0], e1 = cmd[1] - lin[1];
+        t[0] = exp(-(e0 * e0 + e1 * e1) / c->sigma_lin_vel);
+        double ea = cmd[2] - ang[2];
+        t[1] = exp(-(ea * ea) / c->sigma_ang_vel);
+        double s = 0.0;
+        for (int k = 0; k < nf; ++k) {
+            double gain = (air[k] - c->airtime_min) * (td[k] ? 1.0 : 0.0);
+            double hi = c->airtime_max - c->airtime_min;
+            gain = gain < 0.0 ? 0.0 : (gain > hi ? hi : gain);
+            s += gain;
+        }
+        t[2] = s;
+        s = 0.0;
+        for (int k = 0; k < nf; ++k) {
+            double err = fh[k] - fhd[k];
+            double sp = sqrt(fv[2 * k] * fv[2 * k] + fv[2 * k + 1] * fv[2 * k + 1]);
+            s += err * err * sqrt(sp);
+        }
+        t[3] = s;
+        s = 0.0;
+        for (int k = 0; k < nf; ++k) {
+            double sn = sin(ph[k]);
+            double tgt = c->swing_height * (sn > 0.0 ? sn : 0.0);
+            double d = fh[k] - tgt;
+            s += d * d;
+        }
+        t[4] = exp(-s / c->sigma_phase);
+        s = 0.0;
+        for (int k = 0; k < nf; ++k) {
+            double m = con[k] ? 1.0 : 0.0;
+            double a = fv[2 * k] * m, b = fv[2 * k + 1] * m;
+            s += a * a + b * b;
+        }
+        t[5] = s;
+        double g[3];
+        if (!project_gravity(f->base_orientation + 4 * i, g)) {
+            if (first_bad < 0) first_bad = i;
+            g[0] = g[1] = g[2] = NAN;
+        }
+        t[6] = g[0] * g[0] + g[1] * g[1];
+        double tt = 0.0, jpos = 0.0, ar = 0.0, en = 0.0, pose = 0.0, vv = 0.0;
+        for (int j = 0; j < nj; ++j) {
+            tt += jt[j] * jt[j];
+            double d1 = jp[j] - nom[j];
+            jpos += d1 * d1;
+            double d2 = act[j] - pact[j];
+            ar += d2 * d2;
+            en += fabs(jv[j] * jt[j]);
+            double d3 = jp[j] - def[j];
+            pose += d3 * d3;
+            vv += jv[j] * jv[j];
+        }
+        t[7] = tt; t[8] = jpos; t[9] = ar; t[10] = en;
+        t[11] = exp(-pose);
+        t[12] = f->done[i] ? 1.0 : 0.0;
+        double cn = sqrt(cmd[0] * cmd[0] + cmd[1] * cmd[1]);
+        t[13] = !c->standstill_gated ? cn : (cn > 0.1 ? 0.0 : sqrt(vv));
+        t[14] = lin[2] * lin[2];
+        t[15] = ang[0] * ang[0] + ang[1] * ang[1];
+        const double w[16] = {c->w_lin_vel, c->w_ang_vel, c->w_airtime, c->w_clearance,
+                              c->w_phase, c->w_slip, c->w_orientation, c->w_torque,
+                              c->w_joint_pos, c->w_action_rate, c->w_energy, c->w_pose,
+                              c->w_termination, c->w_standstill, c->w_lin_vel_z,
+                              c->w_ang_vel_xy};
+        double u = 0.0;
+        for (int k = 0; k < 16; ++k) {
+            terms[16 * i + k] = t[k];
+            u += w[k] * t[k];
+        }
+        unclipped[i] = u;
+        total[i] = 0.0 > u ? 0.0 : u;  /* max(unclipped, 0.0) */
+    }
+    return first_bad;
+}
+
+/* envkit.py:147-193.  state [N, 9 + 3*nj + 3 + 2*nf], priv [N, state + nf + nj + 3].
+ * noise[5] = (gravity, lin_vel, ang_vel, joint_pos, joint_vel) scales; the stream of
+ * world i is stream_rng(seed, env0 + i, episode, step).  pert [N,3] or NULL. */
+int64_t orc_loco_obs(int64_t n, int nj, int nf, const orc_frames *f, const double *prev_action,
+                     const double *command, const double *noise, uint64_t seed, int64_t env0,
+                     int64_t episode, uint64_t step, const double *pert, double *state,
+                     double *priv) {
+    const int S = 9 + 3 * nj + 3 + 2 * nf, P = S + nf + nj + 3;
+    int64_t first_bad = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        double clean[512];
+        int o = 0;
+        if (!project_gravity(f->base_orientation + 4 * i, clean)) {
+            if (first_bad < 0) first_bad = i;
+            clean[0] = clean[1] = clean[2] = NAN;
+        }
+        o = 3;
+        for (int k = 0; k < 3; ++k) clean[o++] = f->base_lin_vel[3 * i + k];
+        for (int k = 0; k < 3; ++k) clean[o++] = f->base_ang_vel[3 * i + k];
+        for (int k = 0; k < nj; ++k) clean[o++] = f->joint_pos[nj * i + k];
+        for (int k = 0; k < nj; ++k) clean[o++] = f->joint_vel[nj * i + k];
+        for (int k = 0; k < nj; ++k) clean[o++] = prev_action[nj * i + k];
+        for (int k = 0; k < 3; ++k) clean[o++] = command[3 * i + k];
+        for (int k = 0; k < nf; ++k) {
+            clean[o++] = cos(f->phase[nf * i + k]);
+            clean[o++] = sin(f->phase[nf * i + k]);
+        }
+        double *st = state + (int64_t)S * i;
+        memcpy(st, clean, sizeof(double) * S);
+        if (noise) {
+            orc_philox_state px;
+            px_init(&px, seed, (uint64_t)(env0 + i), episode, step);
+            const int start[5] = {0, 3, 6, 9, 9 + nj}, len[5] = {3, 3, 3, nj, nj};
+            for (int g = 0; g < 5; ++g) {
+                double s = noise[g];
+                if (s > 0)
+                    for (int k = 0; k < len[g]; ++k)
+                        st[start[g] + k] = st[start[g] + k] + px_uniform(&px, -s, s);
+            }
+        }
+        double *pr = priv + (int64_t)P * i;
+        memcpy(pr, clean, sizeof(double) * S);
+        o = S;
+        for (int k = 0; k < nf; ++k) pr[o++] = f->foot_contact[nf * i + k] ? 1.0 : 0.0;
+        for (int k = 0; k < nj; ++k) pr[o++] = f->joint_torque[nj * i + k];
+        for (int k = 0; k < 3; ++k) pr[o++] = pert ? pert[3 * i + k] : 0.0;
+    }
+    return first_bad;
+}
+
+/* envkit.py:111-131.  params = (kp, kd, action_scale, torque_limit, range_lo, range_hi,
+ * relative); q_default [nj]. */
+void orc_pd(int64_t n, int nj, const double *params, const double *q_default, const double *a,
+            const double *prev_target, const double *q, const double *v, double *target,
+            double *torque) {
+    double kp = params[0], kd = params[1], sc = params[2], lim = params[3];
+    double lo = params[4], hi = params[5];
+    int rel = params[6] != 0.0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int j = 0; j < nj; ++j) {
+            int64_t e = i * nj + j;
+            double t;
+            if (!rel) {
+                t = q_default[j] + sc * a[e];
+            } else {
+                t = prev_target[e] + sc * a[e];
+                t = t < lo ? lo : t;  /* np.clip = minimum(maximum(x, lo), hi) */
+                t = t > hi ? hi : t;
+            }
+            target[e] = t;
+            double tau = kp * (t - q[e]) - kd * v[e];
+            tau = tau < -lim ? -lim : tau;
+            tau = tau > lim ? lim : tau;
+            torque[e] = tau;
+        }
+}
+
+/* envkit.py:196-202 */
+void orc_progress_clip(int64_t n, const double *raw, const double *hist, double *reward,
+                       double *new_hist) {
+    for (int64_t i = 0; i < n; ++i) {
+        double d = raw[i] - hist[i];
+        reward[i] = 0.0 > d ? 0.0 : d;          /* max(raw - hist, 0.0) */
+        new_hist[i] = raw[i] > hist[i] ? raw[i] : hist[i];  /* max(hist, raw) */
+    }
+}
+
+/* mathcore.py:143-177 */
+static double wrap(double phi) {
+    const double two_pi = 2.0 * M_PI;
+    double x = phi + M_PI;
+    double m = fmod(x, two_pi);  /* npy_divmod: result takes the divisor's sign */
+    if (m != 0.0) {
+        if ((m < 0) != (two_pi < 0)) m += two_pi;
+    } else {
+        m = copysign(0.0, two_pi);
+    }
+    return m - M_PI;
+}
+void orc_wrap_angle(int64_t n, const double *in, double *out) {
+    for (int64_t i = 0; i < n; ++i) out[i] = wrap(in[i]);
+}
+void orc_advance_phase(int64_t n, int nf, const double *phi, const double *freq,
+                       const double *dt, double *out) {
+    const double two_pi = 2.0 * M_PI;
+    for (int64_t i = 0; i < n; ++i)
+        for (int k = 0; k < nf; ++k) out[i * nf + k] = wrap(phi[i * nf + k] + two_pi * freq[i] * dt[i]);
+}
+
+/* randomization.py:88-108 (uniform kind): specs given as (offset, length, scale) triples
+ * over one flat observation row; stream of row i = stream_rng(seed, env0 + i, ep, step). */
+void orc_sensor_noise(int64_t n, int dim, const double *obs, int nspec, const int32_t *spec_off,
+                      const int32_t *spec_len, const double *spec_scale, uint64_t seed,
+                      int64_t env0, int64_t episode, uint64_t step, double *out) {
+    for (int64_t i = 0; i < n; ++i) {
+        memcpy(out + (int64_t)dim * i, obs + (int64_t)dim * i, sizeof(double) * dim);
+        orc_philox_state px;
+        px_init(&px, seed, (uint64_t)(env0 + i), episode, step);
+        for (int s = 0; s < nspec; ++s) {
+            double sc = spec_scale[s];
+            if (sc == 0.0) continue;
+            for (int k = 0; k < spec_len[s]; ++k) {
+                double *x = out + (int64_t)dim * i + spec_off[s] + k;
+                *x = *x + px_uniform(&px, -sc, sc);
+            }
+        }
+    }
+}
+
+/* randomization.py:188-199 */
+void orc_pose_injection(int64_t n, int dim, const double *pose, const double *bounds /*[dim,2]*/,
+                        double prob, uint64_t seed, int64_t env0, int64_t episode,
+                        uint64_t step, double *out) {
+    for (int64_t i = 0; i < n; ++i) {
+        orc_philox_state px;
+        px_init(&px, seed, (uint64_t)(env0 + i), episode, step);
+        if (px_uniform(&px, 0.0, 1.0) < prob) {
+            for (int k = 0; k < dim; ++k)
+                out[i * dim + k] = px_uniform(&px, bounds[2 * k], bounds[2 * k + 1]);
+        } else {
+            memcpy(out + i * dim, pose + i * dim, sizeof(double) * dim);
+        }
+    }
+}
+
+/* randomization.py:206-238: state = (level, successes_at_level, episodes,
+ * total_successes); cfg = (max_level, promotion_threshold). */
+void orc_curriculum(int64_t n, int64_t *state, const uint8_t *success, int64_t max_level,
+                    int64_t threshold) {
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t *s = state + 4 * i;
+        s[2] += 1;
+        if (!success[i]) continue;
+        int64_t succ = s[1] + 1, tot = s[3] + 1;
+        if (succ >= threshold && s[0] < max_level) {
+            s[0] += 1;
+            s[1] = 0;
+        } else {
+            s[1] = succ;
+        }
+        s[3] = tot;
+    }
+}

@@ -40,6 +40,37 @@ class EnvConfigC(ctypes.Structure):
     ]
 
 
+REWARD_FIELDS = ("w_lin_vel", "sigma_lin_vel", "w_ang_vel", "sigma_ang_vel", "w_airtime",
+                 "airtime_min", "airtime_max", "w_clearance", "w_phase", "sigma_phase",
+                 "swing_height", "w_slip", "w_orientation", "w_torque", "w_joint_pos",
+                 "w_action_rate", "w_energy", "w_pose", "w_termination", "w_standstill",
+                 "w_lin_vel_z", "w_ang_vel_xy")
+FRAME_FIELDS = ("base_orientation", "base_lin_vel", "base_ang_vel", "joint_pos", "joint_vel",
+                "joint_torque", "foot_height", "foot_height_des", "foot_vel_xy", "foot_contact",
+                "airtime", "touchdown", "phase", "command", "action", "prev_action",
+                "joint_nominal", "joint_default", "done")
+
+
+class RewardConfigC(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_double) for f in REWARD_FIELDS] + [
+        ("standstill_gated", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class LocoFramesC(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in FRAME_FIELDS] + [
+        ("nominal_stride", ctypes.c_int64), ("default_stride", ctypes.c_int64)]
+
+
+class LocoOutputsC(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_void_p) for f in ("total", "unclipped", "terms", "state_obs",
+                                              "privileged_obs")]
+
+
+class NoiseKeyC(ctypes.Structure):
+    _fields_ = [("seed", ctypes.c_uint64), ("env_index_offset", ctypes.c_int64),
+                ("episode", ctypes.c_void_p), ("step", ctypes.c_uint64)]
+
+
 _vp = ctypes.c_void_p
 _u8p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -66,6 +97,21 @@ _SIGS = {
     "dk_env_get_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _u8p]),
     "dk_env_set_state": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _u8p]),
     "dk_env_kernel_launches": (ctypes.c_int64, [_vp]),
+    "dk_loco_tail": (ctypes.c_int, [ctypes.c_int, _i64, _i64, ctypes.c_int, ctypes.c_int,
+                                    ctypes.POINTER(RewardConfigC), ctypes.POINTER(LocoFramesC),
+                                    _vp, _vp, _vp, ctypes.POINTER(NoiseKeyC), _vp,
+                                    ctypes.POINTER(LocoOutputsC), _vp, _vp]),
+    "dk_loco_pd": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                  _vp, _vp, _vp]),
+    "dk_loco_phase": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
+                                     _vp]),
+    "dk_loco_progress_clip": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp, _vp]),
+    "dk_dr_sensor_noise": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_int,
+                                          _vp, _vp, _vp, ctypes.POINTER(NoiseKeyC), _vp]),
+    "dk_dr_pose_injection": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp,
+                                            ctypes.c_double, ctypes.POINTER(NoiseKeyC), _vp,
+                                            _vp]),
+    "dk_dr_curriculum": (ctypes.c_int, [_i64, _vp, _vp, _i64, _i64, _vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -26,7 +26,10 @@ COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relax
 UNITS = {
     "envstep_f32.cu": [],
     "envstep_f64.cu": ["--fmad=false"],
+    "locomotion_f32.cu": [],
+    "locomotion_f64.cu": ["--fmad=false"],
     "capi.cu": [],
+    "capi_loco.cu": [],
 }
 
 

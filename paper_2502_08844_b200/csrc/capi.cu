@@ -216,6 +216,7 @@ int check_env(const dk_env *e) {
 extern "C" {
 
 int dk_abi_version(void) { return DK_ABI_VERSION; }
+int dk_internal_fail(int code, const char *msg) { return fail(code, "%s", msg); }
 const char *dk_last_error(void) { return g_last_error.c_str(); }
 
 int dk_task_id(const char *name) {

@@ -1,0 +1,435 @@
+// locomotion.cuh -- the locomotion step tail at Go1 shape.
+//
+// loco_tail_kernel fuses, per world and step, the reward table
+// (rewards.total_reward + the 16 terms, rewards.py:97-211) with the observation
+// builder (envkit.build_locomotion_observation, envkit.py:147-193: projected
+// gravity, phase encoding, Philox-keyed uniform sensor noise, privileged slot),
+// so each frame is read from HBM once and every output is written once.
+// One thread owns one (step, world) row; per-warp shared-memory tiles turn the
+// row-major outputs into contiguous row stores.  The joint / foot loops are
+// runtime-sized (Go1: 12 joints, 4 feet; bipeds; hands), accumulating in
+// registers in the reference's term order.
+#pragma once
+#include "envmath.cuh"
+
+namespace dk {
+
+template <typename T>
+struct LocoFrames {  // rows [K*N, dim]; nominal / default: stride 0 = broadcast [dim]
+    const T *q, *lin, *ang, *jpos, *jvel, *jtau, *fh, *fhd, *fvel;
+    const uint8_t *contact;
+    const T *air;
+    const uint8_t *touchdown;
+    const T *phase, *cmd, *act, *pact, *nom, *def;
+    const uint8_t *done;
+    int64_t nom_stride, def_stride;
+};
+
+template <typename T>
+struct RewardCfg {  // RewardTermConfig (rewards.py:51-75)
+    T w[16];        // weights in TERM_REGISTRY order (rewards.py:181-198)
+    T sigma_lin, sigma_ang, airtime_min, airtime_max, sigma_phase, swing_height;
+    int gated;
+};
+
+template <typename T>
+struct LocoOut {
+    T *total, *unclipped, *terms, *state, *priv;  // terms / state / priv may be null
+};
+
+struct LocoArgs {
+    int64_t K, N;       // steps x worlds rows
+    int nj, nf;
+    uint64_t seed;
+    int64_t env0;
+    uint64_t step0;
+    const uint32_t *episode;  // [N] or null (episode 0)
+    double noise[5];          // gravity, lin_vel, ang_vel, joint_pos, joint_vel
+    int has_noise;
+};
+
+// mathcore.project_gravity (mathcore.py:93-97) incl. quat_check_unit (42-48);
+// returns false for a non-unit quaternion.
+template <typename T>
+__device__ __forceinline__ bool project_gravity(const T *q4, T *g) {
+    const T w = q4[0], x = q4[1], y = q4[2], z = q4[3];
+    const T nrm = RealOps<T>::sqrt_(w * w + x * x + y * y + z * z);
+    if (fabs(nrm - T(1)) > T(1e-6)) return false;  // (NaN passes, as in the reference)
+    // quat_rotate(conj(q), (0,0,-1)) written out like quat_mul(quat_mul(c, p), conj(c))
+    const T c0 = w, c1 = -x, c2 = -y, c3 = -z;
+    const T a0 = c0 * T(0) - c1 * T(0) - c2 * T(0) - c3 * T(-1);
+    const T a1 = c0 * T(0) + c1 * T(0) + c2 * T(-1) - c3 * T(0);
+    const T a2 = c0 * T(0) - c1 * T(-1) + c2 * T(0) + c3 * T(0);
+    const T a3 = c0 * T(-1) + c1 * T(0) - c2 * T(0) + c3 * T(0);
+    const T d1 = -c1, d2 = -c2, d3 = -c3;
+    const T r1 = a0 * d1 + a1 * c0 + a2 * d3 - a3 * d2;
+    const T r2 = a0 * d2 - a1 * d3 + a2 * c0 + a3 * d1;
+    const T r3 = a0 * d3 + a1 * d2 - a2 * d1 + a3 * c0;
+    const T m = RealOps<T>::sqrt_(r1 * r1 + r2 * r2 + r3 * r3);
+    g[0] = r1 / m; g[1] = r2 / m; g[2] = r3 / m;
+    return true;
+}
+
+template <typename T>
+__device__ __forceinline__ T rexp(T x) { return RealOps<T>::exp_(x); }
+
+template <typename T>
+__device__ __forceinline__ void rsincos(T x, T *s, T *c) { RealOps<T>::sincos_(x, s, c); }
+
+template <typename T>
+__global__ void __launch_bounds__(128)
+loco_tail_kernel(LocoFrames<T> f, const T *__restrict__ prev_action, const T *__restrict__ command,
+                 const T *__restrict__ pert, RewardCfg<T> c, LocoArgs a, LocoOut<T> out,
+                 unsigned long long *err) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int nj = a.nj, nf = a.nf;
+    const int S = 9 + 3 * nj + 3 + 2 * nf;  // state slot
+    const int P = S + nf + nj + 3;          // privileged slot
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    T *tile = reinterpret_cast<T *>(smem_raw) + (size_t)warp * 32 * P;
+    T *row = tile + (size_t)lane * P;
+    const int64_t rows = a.K * a.N;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t r0 = r - lane;  // first row of this warp
+    const bool live = r < rows;
+
+    if (live) {
+        const T *lin = f.lin + 3 * r, *ang = f.ang + 3 * r;
+        const T *cmd = (command ? command : f.cmd) + 3 * r;
+        const T *pa = (prev_action ? prev_action : f.pact) + (int64_t)nj * r;
+        const T *nom = f.nom + f.nom_stride * r, *def = f.def + f.def_stride * r;
+        T t[16];
+        // lin / ang velocity tracking (rewards.py:97-104): from the FRAME's command
+        const T *fcmd = f.cmd + 3 * r;
+        const T e0 = fcmd[0] - lin[0], e1 = fcmd[1] - lin[1];
+        t[0] = rexp(-(e0 * e0 + e1 * e1) / c.sigma_lin);
+        const T ea = fcmd[2] - ang[2];
+        t[1] = rexp(-(ea * ea) / c.sigma_ang);
+        // projected gravity -> orientation term + obs
+        T g[3];
+        if (!project_gravity(f.q + 4 * r, g)) {
+            atomicMin(err, (unsigned long long)r);  // InvalidInputError (mathcore.py:46-47)
+            g[0] = g[1] = g[2] = T(NAN);
+        }
+        t[6] = g[0] * g[0] + g[1] * g[1];
+        int o = 0;
+        row[o++] = g[0]; row[o++] = g[1]; row[o++] = g[2];
+        for (int k = 0; k < 3; ++k) row[o++] = lin[k];
+        for (int k = 0; k < 3; ++k) row[o++] = ang[k];
+        // joints: terms 7-11, 13 (gated) + obs joint_pos / joint_vel / prev_action / torque
+        T tt = 0, jp = 0, ar = 0, en = 0, pose = 0, vv = 0;
+        const T *q = f.jpos + (int64_t)nj * r, *qd = f.jvel + (int64_t)nj * r;
+        const T *tau = f.jtau + (int64_t)nj * r, *act = f.act + (int64_t)nj * r;
+        const T *fpa = f.pact + (int64_t)nj * r;
+        const int o_jp = 9, o_jv = 9 + nj, o_pa = 9 + 2 * nj, o_cmd = 9 + 3 * nj;
+        const int o_ph = o_cmd + 3, o_con = S, o_tau = S + nf, o_pert = S + nf + nj;
+        for (int j = 0; j < nj; ++j) {
+            const T qj = __ldg(q + j), vj = __ldg(qd + j), tj = __ldg(tau + j);
+            tt = tt + tj * tj;
+            const T d1 = qj - __ldg(nom + j);
+            jp = jp + d1 * d1;
+            const T d2 = __ldg(act + j) - __ldg(fpa + j);
+            ar = ar + d2 * d2;
+            en = en + fabs(vj * tj);
+            const T d3 = qj - __ldg(def + j);
+            pose = pose + d3 * d3;
+            vv = vv + vj * vj;
+            row[o_jp + j] = qj;
+            row[o_jv + j] = vj;
+            row[o_pa + j] = __ldg(pa + j);
+            row[o_tau + j] = tj;
+        }
+        t[7] = tt; t[8] = jp; t[9] = ar; t[10] = en;
+        t[11] = rexp(-pose);
+        for (int k = 0; k < 3; ++k) row[o_cmd + k] = cmd[k];
+        // feet: terms 2-5 + obs phase cos/sin and contact flags
+        T air_s = 0, clr = 0, ph = 0, slip = 0;
+        const T *air = f.air + (int64_t)nf * r, *fh = f.fh + (int64_t)nf * r;
+        const T *fhd = f.fhd + (int64_t)nf * r, *fv = f.fvel + (int64_t)2 * nf * r;
+        const T *phase = f.phase + (int64_t)nf * r;
+        const uint8_t *td = f.touchdown + (int64_t)nf * r, *con = f.contact + (int64_t)nf * r;
+        const T span = c.airtime_max - c.airtime_min;
+        for (int k = 0; k < nf; ++k) {
+            T gain = (__ldg(air + k) - c.airtime_min) * (td[k] ? T(1) : T(0));
+            gain = gain < T(0) ? T(0) : (gain > span ? span : gain);  // np.clip
+            air_s = air_s + gain;
+            const T hk = __ldg(fh + k), err_h = hk - __ldg(fhd + k);
+            const T vx = __ldg(fv + 2 * k), vy = __ldg(fv + 2 * k + 1);
+            const T sp = RealOps<T>::sqrt_(vx * vx + vy * vy);
+            clr = clr + err_h * err_h * RealOps<T>::sqrt_(sp);
+            T sn, cs;
+            rsincos(__ldg(phase + k), &sn, &cs);
+            const T tgt = c.swing_height * (sn > T(0) ? sn : T(0));  // swing_height_profile
+            const T dz = hk - tgt;
+            ph = ph + dz * dz;
+            const T m = con[k] ? T(1) : T(0);
+            const T cx = vx * m, cy = vy * m;
+            slip = slip + (cx * cx + cy * cy);
+            row[o_ph + 2 * k] = cs;
+            row[o_ph + 2 * k + 1] = sn;
+            row[o_con + k] = m;
+        }
+        t[2] = air_s; t[3] = clr; t[4] = rexp(-ph / c.sigma_phase); t[5] = slip;
+        t[12] = f.done[r] ? T(1) : T(0);
+        const T cn = RealOps<T>::sqrt_(fcmd[0] * fcmd[0] + fcmd[1] * fcmd[1]);
+        t[13] = !c.gated ? cn : (cn > T(0.1) ? T(0) : RealOps<T>::sqrt_(vv));
+        t[14] = lin[2] * lin[2];
+        t[15] = ang[0] * ang[0] + ang[1] * ang[1];
+        T u = T(0);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) u = u + c.w[k] * t[k];  // sum(weighted) in registry order
+        out.unclipped[r] = u;
+        out.total[r] = T(0) > u ? T(0) : u;                  // max(unclipped, 0.0)
+        if (out.terms) {
+#pragma unroll
+            for (int k = 0; k < 16; ++k) out.terms[16 * r + k] = t[k];
+        }
+        for (int k = 0; k < 3; ++k) row[o_pert + k] = pert ? pert[3 * r + k] : T(0);
+    }
+    __syncwarp();
+    const int64_t nrow = rows - r0 < 32 ? rows - r0 : 32;
+    if (out.priv) {  // privileged slot: the clean signals + contacts, torques, perturbation
+        for (int rr = 0; rr < nrow; ++rr) {
+            T *dst = out.priv + (r0 + rr) * P;
+            for (int col = lane; col < P; col += 32) dst[col] = tile[rr * P + col];
+        }
+    }
+    if (live && a.has_noise) {
+        // uniform noise per group, drawn in the reference's order from
+        // stream_rng(seed, env, episode, step) (envkit.py:41-49, 176-180)
+        const int64_t k = r / a.N, i = r - k * a.N;
+        Philox4x64 rng;
+        rng.init(a.seed, (uint64_t)(a.env0 + i), a.episode ? a.episode[i] : 0u,
+                 a.step0 + (uint64_t)k);
+        const int start[5] = {0, 3, 6, 9, 9 + nj}, len[5] = {3, 3, 3, nj, nj};
+        for (int gi = 0; gi < 5; ++gi) {
+            const double s = a.noise[gi];
+            if (s > 0)
+                for (int e = 0; e < len[gi]; ++e)
+                    row[start[gi] + e] = row[start[gi] + e] + (T)rng.uniform(-s, s);
+        }
+    }
+    __syncwarp();
+    if (out.state) {
+        for (int rr = 0; rr < nrow; ++rr) {
+            T *dst = out.state + (r0 + rr) * S;
+            for (int col = lane; col < S; col += 32) dst[col] = tile[rr * P + col];
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Small batched kernels (one thread per element / row).
+
+// action_to_target + pd_torque (envkit.py:111-131); a, prev, q, v [N, J]
+template <typename T>
+__global__ void pd_kernel(int64_t n, int nj, T kp, T kd, T scale, T limit, T lo, T hi, int relative,
+                          const T *q_default, const T *a, const T *prev, const T *q, const T *v,
+                          T *target, T *torque) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * nj) return;
+    const int j = (int)(e % nj);
+    T t;
+    if (!relative) {
+        t = q_default[j] + scale * a[e];
+    } else {
+        t = prev[e] + scale * a[e];
+        t = t < lo ? lo : t;  // np.clip(target, lo, hi)
+        t = t > hi ? hi : t;
+    }
+    if (target) target[e] = t;
+    T tau = kp * (t - q[e]) - kd * v[e];
+    tau = tau < -limit ? -limit : tau;
+    tau = tau > limit ? limit : tau;
+    torque[e] = tau;
+}
+
+// wrap_angle(phi + 2*pi*f*dt) (mathcore.py:143-171): NumPy divmod semantics
+template <typename T>
+__device__ __forceinline__ T wrap_angle_dev(T phi) {
+    const T two_pi = T(6.283185307179586), pi = T(3.141592653589793);
+    const T x = phi + pi;
+    T m = fmod(x, two_pi);
+    if (m != T(0)) {
+        if (m < T(0)) m = m + two_pi;
+    } else {
+        m = T(0);
+    }
+    return m - pi;
+}
+
+template <typename T>
+__global__ void phase_kernel(int64_t n, int nf, const T *phi, const T *freq, const T *dt,
+                             T *out_phi, T *out_cs) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * nf) return;
+    const int64_t i = e / nf;
+    const T np_ = wrap_angle_dev(phi[e] + T(6.283185307179586) * freq[i] * dt[i]);
+    if (out_phi) out_phi[e] = np_;
+    if (out_cs) {  // phase_encode (mathcore.py:174-177)
+        T s, c;
+        RealOps<T>::sincos_(np_, &s, &c);
+        out_cs[2 * e] = c;
+        out_cs[2 * e + 1] = s;
+    }
+}
+
+// progress_clip_reward (envkit.py:196-202)
+template <typename T>
+__global__ void progress_kernel(int64_t n, const T *raw, T *hist, T *reward) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const T h = hist[i], x = raw[i], d = x - h;
+    reward[i] = T(0) > d ? T(0) : d;
+    hist[i] = x > h ? x : h;
+}
+
+// apply_sensor_noise, uniform kind (randomization.py:88-108), in place on rows [N, dim]
+template <typename T>
+__global__ void sensor_noise_kernel(int64_t n, int dim, T *obs, int nspec, const int *off,
+                                    const int *len, const double *scale, uint64_t seed,
+                                    int64_t env0, const uint32_t *episode, uint64_t step) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Philox4x64 rng;
+    rng.init(seed, (uint64_t)(env0 + i), episode ? episode[i] : 0u, step);
+    for (int s = 0; s < nspec; ++s) {
+        const double sc = scale[s];
+        if (sc == 0.0) continue;
+        for (int k = 0; k < len[s]; ++k) {
+            T *x = obs + i * dim + off[s] + k;
+            *x = *x + (T)rng.uniform(-sc, sc);
+        }
+    }
+}
+
+// pose_injection (randomization.py:188-199), in place on rows [N, dim]; bounds [dim, 2]
+template <typename T>
+__global__ void pose_injection_kernel(int64_t n, int dim, T *pose, const double *bounds,
+                                      double prob, uint64_t seed, int64_t env0,
+                                      const uint32_t *episode, uint64_t step, uint8_t *injected) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    Philox4x64 rng;
+    rng.init(seed, (uint64_t)(env0 + i), episode ? episode[i] : 0u, step);
+    const bool inj = rng.uniform(0.0, 1.0) < prob;
+    if (inj)
+        for (int k = 0; k < dim; ++k) pose[i * dim + k] = (T)rng.uniform(bounds[2 * k], bounds[2 * k + 1]);
+    if (injected) injected[i] = inj ? 1 : 0;
+}
+
+// curriculum_update (randomization.py:224-238); state [N,4] = (level,
+// successes_at_level, episodes, total_successes)
+static __global__ void curriculum_kernel(int64_t n, int64_t *state, const uint8_t *success,
+                                  int64_t max_level, int64_t threshold) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t *s = state + 4 * i;
+    s[2] += 1;
+    if (!success[i]) return;
+    const int64_t succ = s[1] + 1;
+    if (succ >= threshold && s[0] < max_level) {
+        s[0] += 1;
+        s[1] = 0;
+    } else {
+        s[1] = succ;
+    }
+    s[3] += 1;
+}
+
+}  // namespace dk
+
+namespace dk {
+
+template <typename T>
+cudaError_t launch_loco_tail(const LocoFrames<T> &f, const T *prev_action, const T *command,
+                             const T *pert, const RewardCfg<T> &c, const LocoArgs &a,
+                             const LocoOut<T> &out, unsigned long long *err, cudaStream_t st) {
+    const int64_t rows = a.K * a.N;
+    if (rows == 0) return cudaSuccess;
+    const int P = 9 + 3 * a.nj + 3 + 2 * a.nf + a.nf + a.nj + 3;
+    const size_t per_warp = (size_t)32 * P * sizeof(T);
+    int warps = 4;
+    while (warps > 1 && warps * per_warp > 200 * 1024) warps /= 2;
+    const size_t smem = warps * per_warp;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(loco_tail_kernel<T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    const int bs = 32 * warps;
+    loco_tail_kernel<T><<<(unsigned)((rows + bs - 1) / bs), bs, smem, st>>>(
+        f, prev_action, command, pert, c, a, out, err);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_pd(int64_t n, int nj, T kp, T kd, T scale, T limit, T lo, T hi, int relative,
+                      const T *q_default, const T *a, const T *prev, const T *q, const T *v,
+                      T *target, T *torque, cudaStream_t st) {
+    const int64_t m = n * nj;
+    if (m == 0) return cudaSuccess;
+    pd_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, st>>>(n, nj, kp, kd, scale, limit, lo, hi,
+                                                             relative, q_default, a, prev, q, v,
+                                                             target, torque);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_phase(int64_t n, int nf, const T *phi, const T *freq, const T *dt, T *out_phi,
+                         T *out_cs, cudaStream_t st) {
+    const int64_t m = n * nf;
+    if (m == 0) return cudaSuccess;
+    phase_kernel<T><<<(unsigned)((m + 255) / 256), 256, 0, st>>>(n, nf, phi, freq, dt, out_phi,
+                                                                out_cs);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_progress(int64_t n, const T *raw, T *hist, T *reward, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    progress_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, raw, hist, reward);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_sensor_noise(int64_t n, int dim, T *obs, int nspec, const int *off,
+                                const int *len, const double *scale, uint64_t seed, int64_t env0,
+                                const uint32_t *episode, uint64_t step, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    sensor_noise_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        n, dim, obs, nspec, off, len, scale, seed, env0, episode, step);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_pose_injection(int64_t n, int dim, T *pose, const double *bounds, double prob,
+                                  uint64_t seed, int64_t env0, const uint32_t *episode,
+                                  uint64_t step, uint8_t *injected, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    pose_injection_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        n, dim, pose, bounds, prob, seed, env0, episode, step, injected);
+    return cudaGetLastError();
+}
+
+#define DK_LOCO_LAUNCHERS(EXT, T)                                                                \
+    EXT template cudaError_t launch_loco_tail<T>(const LocoFrames<T> &, const T *, const T *,    \
+                                                 const T *, const RewardCfg<T> &,               \
+                                                 const LocoArgs &, const LocoOut<T> &,          \
+                                                 unsigned long long *, cudaStream_t);           \
+    EXT template cudaError_t launch_pd<T>(int64_t, int, T, T, T, T, T, T, int, const T *,        \
+                                          const T *, const T *, const T *, const T *, T *, T *, \
+                                          cudaStream_t);                                        \
+    EXT template cudaError_t launch_phase<T>(int64_t, int, const T *, const T *, const T *, T *, \
+                                             T *, cudaStream_t);                                \
+    EXT template cudaError_t launch_progress<T>(int64_t, const T *, T *, T *, cudaStream_t);     \
+    EXT template cudaError_t launch_sensor_noise<T>(int64_t, int, T *, int, const int *,         \
+                                                    const int *, const double *, uint64_t,      \
+                                                    int64_t, const uint32_t *, uint64_t,        \
+                                                    cudaStream_t);                              \
+    EXT template cudaError_t launch_pose_injection<T>(int64_t, int, T *, const double *, double, \
+                                                      uint64_t, int64_t, const uint32_t *,      \
+                                                      uint64_t, uint8_t *, cudaStream_t);
+
+}  // namespace dk
