@@ -23,6 +23,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import os
 import platform
 import sys
@@ -53,6 +54,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=20_000)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-tail", action="store_true", help="skip the Go1-shape step-tail line")
     return ap.parse_args()
 
 
@@ -310,6 +312,10 @@ def run_b200(args, rank, world, local_rank, dist):
     if args.e2e_steps > 0:
         e2e = measure_e2e(env, args, dev, dist, A, O, I, esz, world)
 
+    tail = None
+    if not args.no_tail:
+        tail = bench_go1_tail(args, dev, rank)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
@@ -345,11 +351,131 @@ def run_b200(args, rank, world, local_rank, dist):
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": gpu_launches,
+            "go1_tail": tail,
             "clocks": clocks.summary(),
             "library": _native.LIB_PATH,
         }
         print(json.dumps(line), flush=True)
     env.close()
+
+
+def synthetic_frames(R, J, F, dev, dtype, seed):
+    """R LocomotionFrames drawn like gaitgen.random_frame (gaitgen.py:104-129),
+    generated on the device (the reference is not available on the GPU box)."""
+    import torch
+
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+
+    def nrm(shape, s=1.0):
+        return torch.randn(shape, generator=g, device=dev, dtype=torch.float64) * s
+
+    def uni(shape, lo, hi):
+        return torch.rand(shape, generator=g, device=dev, dtype=torch.float64) * (hi - lo) + lo
+
+    q = nrm((R, 4))
+    q = q / q.norm(dim=1, keepdim=True)
+    f = {"base_orientation": q, "base_lin_vel": nrm((R, 3)), "base_ang_vel": nrm((R, 3)),
+         "joint_pos": nrm((R, J)), "joint_vel": nrm((R, J), 2.0),
+         "joint_torque": nrm((R, J), 5.0), "foot_height": uni((R, F), 0, 0.15),
+         "foot_height_des": uni((R, F), 0, 0.15), "foot_vel_xy": nrm((R, F, 2), 0.5),
+         "foot_contact": uni((R, F), 0, 1) < 0.5, "airtime": uni((R, F), 0, 0.8),
+         "touchdown": uni((R, F), 0, 1) < 0.3, "phase": uni((R, F), -math.pi, math.pi),
+         "command": nrm((R, 3), 0.5), "action": uni((R, J), -1, 1),
+         "prev_action": uni((R, J), -1, 1), "joint_nominal": nrm((J,), 0.2),
+         "joint_default": nrm((J,), 0.2), "done": uni((R,), 0, 1) < 0.1}
+    for k, v in f.items():
+        f[k] = v.to(torch.uint8) if v.dtype == torch.bool else v.to(dtype)
+    return f
+
+
+def bench_go1_tail(args, dev, rank):
+    """Go1-shape step tail (12 joints, 4 feet): rewards.total_reward (16 terms)
+    + build_locomotion_observation with Philox noise, fused (SURVEY §8a B1+B2).
+    One launch = K_TAIL steps x N worlds rows."""
+    import torch
+
+    from paper_2502_08844_b200 import locomotion as L
+
+    n, J, F, K = args.num_envs, 12, 4, 100
+    tdt = torch.float64 if args.dtype == "float64" else torch.float32
+    esz = 8 if tdt == torch.float64 else 4
+    ring = [synthetic_frames(K * n, J, F, dev, tdt, 10 + j) for j in range(3)]
+    noise = L.ObservationNoise(0.05, 0.1, 0.2, 0.01, 1.5)
+    cfg = L.RewardTermConfig()
+
+    def run(j):
+        return L.locomotion_tail(ring[j % len(ring)], cfg, noise=noise,
+                                 key=L.NoiseKey(0, rank * n, None, j * K), num_worlds=n,
+                                 check=False)
+
+    for j in range(3):
+        run(j)
+    torch.cuda.synchronize(dev)
+    launches = 12
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(launches)]
+    stream = torch.cuda.current_stream(dev)
+    for j in range(launches):
+        evs[j][0].record(stream)
+        run(j)
+        evs[j][1].record(stream)
+    torch.cuda.synchronize(dev)
+    ms = [a.elapsed_time(b) for a, b in evs]
+    avg_s = float(np.mean(ms)) / 1e3
+    S = 9 + 3 * J + 3 + 2 * F
+    P = S + F + J + 3
+    in_bytes = esz * (4 + 3 + 3 + 3 * J + 2 * F + 2 * F + F + F + 3 + 2 * J) + 2 * F + 1
+    out_bytes = esz * (2 + 16 + S + P)
+    rows = K * n
+    value = rows / avg_s
+    peak, src = hbm_peak()
+    achieved = rows * (in_bytes + out_bytes) / avg_s / 1e9
+    res = {"metric": "Go1-shape step-tail world-steps/s (16-term reward + noisy obs), "
+                     f"{n} worlds/GPU", "value": value, "unit": "world_steps/s",
+           "rows_per_launch": rows, "avg_launch_ms": avg_s * 1e3,
+           "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                        "frac": achieved / peak, "peak_source": src,
+                        "bytes_per_world_step": in_bytes + out_bytes,
+                        "traffic": ncu_traffic("go1_tail", args.dtype, n, K),
+                        "kernel": "loco_tail_kernel"}}
+    if rank == 0 and not args.no_cpu:
+        res["cpu_baseline"] = cpu_tail_rate(n, J, F, args.cpu_seconds / 2)
+    return res
+
+
+def cpu_tail_rate(n, J, F, seconds):
+    """The oracle's total_reward + build_locomotion_observation on all host
+    threads over random Go1-shape frames (a bounded sample)."""
+    from oracle import locomotion as olo
+    from oracle.oracle import max_threads
+
+    rng = np.random.default_rng(0)
+    q = rng.normal(size=(n, 4))
+    q /= np.linalg.norm(q, axis=1, keepdims=True)
+    fr = {"base_orientation": q, "base_lin_vel": rng.normal(size=(n, 3)),
+          "base_ang_vel": rng.normal(size=(n, 3)), "joint_pos": rng.normal(size=(n, J)),
+          "joint_vel": rng.normal(0, 2, (n, J)), "joint_torque": rng.normal(0, 5, (n, J)),
+          "foot_height": rng.uniform(0, .15, (n, F)), "foot_height_des": rng.uniform(0, .15, (n, F)),
+          "foot_vel_xy": rng.normal(0, .5, (n, F, 2)), "foot_contact": rng.uniform(size=(n, F)) < .5,
+          "airtime": rng.uniform(0, .8, (n, F)), "touchdown": rng.uniform(size=(n, F)) < .3,
+          "phase": rng.uniform(-np.pi, np.pi, (n, F)), "command": rng.normal(0, .5, (n, 3)),
+          "action": rng.uniform(-1, 1, (n, J)), "prev_action": rng.uniform(-1, 1, (n, J)),
+          "joint_nominal": rng.normal(0, .2, J), "joint_default": rng.normal(0, .2, J),
+          "done": rng.uniform(size=n) < .1}
+    noise = [0.05, 0.1, 0.2, 0.01, 1.5]
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        olo.total_reward(fr)
+        olo.loco_obs(fr, noise=noise, key=(0, 0, 0, reps))
+        reps += 1
+        dt = time.perf_counter() - t0
+        if dt > seconds and reps >= 2:
+            break
+    return {"value": reps * n / dt, "unit": "world_steps/s", "cores": max_threads(),
+            "kind": "port", "sample": f"{reps} x {n} Go1-shape frames in {dt:.1f}s; "
+                                      "oracle/locomotion.c (rewards.total_reward + "
+                                      "envkit.build_locomotion_observation restated)"}
 
 
 def measure_e2e(env, args, dev, dist, A, O, I, esz, world):

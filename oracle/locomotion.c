@@ -105,7 +105,8 @@ int orc_project_gravity(int64_t n, const double *q, double *out, uint8_t *ok) {
  * first frame with a non-unit quaternion, or -1. */
 int64_t orc_total_reward(int64_t n, int nj, int nf, const orc_reward_cfg *c,
                          const orc_frames *f, double *terms, double *unclipped, double *total) {
-    int64_t first_bad = -1;
+    int64_t first_bad = n;
+#pragma omp parallel for schedule(static) reduction(min : first_bad)
     for (int64_t i = 0; i < n; ++i) {
         const double *lin = f->base_lin_vel + 3 * i, *ang = f->base_ang_vel + 3 * i;
         const double *cmd = f->command + 3 * i;
@@ -155,7 +156,7 @@ int64_t orc_total_reward(int64_t n, int nj, int nf, const orc_reward_cfg *c,
         t[5] = s;
         double g[3];
         if (!project_gravity(f->base_orientation + 4 * i, g)) {
-            if (first_bad < 0) first_bad = i;
+            if (i < first_bad) first_bad = i;
             g[0] = g[1] = g[2] = NAN;
         }
         t[6] = g[0] * g[0] + g[1] * g[1];
@@ -191,7 +192,7 @@ int64_t orc_total_reward(int64_t n, int nj, int nf, const orc_reward_cfg *c,
         unclipped[i] = u;
         total[i] = 0.0 > u ? 0.0 : u;  /* max(unclipped, 0.0) */
     }
-    return first_bad;
+    return first_bad == n ? -1 : first_bad;
 }
 
 /* envkit.py:147-193.  state [N, 9 + 3*nj + 3 + 2*nf], priv [N, state + nf + nj + 3].
@@ -202,12 +203,13 @@ int64_t orc_loco_obs(int64_t n, int nj, int nf, const orc_frames *f, const doubl
                      int64_t episode, uint64_t step, const double *pert, double *state,
                      double *priv) {
     const int S = 9 + 3 * nj + 3 + 2 * nf, P = S + nf + nj + 3;
-    int64_t first_bad = -1;
+    int64_t first_bad = n;
+#pragma omp parallel for schedule(static) reduction(min : first_bad)
     for (int64_t i = 0; i < n; ++i) {
         double clean[512];
         int o = 0;
         if (!project_gravity(f->base_orientation + 4 * i, clean)) {
-            if (first_bad < 0) first_bad = i;
+            if (i < first_bad) first_bad = i;
             clean[0] = clean[1] = clean[2] = NAN;
         }
         o = 3;
@@ -241,7 +243,7 @@ int64_t orc_loco_obs(int64_t n, int nj, int nf, const orc_frames *f, const doubl
         for (int k = 0; k < nj; ++k) pr[o++] = f->joint_torque[nj * i + k];
         for (int k = 0; k < 3; ++k) pr[o++] = pert ? pert[3 * i + k] : 0.0;
     }
-    return first_bad;
+    return first_bad == n ? -1 : first_bad;
 }
 
 /* envkit.py:111-131.  params = (kp, kd, action_scale, torque_limit, range_lo, range_hi,

@@ -61,8 +61,9 @@ class _Cfg(ctypes.Structure):
 
 
 def build(force: bool = False) -> str:
+    srcs = [os.path.join(_HERE, f) for f in ("oracle.c", "locomotion.c", "Makefile")]
     if force or not os.path.exists(_LIB_PATH) or (
-        os.path.getmtime(_LIB_PATH) < os.path.getmtime(os.path.join(_HERE, "oracle.c"))
+        os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(f) for f in srcs)
     ):
         subprocess.run(["make", "-s", "-C", _HERE], check=True)
     return _LIB_PATH
