@@ -156,8 +156,9 @@ def ncu_traffic(task, dtype, num_envs, unroll):
 
 
 def cpu_rate(task, num_envs, seconds, nthreads=0, steps=None):
-    from oracle.oracle import ACTION_DIM, TASK_IDS, OracleBatchEnv, max_threads
+    from oracle.oracle import ACTION_DIM, TASK_IDS, OracleBatchEnv, max_threads, use_all_host_threads
 
+    use_all_host_threads()
     A = ACTION_DIM[TASK_IDS[task]]
     env = OracleBatchEnv(task, num_envs)
     env.reset(seed=0)
@@ -448,8 +449,9 @@ def cpu_tail_rate(n, J, F, seconds):
     """The oracle's total_reward + build_locomotion_observation on all host
     threads over random Go1-shape frames (a bounded sample)."""
     from oracle import locomotion as olo
-    from oracle.oracle import max_threads
+    from oracle.oracle import max_threads, use_all_host_threads
 
+    use_all_host_threads()
     rng = np.random.default_rng(0)
     q = rng.normal(size=(n, 4))
     q /= np.linalg.norm(q, axis=1, keepdims=True)
@@ -530,6 +532,10 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hooks for the multi-rank path on a 1-GPU box: every rank on GPU 0
+    # (the ranks' kernels never wait on each other) and a gloo process group
+    if os.environ.get("DK_BENCH_SAME_DEVICE") == "1":
+        local_rank = 0
     if args.impl == "reference":
         run_reference(args, rank)
         return
@@ -539,7 +545,11 @@ def main():
         import torch.distributed as tdist
 
         torch.cuda.set_device(local_rank)
-        tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("DK_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            tdist.init_process_group(backend)
         dist = tdist
     try:
         run_b200(args, rank, world, local_rank, dist)

@@ -256,3 +256,11 @@ class OracleBatchEnv:
 
 def max_threads() -> int:
     return int(lib().orc_max_threads())
+
+
+def use_all_host_threads() -> int:
+    """Let the oracle use every core this process may run on (torchrun sets
+    OMP_NUM_THREADS=1 for its workers)."""
+    n = len(os.sched_getaffinity(0))
+    lib().orc_set_threads(n)
+    return n
