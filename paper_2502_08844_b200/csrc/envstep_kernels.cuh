@@ -206,50 +206,52 @@ __device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
     } while (!done);
 }
 
-template <class Task, typename T>
+template <class Task, typename T, int TL>
 struct RolloutShape {
     static constexpr int A = Task::A, O = Task::O, I = Task::I;
     static constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));  // reals per world
+    static constexpr int WPC = 32 * TL;                                      // worlds per CTA
     static constexpr int G = WF * (int)sizeof(T) <= 24 ? 8 : 4;            // steps per group
     static constexpr int M = 4;                                              // consumer warps
     static constexpr int NG = M + 2;                                         // state ring (groups)
     static constexpr int NA = 4;                                             // action ring (groups)
+    static constexpr int NR = 8;                                             // raw action ring (groups)
     static constexpr int R = O > I ? O : I;
     // warp w runs on SM sub-partition w % 4: the light stager shares the
     // producer's (warp 0) scheduler, consumers are warps 1, 2, 3, 5, ...
     static constexpr int STAGER = 4;                                         // warp index
     static constexpr int THREADS = 32 * (M + 2);
     // shared memory carve-up
-    static constexpr int NR = 8;                                             // raw action ring (groups)
     static constexpr int NBAR = 2 * NG + 2 * NA;
     static constexpr size_t OFF_BAR = 0;  // full[NG] empty[NG] afull[NA] aempty[NA]
     static constexpr size_t OFF_RING = (8 * NBAR + 127) / 128 * 128;
-    static constexpr size_t RING_G = (size_t)G * WF * 32 * sizeof(T);       // bytes per group
+    static constexpr size_t RING_G = (size_t)G * WF * WPC * sizeof(T);      // bytes per group
     static constexpr size_t OFF_RPART = OFF_RING + NG * RING_G;
-    static constexpr size_t OFF_ACT = OFF_RPART + (size_t)NG * G * 32 * sizeof(T);
-    static constexpr size_t ACT_G = (size_t)G * A * 32 * sizeof(T);
-    static constexpr size_t OFF_RAW = (OFF_ACT + NA * ACT_G + 127) / 128 * 128;  // [NR][G][32][A]
+    static constexpr size_t OFF_ACT = OFF_RPART + (size_t)NG * G * WPC * sizeof(T);
+    static constexpr size_t ACT_G = (size_t)G * A * WPC * sizeof(T);
+    static constexpr size_t OFF_RAW = (OFF_ACT + NA * ACT_G + 127) / 128 * 128;  // [NR][G][WPC][A]
     static constexpr size_t OFF_TILE = OFF_RAW + NR * ACT_G;
     static constexpr size_t OFF_FLAGS = OFF_TILE + (size_t)M * 32 * R * sizeof(T);
-    static constexpr size_t OFF_GFLAG = OFF_FLAGS + (size_t)NG * G * 32;   // [NG] u8: fast group
+    static constexpr size_t OFF_GFLAG = OFF_FLAGS + (size_t)NG * G * WPC;  // [NG] u8: fast group
     static constexpr size_t OFF_CTRL = (OFF_GFLAG + NG + 15) / 16 * 16;
     static constexpr size_t SMEM = OFF_CTRL + 16;
 };
 
-template <class Task, typename T>
-__device__ __forceinline__ void world_to_slot(const typename Task::W &w, T *slot, int lane) {
-    constexpr int WF = RolloutShape<Task, T>::WF;
+// One world's registers <-> its column of a [field][worlds] ring slot.
+template <class Task, typename T, int STRIDE>
+__device__ __forceinline__ void world_to_slot(const typename Task::W &w, T *slot, int col) {
+    constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));
     const T *f = reinterpret_cast<const T *>(&w);
 #pragma unroll
-    for (int j = 0; j < WF; ++j) slot[j * 32 + lane] = f[j];
+    for (int j = 0; j < WF; ++j) slot[j * STRIDE + col] = f[j];
 }
 
-template <class Task, typename T>
-__device__ __forceinline__ void slot_to_world(typename Task::W &w, const T *slot, int lane) {
-    constexpr int WF = RolloutShape<Task, T>::WF;
+template <class Task, typename T, int STRIDE>
+__device__ __forceinline__ void slot_to_world(typename Task::W &w, const T *slot, int col) {
+    constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));
     T *f = reinterpret_cast<T *>(&w);
 #pragma unroll
-    for (int j = 0; j < WF; ++j) f[j] = slot[j * 32 + lane];
+    for (int j = 0; j < WF; ++j) f[j] = slot[j * STRIDE + col];
 }
 
 // Environment.reset (envkit.py:502-519) of one world inside a rollout: the
@@ -289,18 +291,22 @@ __device__ __forceinline__ void warp_store_rows_skip(T *__restrict__ out, int64_
     __syncwarp();
 }
 
-template <class Task, typename T, bool R1>
-__global__ void __launch_bounds__(RolloutShape<Task, T>::THREADS)
+// TL = 32-world tiles per CTA (the launcher uses TL = 1: interleaving two
+// worlds' chains in one producer lane, TL = 2 on 64-world CTAs, was measured
+// 1.7x slower per world at 8192 worlds -- the chains did not overlap and 20 of
+// 148 SMs sat idle -- profiles/r01_ncu_summary.md).
+template <class Task, typename T, bool R1, int TL>
+__global__ void __launch_bounds__(RolloutShape<Task, T, TL>::THREADS)
 rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T> p, Worlds<T> w,
                StepOut<T> out, unsigned long long *err) {
-    using S = RolloutShape<Task, T>;
+    using S = RolloutShape<Task, T, TL>;
     constexpr int A = Task::A, O = Task::O, I = Task::I, WF = S::WF, G = S::G, M = S::M;
-    constexpr int NG = S::NG, NA = S::NA;
+    constexpr int NG = S::NG, NA = S::NA, WPC = S::WPC;
     extern __shared__ __align__(16) unsigned char smem[];
-    T *ring = reinterpret_cast<T *>(smem + S::OFF_RING);    // [NG][G][WF][32]
-    T *rpart = reinterpret_cast<T *>(smem + S::OFF_RPART);  // [NG][G][32]
-    T *aring = reinterpret_cast<T *>(smem + S::OFF_ACT);    // [NA][G][A][32]
-    uint8_t *flags = smem + S::OFF_FLAGS;                   // [NG][G][32] bit0 trunc, bit1 reset
+    T *ring = reinterpret_cast<T *>(smem + S::OFF_RING);    // [NG][G][WF][WPC]
+    T *rpart = reinterpret_cast<T *>(smem + S::OFF_RPART);  // [NG][G][WPC]
+    T *aring = reinterpret_cast<T *>(smem + S::OFF_ACT);    // [NA][G][A][WPC]
+    uint8_t *flags = smem + S::OFF_FLAGS;                   // [NG][G][WPC] bit0 trunc, bit1 reset
     uint8_t *gflag = smem + S::OFF_GFLAG;                   // [NG] 1: no world truncated in the group
     int *ctrl = reinterpret_cast<int *>(smem + S::OFF_CTRL);
     const uint32_t bar = smem_u32(smem + S::OFF_BAR);
@@ -309,9 +315,7 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t n = sc.n;
-    const int64_t i = (int64_t)blockIdx.x * 32 + lane;
-    const int64_t row0 = (int64_t)blockIdx.x * 32;
-    const bool in_range = i < n;
+    const int64_t cta0 = (int64_t)blockIdx.x * WPC;  // first world of this CTA
     const int K32 = (int)K;  // host guarantees K < 2^31
     const int ngroups = (K32 + G - 1) / G;
 
@@ -323,7 +327,6 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         uint64_t *b = reinterpret_cast<uint64_t *>(smem + S::OFF_BAR);
 #pragma unroll
         for (int d = 0; d < 2 * NG + 2 * NA; ++d) mbar_init(&b[d], 32);
-
     }
     __syncthreads();
     const bool blocked = ctrl[0] != 0;
@@ -333,9 +336,9 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
     const int32_t *steps_src = src ? w.steps[1] : w.steps[0];
     const uint8_t *nr_src = src ? w.needs_reset[1] : w.needs_reset[0];
 
-    // step at which this world would need a reset (UsageError, envkit.py:527-528)
-    auto usage_step = [&](int32_t steps) -> int {
-        if (!in_range) return K32;
+    // step at which world i would need a reset (UsageError, envkit.py:527-528)
+    auto usage_step = [&](int64_t i, int32_t steps) -> int {
+        if (i >= n) return K32;
         if (nr_src[i]) return 0;
         if (!sc.autoreset && (int64_t)sc.episode_length - steps < K)
             return (int)((int64_t)sc.episode_length - steps);
@@ -353,43 +356,53 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         uint32_t *ep_dst = src ? w.episode[0] : w.episode[1];
         uint8_t *nr_dst = src ? w.needs_reset[0] : w.needs_reset[1];
 
-        typename Task::W wd;
-        int32_t steps = 0;
-        uint32_t episode = 0;
-        if (in_range) {
-            Task::load(wd, st_src, i, n);
-            steps = steps_src[i];
-            episode = ep_src[i];
-        } else {
-            Task::zero(wd);
+        typename Task::W wd[TL];
+        int32_t steps[TL];
+        uint32_t episode[TL];
+        bool live[TL], can_reset[TL];
+#pragma unroll
+        for (int t = 0; t < TL; ++t) {
+            const int64_t i = cta0 + t * 32 + lane;
+            live[t] = i < n;
+            steps[t] = 0;
+            episode[t] = 0;
+            if (live[t]) {
+                Task::load(wd[t], st_src, i, n);
+                steps[t] = steps_src[i];
+                episode[t] = ep_src[i];
+            } else {
+                Task::zero(wd[t]);
+            }
+            const int ku = usage_step(i, steps[t]);
+            if (ku < K32) record_error(err, ku, n, i, kErrUsage);
+            Task::refresh(wd[t]);
+            can_reset[t] = sc.autoreset && live[t];
         }
-        const int ku = usage_step(steps);
-        if (ku < K32) record_error(err, ku, n, i, kErrUsage);
-        Task::refresh(wd);
-        const uint64_t gidx = (uint64_t)(sc.env_offset + i);
 
-        const bool can_reset = sc.autoreset && in_range;
-        auto step_body = [&](int s, int k, T *ring_g, T *rp_g, uint8_t *fl_g, const T *u) {
+        auto step_body = [&](int t, int s, int k, T *ring_g, T *rp_g, uint8_t *fl_g, const T *u) {
+            const int col = t * 32 + lane;
             T rp = T(0);
-            Task::step_u(wd, u, p);
+            Task::step_u(wd[t], u, p);
             if (!R1) {
                 for (int rep = 1; rep < sc.action_repeat; ++rep) {
                     T inf[I];
-                    rp += Task::reward(wd, p, inf);
-                    Task::step_u(wd, u, p);
+                    rp += Task::reward(wd[t], p, inf);
+                    Task::step_u(wd[t], u, p);
                 }
             }
-            steps += 1;
-            const bool truncated = steps >= sc.episode_length;
-            const bool reset = truncated && can_reset;
-            world_to_slot<Task, T>(wd, ring_g + s * WF * 32, lane);
-            if (!R1) rp_g[s * 32 + lane] = rp;
-            fl_g[s * 32 + lane] = (uint8_t)((truncated ? 1 : 0) | (reset ? 2 : 0));
+            steps[t] += 1;
+            const bool truncated = steps[t] >= sc.episode_length;
+            const bool reset = truncated && can_reset[t];
+            world_to_slot<Task, T, WPC>(wd[t], ring_g + s * WF * WPC, col);
+            if (!R1) rp_g[s * WPC + col] = rp;
+            fl_g[s * WPC + col] = (uint8_t)((truncated ? 1 : 0) | (reset ? 2 : 0));
             if (__builtin_expect(reset, 0)) {
-                episode += 1;
-                steps = 0;
-                wd = autoreset_world<Task, T>(sc.seed, gidx, episode, p, sc.wide_init,
-                                              out.obs + ((int64_t)k * n + i) * O);
+                episode[t] += 1;
+                steps[t] = 0;
+                const int64_t i = cta0 + col;
+                wd[t] = autoreset_world<Task, T>(sc.seed, (uint64_t)(sc.env_offset + i),
+                                                 episode[t], p, sc.wide_init,
+                                                 out.obs + ((int64_t)k * n + i) * O);
             }
         };
 
@@ -398,82 +411,111 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             const int sb = g % NG, ab = g % NA;
             mbar_wait_u32(afull_b + 8 * ab, (uint32_t)(g / NA) & 1u);
             mbar_wait_u32(empty_b + 8 * sb, (uint32_t)(g / NG) & 1u);  // phase 0 pre-armed
-            T *ring_g = ring + (size_t)sb * G * WF * 32;
-            T *rp_g = rpart + (size_t)sb * G * 32;
-            uint8_t *fl_g = flags + sb * G * 32;
-            const T *act_g = aring + (size_t)ab * G * A * 32;
+            T *ring_g = ring + (size_t)sb * G * WF * WPC;
+            T *rp_g = rpart + (size_t)sb * G * WPC;
+            uint8_t *fl_g = flags + sb * G * WPC;
+            const T *act_g = aring + (size_t)ab * G * A * WPC;
             const int k0 = g * G;
             // fast group: no world of this warp reaches episode_length inside
             // it (124 of 125 groups at episode_length 1000), so the chain
             // carries no step counting, flags or reset branch
-            const bool fast = (k0 + G <= K32) &&
-                              !__any_sync(0xffffffffu, in_range && steps + G >= sc.episode_length);
+            bool near_end = false;
+#pragma unroll
+            for (int t = 0; t < TL; ++t) near_end |= live[t] && steps[t] + G >= sc.episode_length;
+            const bool fast = (k0 + G <= K32) && !__any_sync(0xffffffffu, near_end);
             if (fast) {
-                T u[G][A];  // the whole group's controls, loaded ahead of the chain
+                T u[G][TL][A];  // the whole group's controls, loaded ahead of the chains
 #pragma unroll
                 for (int s = 0; s < G; ++s)
 #pragma unroll
-                    for (int j = 0; j < A; ++j) u[s][j] = act_g[(s * A + j) * 32 + lane];
+                    for (int t = 0; t < TL; ++t)
+#pragma unroll
+                        for (int j = 0; j < A; ++j)
+                            u[s][t][j] = act_g[(s * A + j) * WPC + t * 32 + lane];
 #pragma unroll
                 for (int s = 0; s < G; ++s) {
-                    T rp = T(0);
-                    Task::step_u(wd, u[s], p);
-                    if (!R1) {
-                        for (int rep = 1; rep < sc.action_repeat; ++rep) {
-                            T inf[I];
-                            rp += Task::reward(wd, p, inf);
-                            Task::step_u(wd, u[s], p);
+#pragma unroll
+                    for (int t = 0; t < TL; ++t) {  // independent chains interleave here
+                        T rp = T(0);
+                        Task::step_u(wd[t], u[s][t], p);
+                        if (!R1) {
+                            for (int rep = 1; rep < sc.action_repeat; ++rep) {
+                                T inf[I];
+                                rp += Task::reward(wd[t], p, inf);
+                                Task::step_u(wd[t], u[s][t], p);
+                            }
+                            rp_g[s * WPC + t * 32 + lane] = rp;
                         }
-                        rp_g[s * 32 + lane] = rp;
+                        world_to_slot<Task, T, WPC>(wd[t], ring_g + s * WF * WPC, t * 32 + lane);
                     }
-                    world_to_slot<Task, T>(wd, ring_g + s * WF * 32, lane);
                 }
-                steps += G;
+#pragma unroll
+                for (int t = 0; t < TL; ++t) steps[t] += G;
             } else {
 #pragma unroll 1
                 for (int s = 0; s < min(G, K32 - k0); ++s) {
-                    T u[A];
 #pragma unroll
-                    for (int j = 0; j < A; ++j) u[j] = act_g[(s * A + j) * 32 + lane];
-                    step_body(s, k0 + s, ring_g, rp_g, fl_g, u);
+                    for (int t = 0; t < TL; ++t) {
+                        T u[A];
+#pragma unroll
+                        for (int j = 0; j < A; ++j) u[j] = act_g[(s * A + j) * WPC + t * 32 + lane];
+                        step_body(t, s, k0 + s, ring_g, rp_g, fl_g, u);
+                    }
                 }
             }
             if (lane == 0) gflag[sb] = fast ? 1 : 0;
             mbar_arrive_u32(aempty_b + 8 * ab);
             mbar_arrive_u32(full_b + 8 * sb);
         }
-        if (in_range) {
-            Task::store(wd, st_dst, i, n);
-            steps_dst[i] = steps;
-            ep_dst[i] = episode;
-            // without autoreset a world that truncated in this window needs a reset
-            nr_dst[i] = (!sc.autoreset && steps >= sc.episode_length) ? 1 : 0;
+#pragma unroll
+        for (int t = 0; t < TL; ++t) {
+            const int64_t i = cta0 + t * 32 + lane;
+            if (live[t]) {
+                Task::store(wd[t], st_dst, i, n);
+                steps_dst[i] = steps[t];
+                ep_dst[i] = episode[t];
+                // without autoreset a world that truncated in this window needs a reset
+                nr_dst[i] = (!sc.autoreset && steps[t] >= sc.episode_length) ? 1 : 0;
+            }
         }
     } else if (warp == S::STAGER) {
         // ------------------------------------------------------------ stager
-        const int ku = usage_step(in_range ? steps_src[i] : 0);
-        bool ok = true;
         // raw actions stream into an NR-group shared-memory ring through
-        // cp.async (each lane copies its own world's values), NR-1 groups ahead
+        // cp.async (each lane copies its own worlds' values), NR-1 groups ahead
         // of the group being validated.  (1-D TMA bulk copies of the 128 B
         // rows were measured 24% slower end to end: eight tiny bulk ops per
         // group serialise in the copy engine and the producer starved.)
         constexpr int NR = S::NR;
-        constexpr int ROWV = 32 * A;  // values per row slot
-        T *raw = reinterpret_cast<T *>(smem + S::OFF_RAW);  // [NR][G][32][A]
-        const T *arow = actions + (in_range ? i * A : 0);
-        const int64_t astep = in_range ? n * A : 0;
+        constexpr int ROWV = WPC * A;  // values per row slot
+        T *raw = reinterpret_cast<T *>(smem + S::OFF_RAW);  // [NR][G][WPC][A]
+        int ku[TL];
+        bool ok[TL], live[TL];
+        const T *arow[TL];
+        int64_t astep[TL];
+#pragma unroll
+        for (int t = 0; t < TL; ++t) {
+            const int64_t i = cta0 + t * 32 + lane;
+            live[t] = i < n;
+            ku[t] = usage_step(i, live[t] ? steps_src[i] : 0);
+            ok[t] = true;
+            arow[t] = actions + (live[t] ? i * A : 0);
+            astep[t] = live[t] ? n * A : 0;
+        }
         auto issue = [&](int g) {
             T *dst = raw + (size_t)(g % NR) * G * ROWV;
             const int k0 = g * G;
 #pragma unroll
-            for (int s = 0; s < G; ++s) {
-                const bool v = in_range && k0 + s < K32;
+            for (int s = 0; s < G; ++s)
 #pragma unroll
-                for (int j = 0; j < A; ++j)
-                    cp_async_ca<sizeof(T)>(dst + s * ROWV + lane * A + j,
-                                           v ? arow + (int64_t)(k0 + s) * astep + j : actions, v);
-            }
+                for (int t = 0; t < TL; ++t) {
+                    const bool v = live[t] && k0 + s < K32;
+#pragma unroll
+                    for (int j = 0; j < A; ++j)
+                        cp_async_ca<sizeof(T)>(dst + s * ROWV + (t * 32 + lane) * A + j,
+                                               v ? arow[t] + (int64_t)(k0 + s) * astep[t] + j
+                                                 : actions,
+                                               v);
+                }
             cp_async_commit();  // one group per call (empty groups past K keep the count)
         };
 #pragma unroll 1
@@ -485,31 +527,37 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             const int ab = g % NA;
             const int k0 = g * G;
             const T *src_g = raw + (size_t)(g % NR) * G * ROWV;
-            T v[G][A];
+            T v[G][TL][A];
 #pragma unroll
             for (int s = 0; s < G; ++s)
 #pragma unroll
-                for (int j = 0; j < A; ++j) v[s][j] = src_g[s * ROWV + lane * A + j];
+                for (int t = 0; t < TL; ++t)
+#pragma unroll
+                    for (int j = 0; j < A; ++j)
+                        v[s][t][j] = src_g[s * ROWV + (t * 32 + lane) * A + j];
             if (g >= NA) mbar_wait_u32(aempty_b + 8 * ab, (uint32_t)(g / NA - 1) & 1u);
-            T *act_g = aring + (size_t)ab * G * A * 32;
+            T *act_g = aring + (size_t)ab * G * A * WPC;
 #pragma unroll
-            for (int s = 0; s < G; ++s) {
-                bool fin = true;
-                T a[A], u[A];
+            for (int s = 0; s < G; ++s)
 #pragma unroll
-                for (int j = 0; j < A; ++j) {
-                    fin &= RealOps<T>::finite_(v[s][j]);
-                    a[j] = fmin(fmax(v[s][j], T(-1)), T(1));  // envkit.py:532
+                for (int t = 0; t < TL; ++t) {
+                    bool fin = true;
+                    T a[A], u[A];
+#pragma unroll
+                    for (int j = 0; j < A; ++j) {
+                        fin &= RealOps<T>::finite_(v[s][t][j]);
+                        a[j] = fmin(fmax(v[s][t][j], T(-1)), T(1));  // envkit.py:532
+                    }
+                    // the force / torque clip of step_dynamics, off the producer's chain
+                    Task::control(a, p, u);
+#pragma unroll
+                    for (int j = 0; j < A; ++j) act_g[(s * A + j) * WPC + t * 32 + lane] = u[j];
+                    if (__builtin_expect(
+                            !fin && ok[t] && live[t] && k0 + s < ku[t] && k0 + s < K32, 0)) {
+                        ok[t] = false;  // envkit.py:529-531
+                        record_error(err, k0 + s, n, cta0 + t * 32 + lane, kErrInvalid);
+                    }
                 }
-                // the force / torque clip of step_dynamics, off the producer's chain
-                Task::control(a, p, u);
-#pragma unroll
-                for (int j = 0; j < A; ++j) act_g[(s * A + j) * 32 + lane] = u[j];
-                if (__builtin_expect(!fin && ok && in_range && k0 + s < ku && k0 + s < K32, 0)) {
-                    ok = false;  // envkit.py:529-531
-                    record_error(err, k0 + s, n, i, kErrInvalid);
-                }
-            }
             mbar_arrive_u32(afull_b + 8 * ab);
         }
         cp_async_wait<0>();
@@ -524,75 +572,83 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             for (int d = 0; d < NG; ++d) mbar_arrive_u32(empty_b + 8 * d);  // slots start free
         }
         // FULL: all 32 rows of the tile exist -> no per-element bounds checks
-        auto run = [&](auto full_c) {
+        auto run_tile = [&](auto full_c, int t, int g, const T *ring_g, const T *rp_g,
+                            const uint8_t *fl_g, bool fast) {
             constexpr bool FULL = decltype(full_c)::value;
+            const int col = t * 32 + lane;
+            const int64_t row0 = cta0 + t * 32;
+            const int64_t i = row0 + lane;
+            const bool in_range = i < n;
+            const int kend = min(G, K32 - g * G);
+            const int64_t kb = (int64_t)g * G * n;  // element row of step g*G
+            T *obs_p = out.obs + (kb + row0) * O;
+            T *info_p = has_info ? out.info + (kb + row0) * I : nullptr;
+            T *rew_p = out.reward + kb + i;
+            uint8_t *done_p = out.done + kb + i, *trunc_p = out.trunc + kb + i;
+            uint8_t *mask_p = has_mask ? out.term_mask + kb + i : nullptr;
 #pragma unroll 1
-            for (int g = c; g < ngroups; g += M) {
-                const int sb = g % NG;
-                mbar_wait_u32(full_b + 8 * sb, (uint32_t)(g / NG) & 1u);
-                const T *ring_g = ring + (size_t)sb * G * WF * 32;
-                const T *rp_g = rpart + (size_t)sb * G * 32;
-                const uint8_t *fl_g = flags + sb * G * 32;
-                const bool fast = gflag[sb] != 0;
-                const int kend = min(G, K32 - g * G);
-                const int64_t kb = (int64_t)g * G * n;  // element row of step g*G
-                T *obs_p = out.obs + (kb + row0) * O;
-                T *info_p = has_info ? out.info + (kb + row0) * I : nullptr;
-                T *rew_p = out.reward + kb + i;
-                uint8_t *done_p = out.done + kb + i, *trunc_p = out.trunc + kb + i;
-                uint8_t *mask_p = has_mask ? out.term_mask + kb + i : nullptr;
-#pragma unroll 1
-                for (int s = 0; s < kend; ++s) {
-                    typename Task::W wd;
-                    slot_to_world<Task, T>(wd, ring_g + s * WF * 32, lane);
-                    const uint8_t fl = fast ? 0 : fl_g[s * 32 + lane];
-                    const bool reset = (fl & 2) != 0;
-                    T info[I];
-                    const T r = R1 ? (T(0) + Task::reward(wd, p, info))
-                                   : (rp_g[s * 32 + lane] + Task::reward(wd, p, info)) / inv_rep;
-                    T o[O];
-                    Task::obs(wd, p, o);
-                    if (__builtin_expect(reset, 0) && out.term_obs) {
-                        T *t = out.term_obs + (kb + (int64_t)s * n + i) * O;
+            for (int s = 0; s < kend; ++s) {
+                typename Task::W wd;
+                slot_to_world<Task, T, WPC>(wd, ring_g + s * WF * WPC, col);
+                const uint8_t fl = fast ? 0 : fl_g[s * WPC + col];
+                const bool reset = (fl & 2) != 0;
+                T info[I];
+                const T r = R1 ? (T(0) + Task::reward(wd, p, info))
+                               : (rp_g[s * WPC + col] + Task::reward(wd, p, info)) / inv_rep;
+                T o[O];
+                Task::obs(wd, p, o);
+                if (__builtin_expect(reset, 0) && out.term_obs) {
+                    T *tt = out.term_obs + (kb + (int64_t)s * n + i) * O;
 #pragma unroll
-                        for (int j = 0; j < O; ++j) t[j] = o[j];
-                    }
-                    // the producer wrote the post-reset observation of reset worlds
-                    const uint32_t skip = __ballot_sync(0xffffffffu, reset);
-                    if (__builtin_expect(skip == 0u, 1)) {
-                        if (FULL)
-                            warp_store_tile<T, O>(obs_p, o, tile, lane);
-                        else
-                            warp_store_rows<T, O>(obs_p - row0 * O, row0, n, o, tile, lane);
-                    } else {
-                        warp_store_rows_skip<T, O>(obs_p - row0 * O, row0, n, o, tile, lane, skip);
-                    }
-                    if (has_info) {
-                        if (FULL)
-                            warp_store_tile<T, I>(info_p, info, tile, lane);
-                        else
-                            warp_store_rows<T, I>(info_p - row0 * I, row0, n, info, tile, lane);
-                    }
-                    if (FULL || in_range) {
-                        *rew_p = r;
-                        *done_p = 0;
-                        *trunc_p = fl & 1;
-                        if (has_mask) *mask_p = reset ? 1 : 0;
-                    }
-                    obs_p += n * O;
-                    info_p += n * I;
-                    rew_p += n;
-                    done_p += n;
-                    trunc_p += n;
-                    mask_p += n;
+                    for (int j = 0; j < O; ++j) tt[j] = o[j];
                 }
-                mbar_arrive_u32(empty_b + 8 * sb);
+                // the producer wrote the post-reset observation of reset worlds
+                const uint32_t skip = __ballot_sync(0xffffffffu, reset);
+                if (__builtin_expect(skip == 0u, 1)) {
+                    if (FULL)
+                        warp_store_tile<T, O>(obs_p, o, tile, lane);
+                    else
+                        warp_store_rows<T, O>(obs_p - row0 * O, row0, n, o, tile, lane);
+                } else {
+                    warp_store_rows_skip<T, O>(obs_p - row0 * O, row0, n, o, tile, lane, skip);
+                }
+                if (has_info) {
+                    if (FULL)
+                        warp_store_tile<T, I>(info_p, info, tile, lane);
+                    else
+                        warp_store_rows<T, I>(info_p - row0 * I, row0, n, info, tile, lane);
+                }
+                if (FULL || in_range) {
+                    *rew_p = r;
+                    *done_p = 0;
+                    *trunc_p = fl & 1;
+                    if (has_mask) *mask_p = reset ? 1 : 0;
+                }
+                obs_p += n * O;
+                info_p += n * I;
+                rew_p += n;
+                done_p += n;
+                trunc_p += n;
+                mask_p += n;
             }
         };
-        if (row0 + 32 <= n)
-            run(std::true_type{});
-        else
-            run(std::false_type{});
+#pragma unroll 1
+        for (int g = c; g < ngroups; g += M) {
+            const int sb = g % NG;
+            mbar_wait_u32(full_b + 8 * sb, (uint32_t)(g / NG) & 1u);
+            const T *ring_g = ring + (size_t)sb * G * WF * WPC;
+            const T *rp_g = rpart + (size_t)sb * G * WPC;
+            const uint8_t *fl_g = flags + sb * G * WPC;
+            const bool fast = gflag[sb] != 0;
+#pragma unroll
+            for (int t = 0; t < TL; ++t) {
+                if (cta0 + t * 32 + 32 <= n)
+                    run_tile(std::true_type{}, t, g, ring_g, rp_g, fl_g, fast);
+                else if (cta0 + t * 32 < n)
+                    run_tile(std::false_type{}, t, g, ring_g, rp_g, fl_g, fast);
+            }
+            mbar_arrive_u32(empty_b + 8 * sb);
+        }
     }
     finish_launch(w.cur, w.blocks_done, err, !blocked);
 }

@@ -16,26 +16,35 @@ inline int pick_block(int64_t n) {
     return bs;
 }
 
-template <class Task, typename T>
-inline cudaError_t launch_task_rollout(const T *actions, int64_t K, const EnvScalars &sc,
-                                       const Params<T> &p, const Worlds<T> &w,
-                                       const StepOut<T> &out, unsigned long long *err,
-                                       cudaStream_t st, int64_t *launches) {
-    using S = RolloutShape<Task, T>;
-    auto kern = sc.action_repeat == 1 ? rollout_kernel<Task, T, true> : rollout_kernel<Task, T, false>;
+template <class Task, typename T, int TL>
+inline cudaError_t launch_task_rollout_tl(const T *actions, int64_t K, const EnvScalars &sc,
+                                          const Params<T> &p, const Worlds<T> &w,
+                                          const StepOut<T> &out, unsigned long long *err,
+                                          cudaStream_t st) {
+    using S = RolloutShape<Task, T, TL>;
     static bool attr_set = false;  // per instantiation; opt in above 48 KB once
     if (!attr_set) {
-        for (auto kk : {rollout_kernel<Task, T, true>, rollout_kernel<Task, T, false>}) {
+        for (auto kk : {rollout_kernel<Task, T, true, TL>, rollout_kernel<Task, T, false, TL>}) {
             cudaError_t e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)S::SMEM);
             if (e != cudaSuccess) return e;
         }
         attr_set = true;
     }
-    const int64_t grid = (sc.n + 31) / 32;  // one block per tile of 32 worlds
+    auto kern = sc.action_repeat == 1 ? rollout_kernel<Task, T, true, TL>
+                                      : rollout_kernel<Task, T, false, TL>;
+    const int64_t grid = (sc.n + S::WPC - 1) / S::WPC;  // one block per CTA tile
     kern<<<(unsigned)grid, S::THREADS, S::SMEM, st>>>(actions, K, sc, p, w, out, err);
-    *launches += 1;
     return cudaGetLastError();
+}
+
+template <class Task, typename T>
+inline cudaError_t launch_task_rollout(const T *actions, int64_t K, const EnvScalars &sc,
+                                       const Params<T> &p, const Worlds<T> &w,
+                                       const StepOut<T> &out, unsigned long long *err,
+                                       cudaStream_t st, int64_t *launches) {
+    *launches += 1;
+    return launch_task_rollout_tl<Task, T, 1>(actions, K, sc, p, w, out, err, st);
 }
 
 template <typename T>
