@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tail", action="store_true", help="skip the Go1-shape step-tail line")
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the drop-in BatchEnv.step and world-count sweep lines")
     return ap.parse_args()
 
 
@@ -316,6 +318,10 @@ def run_b200(args, rank, world, local_rank, dist):
     tail = None
     if not args.no_tail:
         tail = bench_go1_tail(args, dev, rank)
+    dropin = sweep = None
+    if rank == 0 and not args.no_extra:
+        dropin = bench_dropin_step(args, dev)
+        sweep = bench_sweep(args, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -353,11 +359,70 @@ def run_b200(args, rank, world, local_rank, dist):
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "go1_tail": tail,
+            "e2e_dropin_step": dropin,
+            "sweep": sweep,
             "clocks": clocks.summary(),
             "library": _native.LIB_PATH,
         }
         print(json.dumps(line), flush=True)
     env.close()
+
+
+def bench_dropin_step(args, dev, steps=300):
+    """The reference-facing call itself: BatchEnv.step(numpy actions) ->
+    numpy obs/rewards/dones/truncs/infos (float64, like the reference)."""
+    import paper_2502_08844_b200 as dk
+
+    env = dk.BatchEnv(dk.EnvConfig(task=args.task), args.num_envs, dtype="float64",
+                      device=dev.index)
+    env.reset(seed=0)
+    acts = np.random.default_rng(0).uniform(-1, 1, (steps + 10, args.num_envs, env.action_dim))
+    for k in range(10):
+        env.step(acts[k])
+    t0 = time.perf_counter()
+    for k in range(steps):
+        env.step(acts[10 + k])
+    dt = time.perf_counter() - t0
+    env.close()
+    return {"value": steps * args.num_envs / dt, "unit": UNIT, "steps": steps,
+            "us_per_call": dt / steps * 1e6,
+            "api": "paper_2502_08844_b200.BatchEnv.step (numpy in/out, f64, infos list)"}
+
+
+def bench_sweep(args, dev, sizes=(1024, 8192, 65536), K=1000, launches=5):
+    """Worlds-per-GPU sweep (BASELINE config 5 style): device-resident rollout
+    throughput and roofline fraction at each size."""
+    import torch
+
+    import paper_2502_08844_b200 as dk
+
+    out = []
+    peak, _ = hbm_peak()
+    for n in sizes:
+        env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.task), n, dtype=args.dtype,
+                                device=dev.index)
+        env.reset(seed=0)
+        tdt = env.dtype
+        esz = 8 if tdt == torch.float64 else 4
+        acts = torch.rand((K, n, env.action_dim), device=dev, dtype=tdt) * 2 - 1
+        o = env._outputs((K,), True)
+        env.rollout(acts, with_info=True, out=o)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(launches):
+            env.rollout(acts, with_info=True, out=o)
+        b.record()
+        torch.cuda.synchronize(dev)
+        env.check()
+        s_per = a.elapsed_time(b) / 1e3 / launches
+        bpw = bytes_per_world_step(env.action_dim, env.obs_dim, len(env.info_keys), esz)
+        rate = n * K / s_per
+        out.append({"worlds": n, "value": rate, "unit": UNIT,
+                    "frac": rate * bpw / 1e9 / peak})
+        env.close()
+        del acts, o
+    return out
 
 
 def synthetic_frames(R, J, F, dev, dtype, seed):

@@ -1,0 +1,3 @@
+cd $GRAFT_REPO_ROOT
+python bench.py > gpurun_out/bench_default.json 2> gpurun_out/bench_default.err
+echo "rc=$?" >> gpurun_out/bench_default.err
