@@ -586,7 +586,7 @@ def measure_e2e(env, args, dev, dist, A, O, I, esz, world):
         dt = float(t.item())
     nterm = int(mask.sum())
     h2d = n * A * esz
-    d2h = n * (O * esz + esz + 3 + I * esz) + nterm * O * esz / K
+    d2h = n * (O * esz + esz + 1 + I * esz) + nterm * O * esz / K  # done/mask derived on host
     return {"value": K * n * world / dt, "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": d2h, "api": "dk_env_rollout_host (C ABI, pinned host buffers)",
             "steps": K, "chunk_steps": chunk}

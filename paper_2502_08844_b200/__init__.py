@@ -15,10 +15,13 @@ from .envkit import (  # noqa: E402,F401
     DeviceBatchEnv,
     DynamicsParams,
     EnvConfig,
+    Environment,
     InvalidInputError,
+    StepResult,
     TaskSpec,
     UsageError,
     make_batch_env,
+    make_env,
     registered_tasks,
     resolve_task,
 )

@@ -463,23 +463,29 @@ int dk_env_rollout_host(dk_env *e, int64_t K, int64_t chunk, const void *actions
     auto steps_in = [&](int64_t j) { return (size_t)std::min<int64_t>(chunk, K - j * chunk); };
 
     // Chunk j's term obs rows are fetched after the host has seen its mask.
+    // done and terminal_mask never cross PCIe: done is identically 0 for these
+    // tasks (envkit.py:543) and, with autoreset, terminal_mask == trunc.
     auto finish_chunk = [&](int64_t j) -> int {
         const int b = (int)(j & 1);
         DK_CUDA(cudaEventSynchronize(e->ev_d2h[b]));
+        const size_t rows = steps_in(j) * n;
+        std::memset(done + off(j), 0, rows);
+        if (mask_host) std::memcpy(mask_host + off(j), trunc + off(j), rows);
         if (*e->err_host != dk::kNoError) return DK_OK;  // reported below
         if (term_obs) {
-            const size_t rows = steps_in(j) * n;
             const uint8_t *m = mask_host + off(j);
+            bool queued = false;
             for (size_t k = 0; k < steps_in(j); ++k) {
                 bool any = false;
                 for (size_t i = 0; i < n && !any; ++i) any = m[k * n + i] != 0;
-                if (any)
+                if (any) {
                     DK_CUDA(cudaMemcpyAsync((char *)term_obs + (off(j) + k * n) * e->O * es,
                                             (char *)e->hs.term[b] + k * n * e->O * es,
                                             n * e->O * es, cudaMemcpyDeviceToHost, e->s_d2h));
+                    queued = true;
+                }
             }
-            (void)rows;
-            DK_CUDA(cudaEventRecord(e->ev_d2h[b], e->s_d2h));
+            if (queued) DK_CUDA(cudaEventRecord(e->ev_d2h[b], e->s_d2h));
         }
         return DK_OK;
     };
@@ -510,13 +516,8 @@ int dk_env_rollout_host(dk_env *e, int64_t K, int64_t chunk, const void *actions
                                 cudaMemcpyDeviceToHost, e->s_d2h));
         DK_CUDA(cudaMemcpyAsync((char *)reward + off(j) * es, e->hs.reward[b], rows * es,
                                 cudaMemcpyDeviceToHost, e->s_d2h));
-        DK_CUDA(cudaMemcpyAsync(done + off(j), e->hs.done[b], rows, cudaMemcpyDeviceToHost,
-                                e->s_d2h));
         DK_CUDA(cudaMemcpyAsync(trunc + off(j), e->hs.trunc[b], rows, cudaMemcpyDeviceToHost,
                                 e->s_d2h));
-        if (mask_host)
-            DK_CUDA(cudaMemcpyAsync(mask_host + off(j), e->hs.mask[b], rows,
-                                    cudaMemcpyDeviceToHost, e->s_d2h));
         if (info)
             DK_CUDA(cudaMemcpyAsync((char *)info + off(j) * e->I * es, e->hs.info[b],
                                     rows * e->I * es, cudaMemcpyDeviceToHost, e->s_d2h));

@@ -586,6 +586,68 @@ def _replace_seed(config, seed):
         return config
 
 
+@dataclass
+class StepResult:
+    """Result of Environment.step (reference: envkit.py:78-84)."""
+
+    observation: dict
+    reward: float
+    done: bool
+    truncated: bool
+    info: dict = field(default_factory=dict)
+
+
+class Environment:
+    """A single world (reference: envkit.py:469-584) on the B200 backend.
+
+    Same lifecycle as the reference: ``reset(seed=None) -> obs``,
+    ``step(action) -> StepResult`` (no autoreset: stepping past truncation
+    raises ``UsageError``), ``observation_shapes()``, ``state``, ``steps``.
+    ``env_index`` keys the world's Philox stream like the reference's."""
+
+    def __init__(self, config, env_index: int = 0, params=None, *, dtype="float64",
+                 device: int | None = None):
+        self.config = config
+        self.env_index = int(env_index)
+        self._b = BatchEnv(config, 1, params=params, dtype=dtype, device=device,
+                           env_index_offset=env_index)
+        self.task = self._b._h.spec
+        self.action_dim = self.task.action_dim
+
+    def reset(self, seed: int | None = None) -> dict:
+        o = self._b.reset(seed)
+        self.config = self._b.config
+        return {k: v[0] for k, v in o.items()}
+
+    def step(self, action) -> StepResult:
+        a = np.asarray(action, dtype=float).reshape(1, self.action_dim)
+        obs, r, d, t, infos = self._b.step(a, autoreset=False)
+        info = dict(infos[0])
+        return StepResult({k: v[0] for k, v in obs.items()}, float(r[0]), bool(d[0]),
+                          bool(t[0]), info)
+
+    @property
+    def state(self):
+        return self._b.envs[0].state
+
+    @property
+    def steps(self):
+        return self._b.envs[0].steps
+
+    def observation_shapes(self) -> dict:
+        o = self.task.obs_dim
+        return {"state": (o,), "privileged_state": (o,)}
+
+    def close(self):
+        self._b.close()
+
+
+def make_env(task: str, **kwargs) -> Environment:
+    """Single-world env (reference: envkit.py:587-588)."""
+    dtype = kwargs.pop("dtype", "float64")
+    return Environment(EnvConfig(task=task, **kwargs), dtype=dtype)
+
+
 def make_batch_env(task: str, num_envs: int, **kwargs) -> BatchEnv:
     """BatchEnv of ``num_envs`` worlds of ``task`` (cf. make_env, envkit.py:587-588)."""
     dtype = kwargs.pop("dtype", "float64")
@@ -594,6 +656,7 @@ def make_batch_env(task: str, num_envs: int, **kwargs) -> BatchEnv:
 
 __all__ = [
     "BackendError", "BatchEnv", "ConfigError", "DeviceBatchEnv", "DynamicsParams", "EnvConfig",
+    "Environment", "StepResult", "make_env",
     "InvalidInputError", "TaskSpec", "UsageError", "make_batch_env", "registered_tasks",
     "resolve_task",
 ]

@@ -292,3 +292,62 @@ def test_ragged_world_counts(pkg, oracle, n, task):
         out2 = env.rollout(view, with_info=True)
         env.check()
         assert torch.equal(out2["obs"], out["obs"]) and torch.equal(out2["reward"], out["reward"])
+
+
+def test_single_environment_matches_batch_world(pkg, golden):
+    """make_env / Environment (envkit.py:469-588) == world i of a BatchEnv."""
+    cfg = pkg.EnvConfig(task="acrobot-swingup", episode_length=5)
+    batch = pkg.BatchEnv(cfg, 8)
+    batch.reset(seed=3)
+    env = pkg.Environment(cfg, env_index=6)
+    o = env.reset(seed=3)
+    assert o["state"].shape == (6,)
+    acts = np.random.default_rng(1).uniform(-1, 1, (5, 8, 1))
+    for k in range(5):
+        bo, br, bd, bt, binfo = batch.step(acts[k], autoreset=False)
+        res = env.step(acts[k, 6])
+        np.testing.assert_array_equal(res.observation["state"], bo["state"][6])
+        assert res.reward == br[6] and res.truncated == bt[6] and not res.done
+        assert res.info == binfo[6]
+    with pytest.raises(pkg.UsageError):
+        env.step([0.0])
+    e2 = pkg.make_env("pendulum-swingup")
+    e2.reset()
+    assert e2.step([0.1]).observation["state"].shape == (3,)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "float64"])
+def test_rollout_host_matches_device_rollout(pkg, dtype):
+    """dk_env_rollout_host (pinned/pageable host buffers, chunked + pipelined,
+    done / terminal_mask derived on the host) == the device rollout."""
+    n, K, chunk = 1000, 2500, 700
+    cfg = pkg.EnvConfig(task="reacher-easy", episode_length=300)
+    a = pkg.DeviceBatchEnv(cfg, n, dtype=dtype)
+    b = pkg.DeviceBatchEnv(cfg, n, dtype=dtype)
+    a.reset(seed=1)
+    b.reset(seed=1)
+    npdt = np.float64 if dtype == "float64" else np.float32
+    acts = np.random.default_rng(2).uniform(-1, 1, (K, n, 2)).astype(npdt)
+    ref = a.rollout(torch.as_tensor(acts, device="cuda"), with_info=True)
+    a.check()
+    O, I = 10, 1
+    obs = np.zeros((K, n, O), npdt)
+    rew = np.zeros((K, n), npdt)
+    done = np.ones((K, n), np.uint8)
+    trunc = np.zeros((K, n), np.uint8)
+    term = np.zeros((K, n, O), npdt)
+    mask = np.zeros((K, n), np.uint8)
+    info = np.zeros((K, n, I), npdt)
+    rc = b._h._lib.dk_env_rollout_host(b._h.h, K, chunk, acts.ctypes.data, obs.ctypes.data,
+                                       rew.ctypes.data, done.ctypes.data, trunc.ctypes.data,
+                                       term.ctypes.data, mask.ctypes.data, info.ctypes.data)
+    assert rc == 0
+    np.testing.assert_array_equal(obs, ref["obs"].cpu().numpy())
+    np.testing.assert_array_equal(rew, ref["reward"].cpu().numpy())
+    np.testing.assert_array_equal(done, ref["done"].cpu().numpy())
+    np.testing.assert_array_equal(trunc, ref["trunc"].cpu().numpy())
+    np.testing.assert_array_equal(mask, ref["terminal_mask"].cpu().numpy())
+    np.testing.assert_array_equal(info, ref["info"].cpu().numpy())
+    m = mask.astype(bool)
+    assert m.sum() == 8 * n
+    np.testing.assert_array_equal(term[m], ref["terminal_obs"].cpu().numpy()[m])
