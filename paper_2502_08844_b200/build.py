@@ -21,7 +21,7 @@ LIB = os.path.join(HERE, "libdeskrl_b200.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+COMMON = [*os.environ.get("DK_NVCC_EXTRA", "").split(),"-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
 UNITS = {
     "envstep_f32.cu": [],

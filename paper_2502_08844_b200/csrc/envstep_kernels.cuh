@@ -177,6 +177,17 @@ __device__ __forceinline__ void cp_async_wait() {
 __device__ __forceinline__ void mbar_arrive_u32(uint32_t addr) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(addr) : "memory");
 }
+__device__ __forceinline__ bool mbar_test_u32(uint32_t addr, uint32_t parity) {
+    uint32_t done;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    return done != 0;
+}
 __device__ __forceinline__ void mbar_wait_u32(uint32_t addr, uint32_t parity) {
     uint32_t done = 0;
     do {
@@ -375,11 +386,22 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             }
         };
 
+        // next group's hand-off barriers, probed (non-blocking) halfway through
+        // the current group so their latency hides under the chain
+        bool next_ready = false;
 #pragma unroll 1
         for (int g = 0; g < ngroups; ++g) {
             const int sb = g % NG, ab = g % NA;
-            mbar_wait_u32(afull_b + 8 * ab, (uint32_t)(g / NA) & 1u);
-            mbar_wait_u32(empty_b + 8 * sb, (uint32_t)(g / NG) & 1u);  // phase 0 pre-armed
+            if (!next_ready) {
+                mbar_wait_u32(afull_b + 8 * ab, (uint32_t)(g / NA) & 1u);
+                mbar_wait_u32(empty_b + 8 * sb, (uint32_t)(g / NG) & 1u);  // phase 0 pre-armed
+            }
+            auto probe_next = [&]() {
+                const int g1 = g + 1;
+                next_ready = mbar_test_u32(afull_b + 8 * (g1 % NA), (uint32_t)(g1 / NA) & 1u) &&
+                             mbar_test_u32(empty_b + 8 * (g1 % NG), (uint32_t)(g1 / NG) & 1u);
+            };
+            next_ready = false;
             T *ring_g = ring + (size_t)sb * G * WF * WPC;
             T *rp_g = rpart + (size_t)sb * G * WPC;
             uint8_t *fl_g = flags + sb * G * WPC;
@@ -417,6 +439,7 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
                         }
                         world_to_slot<Task, T, WPC>(wd[t], ring_g + s * WF * WPC, t * 32 + lane);
                     }
+                    if (s == G / 2 && g + 1 < ngroups) probe_next();
                 }
 #pragma unroll
                 for (int t = 0; t < TL; ++t) steps[t] += G;

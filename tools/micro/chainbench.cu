@@ -1,0 +1,63 @@
+// Microbenchmark: latency of the cartpole f32 step chain in one warp (no memory
+// traffic, no barriers), timed with clock64.  Variants isolate sincos and the
+// 2x2 solve.  Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I.. chainbench.cu
+#include <cstdio>
+#include "../../paper_2502_08844_b200/csrc/tasks.cuh"
+
+using namespace dk;
+
+template <int V>
+__global__ void chain(float *out, long long *cyc, int steps, Params<float> p) {
+    Cartpole<float>::W w;
+    w.x = 0.1f * threadIdx.x / 32.f; w.th = 0.05f; w.xd = 0.f; w.thd = 0.01f;
+    Cartpole<float>::refresh(w);
+    float u[1] = {0.3f};
+    float acc = 0.f;
+    long long t0 = clock64();
+    for (int k = 0; k < steps; ++k) {
+        u[0] = (k & 1) ? 3.f : -3.f;
+        if (V == 0) {
+            Cartpole<float>::step_u(w, u, p);            // full step
+        } else if (V == 1) {
+            float s, c;
+            sincosf_fast(w.th, &s, &c);                  // sincos chain only
+            w.th = w.th + 0.01f * s + 1e-3f * c;
+        } else if (V == 2) {
+            // 2x2 solve + Euler without trig (s, c fixed)
+            const float m12 = p.pole_mass * p.pole_length * w.c;
+            const float det = (p.cart_mass + p.pole_mass) * (p.pole_mass * p.pole_length * p.pole_length) - m12 * m12;
+            const float thdd = RealOps<float>::div_(u[0] - m12 * w.thd, det);
+            w.thd = w.thd + p.dt * thdd;
+            w.c = w.c + p.dt * w.thd * 1e-3f;
+        } else {
+            w.th = fmaf(w.th, 1.0000001f, 1e-7f);       // 1 dependent FFMA per step
+        }
+        acc += w.x;
+    }
+    asm volatile("mov.f32 %0, %0;" : "+f"(w.th) :: "memory");  // loop result before t1
+    long long t1 = clock64();
+    out[threadIdx.x] = acc + w.th + w.thd + w.c;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
+int main() {
+    float *out; long long *cyc;
+    cudaMalloc(&out, 128 * sizeof(float));
+    cudaMalloc(&cyc, sizeof(long long));
+    Params<float> p{0.01f, 9.81f, 1.f, .5f, .05f, 2.5f, 1.f, .1f, .5f, 1.8f, 10.f, 1.f, 1.f, 1.f, 1.f, 0.f, 8.f, 1.f};
+    const int steps = 100000;
+    const char *names[4] = {"full cartpole step_u", "sincosf_fast chain", "2x2 solve + euler", "1 FFMA/step"};
+    for (int v = 0; v < 4; ++v) {
+        for (int rep = 0; rep < 2; ++rep) {
+            if (v == 0) chain<0><<<1, 32>>>(out, cyc, steps, p);
+            if (v == 1) chain<1><<<1, 32>>>(out, cyc, steps, p);
+            if (v == 2) chain<2><<<1, 32>>>(out, cyc, steps, p);
+            if (v == 3) chain<3><<<1, 32>>>(out, cyc, steps, p);
+            cudaDeviceSynchronize();
+        }
+        long long c;
+        cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
+        printf("%-24s %.1f cycles/step\n", names[v], (double)c / steps);
+    }
+    return 0;
+}
