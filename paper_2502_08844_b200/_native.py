@@ -10,7 +10,9 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdeskrl_b200.so")
+# DK_LIB_PATH: developer hook to load an experimental build (tools/exp_variants.sh);
+# the default is the in-tree library.
+LIB_PATH = os.environ.get("DK_LIB_PATH") or os.path.join(_HERE, "libdeskrl_b200.so")
 
 DK_OK, DK_ERR_CONFIG, DK_ERR_INVALID_INPUT, DK_ERR_USAGE, DK_ERR_CUDA = range(5)
 DK_F32, DK_F64 = 0, 1

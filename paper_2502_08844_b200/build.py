@@ -21,7 +21,13 @@ LIB = os.path.join(HERE, "libdeskrl_b200.so")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-COMMON = [*os.environ.get("DK_NVCC_EXTRA", "").split(),"-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+# DK_NVCC_EXTRA / DK_LIB_OUT / DK_OBJ_DIR: developer hooks for experimental
+# variants (tools/exp_variants.sh); unset for the product build.
+if os.environ.get("DK_LIB_OUT"):
+    LIB = os.path.abspath(os.environ["DK_LIB_OUT"])
+if os.environ.get("DK_OBJ_DIR"):
+    OBJDIR = os.path.abspath(os.environ["DK_OBJ_DIR"])
+COMMON = [*os.environ.get("DK_NVCC_EXTRA", "").split(), "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
           "-I", os.path.join(ROOT, "include")]
 UNITS = {
     "envstep_f32.cu": [],

@@ -86,6 +86,7 @@ struct dk_env {
     uint32_t *blocks_done = nullptr;          // last-block counter (device)
     unsigned long long *err_dev = nullptr;
     unsigned long long *err_host = nullptr;  // pinned
+    bool err_stale = false;  // a device-pointer launch ran since err_host was refreshed
     int64_t launches = 0;
     cudaStream_t s_comp = nullptr, s_h2d = nullptr, s_d2h = nullptr;
     cudaEvent_t ev_h2d[2] = {}, ev_comp[2] = {}, ev_d2h[2] = {};
@@ -139,7 +140,7 @@ dk::Worlds<T> worlds(const dk_env *e) {
 
 int rollout_impl(dk_env *e, int64_t K, const void *actions, int autoreset, void *obs, void *reward,
                  uint8_t *done, uint8_t *trunc, void *term_obs, uint8_t *term_mask, void *info,
-                 cudaStream_t st) {
+                 cudaStream_t st, bool copy_err) {
     if (!actions || !obs || !reward || !done || !trunc)
         return fail(DK_ERR_INVALID_INPUT, "actions, obs, reward, done and trunc are required");
     if (K < 0) return fail(DK_ERR_INVALID_INPUT, "num_steps must be >= 0");
@@ -161,9 +162,16 @@ int rollout_impl(dk_env *e, int64_t K, const void *actions, int autoreset, void 
                                        e->err_dev, st, &e->launches);
     }
     if (rc != cudaSuccess) return fail(DK_ERR_CUDA, "rollout launch: %s", cudaGetErrorString(rc));
-    // error word -> pinned host copy (read by dk_env_check_error after a sync)
-    DK_CUDA(cudaMemcpyAsync(e->err_host, e->err_dev, sizeof(unsigned long long),
-                            cudaMemcpyDeviceToHost, st));
+    // error word -> pinned host copy.  The _host entry points queue it behind
+    // every launch (they synchronise anyway); the device-pointer entry points
+    // leave it to dk_env_check_error, so back-to-back launches are not separated
+    // by a copy-engine round trip (~20 us per launch measured on B200).
+    if (copy_err) {
+        DK_CUDA(cudaMemcpyAsync(e->err_host, e->err_dev, sizeof(unsigned long long),
+                                cudaMemcpyDeviceToHost, st));
+    } else {
+        e->err_stale = true;
+    }
     return DK_OK;
 }
 
@@ -343,6 +351,7 @@ int dk_env_reset(dk_env *e, int has_seed, uint64_t seed, void *obs_out, void *st
     DK_CUDA(cudaMemsetAsync(e->err_dev, 0xff, sizeof(unsigned long long), st));
     DK_CUDA(cudaMemcpyAsync(e->err_host, e->err_dev, sizeof(unsigned long long),
                             cudaMemcpyDeviceToHost, st));
+    e->err_stale = false;
     const dk::EnvScalars sc = scalars(e, 1);
     cudaError_t rc;
     if (e->cfg.dtype == DK_F64)
@@ -363,7 +372,7 @@ int dk_env_step(dk_env *e, const void *actions, int autoreset, void *obs, void *
     if (int rc = check_env(e)) return rc;
     DeviceGuard g(e->device);
     return rollout_impl(e, 1, actions, autoreset, obs, reward, done, trunc, term_obs, term_mask,
-                        info, (cudaStream_t)stream);
+                        info, (cudaStream_t)stream, false);
 }
 
 int dk_env_rollout(dk_env *e, int64_t K, const void *actions, void *obs, void *reward,
@@ -372,7 +381,7 @@ int dk_env_rollout(dk_env *e, int64_t K, const void *actions, void *obs, void *r
     if (int rc = check_env(e)) return rc;
     DeviceGuard g(e->device);
     return rollout_impl(e, K, actions, 1, obs, reward, done, trunc, term_obs, term_mask, info,
-                        (cudaStream_t)stream);
+                        (cudaStream_t)stream, false);
 }
 
 int dk_env_check_error(dk_env *e, void *stream, int64_t *step_index, int64_t *env_index) {
@@ -380,6 +389,11 @@ int dk_env_check_error(dk_env *e, void *stream, int64_t *step_index, int64_t *en
     DeviceGuard g(e->device);
     DK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
     DK_CUDA(cudaStreamSynchronize(e->s_comp));
+    if (e->err_stale) {
+        DK_CUDA(cudaMemcpy(e->err_host, e->err_dev, sizeof(unsigned long long),
+                           cudaMemcpyDeviceToHost));
+        e->err_stale = false;
+    }
     const unsigned long long key = *e->err_host;
     if (key == dk::kNoError) return DK_OK;
     *e->err_host = dk::kNoError;
@@ -411,7 +425,7 @@ int dk_env_step_host(dk_env *e, const void *actions, int autoreset, void *obs, v
                             st));
     if (int rc = rollout_impl(e, 1, e->hs.actions[0], autoreset, e->hs.obs[0], e->hs.reward[0],
                               e->hs.done[0], e->hs.trunc[0], e->hs.term[0], e->hs.mask[0],
-                              info ? e->hs.info[0] : nullptr, st))
+                              info ? e->hs.info[0] : nullptr, st, true))
         return rc;
     DK_CUDA(cudaMemcpyAsync(obs, e->hs.obs[0], n * e->O * e->esz, cudaMemcpyDeviceToHost, st));
     DK_CUDA(cudaMemcpyAsync(reward, e->hs.reward[0], n * e->esz, cudaMemcpyDeviceToHost, st));
@@ -507,7 +521,7 @@ int dk_env_rollout_host(dk_env *e, int64_t K, int64_t chunk, const void *actions
         if (int rc = rollout_impl(e, (int64_t)kj, e->hs.actions[b], 1, e->hs.obs[b],
                                   e->hs.reward[b], e->hs.done[b], e->hs.trunc[b],
                                   term_obs ? e->hs.term[b] : nullptr, e->hs.mask[b],
-                                  info ? e->hs.info[b] : nullptr, e->s_comp))
+                                  info ? e->hs.info[b] : nullptr, e->s_comp, true))
             return rc;
         DK_CUDA(cudaEventRecord(e->ev_comp[b], e->s_comp));
         // D2H of the outputs

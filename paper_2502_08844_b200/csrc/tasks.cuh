@@ -20,6 +20,7 @@
 //   obs(W&, P, o[O])         state_obs of the current state
 //   sample(W&, Philox&, P, wide)  sample_initial + refresh
 #pragma once
+#include <type_traits>
 #include "envmath.cuh"
 
 namespace dk {
@@ -125,12 +126,26 @@ struct Cartpole {
         const T r1 = force + mp * l * w.thd * w.thd * w.s;
         const T r2 = mp * g * l * w.s;
         const T det = m11 * m22 - m12 * m12;
-        const T xddot = RealOps<T>::div_(m22 * r1 - m12 * r2, det);
-        const T thetaddot = RealOps<T>::div_(m11 * r2 - m12 * r1, det);
-        w.xd = w.xd + p.dt * xddot;
-        w.thd = w.thd + p.dt * thetaddot;
-        w.x = w.x + p.dt * w.xd;
-        w.th = w.th + p.dt * w.thd;
+        if constexpr (std::is_same<T, float>::value) {
+            // f32 (tolerance-checked, not bit-exact): one reciprocal, and the
+            // angle update folded as th + dt*thd + dt^2*thdd so that only one
+            // FFMA follows the reciprocal on the th -> sincos -> th chain.
+            const float rdet = RealOps<float>::div_(1.0f, det);
+            const float nx = m22 * r1 - m12 * r2, nth = m11 * r2 - m12 * r1;
+            const float dt = p.dt;
+            const float thb = fmaf(dt, w.thd, w.th);
+            w.xd = fmaf(dt * nx, rdet, w.xd);
+            w.thd = fmaf(dt * nth, rdet, w.thd);
+            w.th = fmaf(dt * dt * nth, rdet, thb);
+            w.x = fmaf(dt, w.xd, w.x);
+        } else {
+            const T xddot = RealOps<T>::div_(m22 * r1 - m12 * r2, det);
+            const T thetaddot = RealOps<T>::div_(m11 * r2 - m12 * r1, det);
+            w.xd = w.xd + p.dt * xddot;
+            w.thd = w.thd + p.dt * thetaddot;
+            w.x = w.x + p.dt * w.xd;
+            w.th = w.th + p.dt * w.thd;
+        }
         // inelastic rail stop (envkit.py:330-333), branch-free; NaN passes
         // through unchanged as in the reference's if/elif
         const bool hit = fabs(w.x) > p.rail_limit;

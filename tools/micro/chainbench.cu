@@ -6,6 +6,47 @@
 
 using namespace dk;
 
+// V = 4..7: the producer's fast-group body (8 steps unrolled) with its
+// shared-memory traffic: 4 = u from smem, 5 = + 6 STS per step (world_to_slot),
+// 6 = registers only but unrolled by 8, 7 = 5 with u loaded at the group start.
+template <int V>
+__global__ void group_body(float *out, long long *cyc, int steps, Params<float> p) {
+    __shared__ float ring[8][6][32];
+    __shared__ float act[8][32];
+    const int lane = threadIdx.x;
+    for (int s = 0; s < 8; ++s) act[s][lane] = (s & 1) ? 3.f : -3.f;
+    __syncwarp();
+    Cartpole<float>::W w;
+    w.x = 0.1f * lane / 32.f; w.th = 0.05f; w.xd = 0.f; w.thd = 0.01f;
+    Cartpole<float>::refresh(w);
+    long long t0 = clock64();
+    for (int g = 0; g < steps / 8; ++g) {
+        float ua[8];
+        if (V == 7) {
+#pragma unroll
+            for (int s = 0; s < 8; ++s) ua[s] = act[s][lane];
+        }
+#pragma unroll
+        for (int s = 0; s < 8; ++s) {
+            float u[1];
+            if (V == 6) u[0] = (s & 1) ? 3.f : -3.f;
+            else if (V == 7) u[0] = ua[s];
+            else u[0] = act[s][lane];
+            Cartpole<float>::step_u(w, u, p);
+            if (V == 5 || V == 7) {
+                const float *f = reinterpret_cast<const float *>(&w);
+#pragma unroll
+                for (int j = 0; j < 6; ++j) ring[s][j][lane] = f[j];
+            }
+        }
+        __syncwarp();
+    }
+    asm volatile("mov.f32 %0, %0;" : "+f"(w.th) :: "memory");
+    long long t1 = clock64();
+    out[lane] = w.th + w.thd + w.c + ring[lane & 7][lane % 6][lane];
+    if (lane == 0) cyc[0] = t1 - t0;
+}
+
 template <int V>
 __global__ void chain(float *out, long long *cyc, int steps, Params<float> p) {
     Cartpole<float>::W w;
@@ -46,13 +87,19 @@ int main() {
     cudaMalloc(&cyc, sizeof(long long));
     Params<float> p{0.01f, 9.81f, 1.f, .5f, .05f, 2.5f, 1.f, .1f, .5f, 1.8f, 10.f, 1.f, 1.f, 1.f, 1.f, 0.f, 8.f, 1.f};
     const int steps = 100000;
-    const char *names[4] = {"full cartpole step_u", "sincosf_fast chain", "2x2 solve + euler", "1 FFMA/step"};
-    for (int v = 0; v < 4; ++v) {
+    const char *names[8] = {"full cartpole step_u", "sincosf_fast chain", "2x2 solve + euler", "1 FFMA/step",
+                            "group: u from smem", "group: u smem + 6 STS", "group: regs, unroll 8",
+                            "group: u preload + 6 STS"};
+    for (int v = 0; v < 8; ++v) {
         for (int rep = 0; rep < 2; ++rep) {
             if (v == 0) chain<0><<<1, 32>>>(out, cyc, steps, p);
             if (v == 1) chain<1><<<1, 32>>>(out, cyc, steps, p);
             if (v == 2) chain<2><<<1, 32>>>(out, cyc, steps, p);
             if (v == 3) chain<3><<<1, 32>>>(out, cyc, steps, p);
+            if (v == 4) group_body<4><<<1, 32>>>(out, cyc, steps, p);
+            if (v == 5) group_body<5><<<1, 32>>>(out, cyc, steps, p);
+            if (v == 6) group_body<6><<<1, 32>>>(out, cyc, steps, p);
+            if (v == 7) group_body<7><<<1, 32>>>(out, cyc, steps, p);
             cudaDeviceSynchronize();
         }
         long long c;
