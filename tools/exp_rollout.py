@@ -19,6 +19,8 @@ def main():
     ap.add_argument("--steps", type=int, default=1000)
     ap.add_argument("--launches", type=int, default=20)
     ap.add_argument("--tag", default=os.environ.get("DK_LIB_PATH", "tree"))
+    ap.add_argument("--events", action="store_true", help="record events around every launch")
+    ap.add_argument("--ring", type=int, default=1, help="distinct action/output buffers")
     a = ap.parse_args()
     import torch
 
@@ -28,8 +30,11 @@ def main():
     for n in [int(x) for x in a.worlds.split(",")]:
         env = dk.DeviceBatchEnv(dk.EnvConfig(task=a.task), n, dtype=a.dtype)
         env.reset(seed=0)
-        acts = torch.rand((a.steps, n, env.action_dim), device="cuda", dtype=env.dtype) * 2 - 1
-        out = env._outputs((a.steps,), True)
+        acts_r = [torch.rand((a.steps, n, env.action_dim), device="cuda", dtype=env.dtype) * 2 - 1
+                  for _ in range(a.ring)]
+        out_r = [env._outputs((a.steps,), True) for _ in range(a.ring)]
+        acts, out = acts_r[0], out_r[0]
+        evs = [torch.cuda.Event(enable_timing=True) for _ in range(2 * a.launches)]
         for _ in range(3):
             env.rollout(acts, with_info=True, out=out)
         torch.cuda.synchronize()
@@ -37,8 +42,12 @@ def main():
         import time
         e0.record()
         h0 = time.perf_counter()
-        for _ in range(a.launches):
-            env.rollout(acts, with_info=True, out=out)
+        for L in range(a.launches):
+            if a.events:
+                evs[2 * L].record()
+            env.rollout(acts_r[L % a.ring], with_info=True, out=out_r[L % a.ring])
+            if a.events:
+                evs[2 * L + 1].record()
         host_us = (time.perf_counter() - h0) * 1e6 / a.launches
         e1.record()
         torch.cuda.synchronize()
