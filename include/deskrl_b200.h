@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DK_ABI_VERSION 1
+#define DK_ABI_VERSION 2  /* 2: sensor-noise kinds, randomize_params, delay lines */
 
 /* Status codes.  The Python host maps them to the reference's exception
  * classes: ConfigError (randomization.py:19), InvalidInputError
@@ -231,11 +231,42 @@ int dk_loco_phase(int dtype, int64_t n, int num_feet, const void *phi, const voi
 int dk_loco_progress_clip(int dtype, int64_t n, const void *raw, void *history_max, void *reward,
                           void *stream);
 
-/* apply_sensor_noise, uniform kind (randomization.py:88-108), in place on obs
- * [n, dim]; specs as device arrays (offset, length, scale) in spec order. */
+/* apply_sensor_noise (randomization.py:88-108), in place on obs [n, dim];
+ * specs as device arrays (offset, length, scale, kind) in spec order; kind 0 =
+ * uniform U(-scale, scale), 1 = gaussian Generator.normal(0, scale) (NumPy's
+ * ziggurat, bit-compatible); kind may be NULL (all uniform).  Each world draws
+ * from stream_rng(seed, env_index_offset + world, episode, step). */
 int dk_dr_sensor_noise(int dtype, int64_t n, int dim, void *obs, int num_specs,
                        const int32_t *spec_offset, const int32_t *spec_length,
-                       const double *spec_scale, const dk_noise_key *key, void *stream);
+                       const double *spec_scale, const int32_t *spec_kind,
+                       const dk_noise_key *key, void *stream);
+
+/* randomize_params (randomization.py:156-181) for n worlds, float64: out
+ * [n, num_fields] = nominal [num_fields] with ranges r (device arrays, spec
+ * order) applied to field[r]: distribution 0 uniform_additive, 1
+ * uniform_multiplicative, 2 log_uniform (low/high already log()ed by the
+ * caller); a positive nominal is redrawn while non-positive, up to 100 tries.
+ * fail_world: device u64 the caller initialises to ~0; receives
+ * world * num_ranges + range of the first world (then range) that could not
+ * be drawn (ConfigError, randomization.py:179). */
+int dk_dr_randomize_params(int64_t n, int num_fields, const double *nominal, int num_ranges,
+                           const int32_t *field, const int32_t *distribution, const double *low,
+                           const double *high, const dk_noise_key *key, double *out,
+                           unsigned long long *fail_world, void *stream);
+
+/* DelayLine (randomization.py:27-62) for n worlds.  State (device): ring
+ * [n, max_delay + 1, dim] of dtype, head / count / delay [n] int32.
+ * reset: empties every line and draws its episode delay
+ * Generator.integers(min_delay, max_delay + 1) from the world's stream.
+ * push_pop: appends value [n, dim] and writes out [n, dim] = the value aged
+ * d steps (d = episode delay, or a fresh per-step draw when per_step), the
+ * oldest held value during warm-up. */
+int dk_dr_delay_reset(int64_t n, int min_delay, int max_delay, const dk_noise_key *key,
+                      int32_t *delay, int32_t *count, int32_t *head, void *stream);
+int dk_dr_delay_push_pop(int dtype, int64_t n, int dim, int min_delay, int max_delay,
+                         int per_step, void *ring, int32_t *head, int32_t *count,
+                         const int32_t *delay, const dk_noise_key *key, const void *value,
+                         void *out, void *stream);
 
 /* pose_injection (randomization.py:188-199), in place on pose [n, dim];
  * bounds device double [dim, 2]; injected [n] u8 (may be NULL). */

@@ -8,8 +8,18 @@
  *   envkit.py:196-202      progress_clip_reward
  *   mathcore.py:42-97      quat_check_unit, quat_mul/conj/rotate, project_gravity
  *   mathcore.py:143-177    wrap_angle, advance_phase, phase_encode
- *   randomization.py:88-108, 188-199, 224-238  uniform sensor noise, pose injection,
- *                          curriculum_update
+ *   randomization.py:27-62   DelayLine (reset / push_pop) with Generator.integers
+ *   randomization.py:88-108  apply_sensor_noise, uniform and gaussian kinds
+ *   randomization.py:156-181 randomize_params (additive / multiplicative / log-uniform,
+ *                            positivity resampling, <= 100 tries)
+ *   randomization.py:188-199, 224-238  pose injection, curriculum_update
+ * NumPy dependencies restated (NumPy 2.3, numpy/random/src/distributions/):
+ *   Generator.normal    = loc + scale * random_standard_normal (256-layer ziggurat,
+ *                         tables in paper_2502_08844_b200/csrc/ziggurat_tables.h,
+ *                         generated and checked by tools/gen_ziggurat_tables.py)
+ *   Generator.integers  = random_bounded_uint64_fill: Lemire's nearly-divisionless
+ *                         method on next_uint32 (Philox keeps the unused high half of
+ *                         a 64-bit word for the next 32-bit draw) or next_uint64
  * Parity: pinned against tests/golden/loco_golden.npz (generated from the reference
  * by tests/golden/make_golden_loco.py).  Integer / selection logic is bit-exact;
  * sums of products are sequential here, where NumPy uses BLAS dot / pairwise sums
@@ -46,6 +56,85 @@ static uint64_t px_next(orc_philox_state *p) {
 static double px_uniform(orc_philox_state *p, double lo, double hi) {
     double range = hi - lo;
     return lo + range * ((double)(px_next(p) >> 11) * (1.0 / 9007199254740992.0));
+}
+static double px_double(orc_philox_state *p) {
+    return (double)(px_next(p) >> 11) * (1.0 / 9007199254740992.0);
+}
+
+#define DK_ZIG_QUAL static const
+#include "../paper_2502_08844_b200/csrc/ziggurat_tables.h"
+
+/* random_standard_normal (distributions.c) */
+static double px_normal(orc_philox_state *p) {
+    for (;;) {
+        uint64_t r = px_next(p);
+        const int idx = (int)(r & 0xff);
+        r >>= 8;
+        const int sign = (int)(r & 1);
+        const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+        double x = (double)rabs * dk_zig_wi[idx];
+        if (sign) x = -x;
+        if (rabs < dk_zig_ki[idx]) return x;
+        if (idx == 0) {
+            for (;;) {
+                const double xx = -DK_ZIG_NOR_INV_R * log1p(-px_double(p));
+                const double yy = -log1p(-px_double(p));
+                if (yy + yy > xx * xx)
+                    return ((rabs >> 8) & 1) ? -(DK_ZIG_NOR_R + xx) : DK_ZIG_NOR_R + xx;
+            }
+        } else {
+            if (((dk_zig_fi[idx - 1] - dk_zig_fi[idx]) * px_double(p) + dk_zig_fi[idx]) <
+                exp(-0.5 * x * x))
+                return x;
+        }
+    }
+}
+
+/* Generator.integers(low, high) (high exclusive): random_bounded_uint64_fill */
+typedef struct {
+    orc_philox_state px;
+    int has32;
+    uint32_t u32;
+} orc_px32;
+static uint32_t px_next32(orc_px32 *p) {
+    if (p->has32) {
+        p->has32 = 0;
+        return p->u32;
+    }
+    const uint64_t v = px_next(&p->px);
+    p->has32 = 1;
+    p->u32 = (uint32_t)(v >> 32);
+    return (uint32_t)v;
+}
+static int64_t px_integers(orc_px32 *p, int64_t low, int64_t high) {
+    const uint64_t rng = (uint64_t)(high - 1 - low);
+    if (rng == 0) return low;
+    if (rng <= 0xFFFFFFFFULL) {
+        if (rng == 0xFFFFFFFFULL) return low + (int64_t)px_next32(p);
+        const uint32_t excl = (uint32_t)rng + 1u;
+        uint64_t m = (uint64_t)px_next32(p) * excl;
+        uint32_t left = (uint32_t)m;
+        if (left < excl) {
+            const uint32_t thr = (uint32_t)(0xFFFFFFFFu - (uint32_t)rng) % excl;
+            while (left < thr) {
+                m = (uint64_t)px_next32(p) * excl;
+                left = (uint32_t)m;
+            }
+        }
+        return low + (int64_t)(m >> 32);
+    }
+    if (rng == 0xFFFFFFFFFFFFFFFFULL) return low + (int64_t)px_next(&p->px);
+    const uint64_t excl = rng + 1;
+    uint64_t x = px_next(&p->px);
+    uint64_t left = x * excl;
+    if (left < excl) {
+        const uint64_t thr = (0xFFFFFFFFFFFFFFFFULL - rng) % excl;
+        while (left < thr) {
+            x = px_next(&p->px);
+            left = x * excl;
+        }
+    }
+    return low + (int64_t)(uint64_t)(((unsigned __int128)x * excl) >> 64);
 }
 
 /* RewardTermConfig, rewards.py:51-75, field order preserved */
@@ -308,8 +397,9 @@ void orc_advance_phase(int64_t n, int nf, const double *phi, const double *freq,
 /* randomization.py:88-108 (uniform kind): specs given as (offset, length, scale) triples
  * over one flat observation row; stream of row i = stream_rng(seed, env0 + i, ep, step). */
 void orc_sensor_noise(int64_t n, int dim, const double *obs, int nspec, const int32_t *spec_off,
-                      const int32_t *spec_len, const double *spec_scale, uint64_t seed,
-                      int64_t env0, int64_t episode, uint64_t step, double *out) {
+                      const int32_t *spec_len, const double *spec_scale,
+                      const int32_t *spec_kind /* 0 uniform, 1 gaussian; NULL = uniform */,
+                      uint64_t seed, int64_t env0, int64_t episode, uint64_t step, double *out) {
     for (int64_t i = 0; i < n; ++i) {
         memcpy(out + (int64_t)dim * i, obs + (int64_t)dim * i, sizeof(double) * dim);
         orc_philox_state px;
@@ -319,10 +409,109 @@ void orc_sensor_noise(int64_t n, int dim, const double *obs, int nspec, const in
             if (sc == 0.0) continue;
             for (int k = 0; k < spec_len[s]; ++k) {
                 double *x = out + (int64_t)dim * i + spec_off[s] + k;
-                *x = *x + px_uniform(&px, -sc, sc);
+                if (spec_kind && spec_kind[s] == 1)
+                    *x = *x + (0.0 + sc * px_normal(&px));  /* Generator.normal(0, sc) */
+                else
+                    *x = *x + px_uniform(&px, -sc, sc);
             }
         }
     }
+}
+
+/* randomize_params (randomization.py:156-181) for n worlds: nominal [F];
+ * ranges (field, distribution 0 additive / 1 multiplicative / 2 log-uniform,
+ * low, high) in spec order; out [n, F].  Returns -1, or the first world whose
+ * field could not be drawn positive in 100 tries (ConfigError). */
+int64_t orc_randomize_params(int64_t n, int nf, const double *nominal, int nr, const int32_t *field,
+                             const int32_t *dist, const double *low, const double *high,
+                             uint64_t seed, int64_t env0, int64_t episode, uint64_t step,
+                             double *out) {
+    int64_t fail = -1;
+    for (int64_t i = 0; i < n; ++i) {
+        double *o = out + i * nf;
+        memcpy(o, nominal, sizeof(double) * nf);
+        orc_philox_state px;
+        px_init(&px, seed, (uint64_t)(env0 + i), episode, step);
+        for (int r = 0; r < nr; ++r) {
+            const double base = nominal[field[r]];
+            const int positive = base > 0;
+            double value = 0.0;
+            int ok = 0;
+            for (int attempt = 0; attempt < 100; ++attempt) {
+                if (dist[r] == 0)
+                    value = base + px_uniform(&px, low[r], high[r]);
+                else if (dist[r] == 1)
+                    value = base * px_uniform(&px, low[r], high[r]);
+                else
+                    value = base * exp(px_uniform(&px, log(low[r]), log(high[r])));
+                if (!positive || value > 0) {
+                    ok = 1;
+                    break;
+                }
+            }
+            if (!ok && fail < 0) fail = i;
+            o[field[r]] = value;
+        }
+    }
+    return fail;
+}
+
+/* DelayLine (randomization.py:27-62), batched: ring [n, cap, dim] with
+ * cap = max_delay + 1, head = next write slot, count = items held.
+ * reset: count = head = 0 and, per world, delay = integers(min, max + 1) from
+ * the world's stream (randomization.py:44-46). */
+void orc_delay_reset(int64_t n, int min_delay, int max_delay, uint64_t seed, int64_t env0,
+                     int64_t episode, uint64_t step, int32_t *delay, int32_t *count,
+                     int32_t *head) {
+    for (int64_t i = 0; i < n; ++i) {
+        orc_px32 p;
+        px_init(&p.px, seed, (uint64_t)(env0 + i), episode, step);
+        p.has32 = 0;
+        delay[i] = (int32_t)px_integers(&p, min_delay, (int64_t)max_delay + 1);
+        count[i] = 0;
+        head[i] = 0;
+    }
+}
+
+/* push_pop (randomization.py:56-62): append value, draw the delay per step (or
+ * use the episode's), return the element len-1-d (clamped to the oldest). */
+void orc_delay_push_pop(int64_t n, int dim, int min_delay, int max_delay, int per_step,
+                        double *ring, int32_t *head, int32_t *count, const int32_t *delay,
+                        uint64_t seed, int64_t env0, int64_t episode, uint64_t step,
+                        const double *value, double *out) {
+    const int cap = max_delay + 1;
+    for (int64_t i = 0; i < n; ++i) {
+        double *rb = ring + i * (int64_t)cap * dim;
+        memcpy(rb + (int64_t)head[i] * dim, value + i * dim, sizeof(double) * dim);
+        head[i] = (head[i] + 1) % cap;
+        if (count[i] < cap) count[i] += 1;
+        int d = delay[i];
+        if (per_step) {
+            orc_px32 p;
+            px_init(&p.px, seed, (uint64_t)(env0 + i), episode, step);
+            p.has32 = 0;
+            d = (int)px_integers(&p, min_delay, (int64_t)max_delay + 1);
+        }
+        int idx = count[i] - 1 - d;
+        if (idx < 0) idx = 0;
+        const int slot = ((head[i] - count[i] + idx) % cap + cap) % cap;
+        memcpy(out + i * dim, rb + (int64_t)slot * dim, sizeof(double) * dim);
+    }
+}
+
+/* Generator.standard_normal / integers on one stream (oracle self-checks) */
+void orc_stream_normal(uint64_t seed, uint64_t env, int64_t episode, uint64_t step, int64_t count,
+                       double *out) {
+    orc_philox_state px;
+    px_init(&px, seed, env, episode, step);
+    for (int64_t k = 0; k < count; ++k) out[k] = px_normal(&px);
+}
+void orc_stream_integers(uint64_t seed, uint64_t env, int64_t episode, uint64_t step,
+                         int64_t low, int64_t high, int64_t count, int64_t *out) {
+    orc_px32 p;
+    px_init(&p.px, seed, env, episode, step);
+    p.has32 = 0;
+    for (int64_t k = 0; k < count; ++k) out[k] = px_integers(&p, low, high);
 }
 
 /* randomization.py:188-199 */

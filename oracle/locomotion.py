@@ -146,19 +146,89 @@ def advance_phase(phi, freq, dt):
 
 
 def sensor_noise(obs, specs, key):
-    """specs: list of (offset, length, scale)."""
+    """specs: list of (offset, length, scale[, kind]) -- kind "uniform" / "gaussian"."""
     obs = np.ascontiguousarray(obs, dtype=np.float64)
     n, dim = obs.shape
     off = np.array([s[0] for s in specs], dtype=np.int32)
     ln = np.array([s[1] for s in specs], dtype=np.int32)
     sc = np.array([s[2] for s in specs], dtype=np.float64)
+    kd = np.array([1 if len(s) > 3 and s[3] == "gaussian" else 0 for s in specs], dtype=np.int32)
     out = np.zeros_like(obs)
     seed, env0, ep, step = key
     _lib().orc_sensor_noise(ctypes.c_int64(n), dim, _vp(obs), len(specs), _vp(off),
-                            _vp(ln), _vp(sc), ctypes.c_uint64(seed),
+                            _vp(ln), _vp(sc), _vp(kd), ctypes.c_uint64(seed),
                             ctypes.c_int64(env0), ctypes.c_int64(ep), ctypes.c_uint64(step),
                             _vp(out))
     return out
+
+
+def stream_normal(key, count):
+    """Generator.standard_normal(count) of stream_rng(*key)."""
+    out = np.zeros(count)
+    seed, env, ep, step = key
+    _lib().orc_stream_normal(ctypes.c_uint64(seed), ctypes.c_uint64(env), ctypes.c_int64(ep),
+                             ctypes.c_uint64(step), ctypes.c_int64(count), _vp(out))
+    return out
+
+
+def stream_integers(key, low, high, count):
+    """[Generator.integers(low, high) for _ in range(count)] of stream_rng(*key)."""
+    out = np.zeros(count, dtype=np.int64)
+    seed, env, ep, step = key
+    _lib().orc_stream_integers(ctypes.c_uint64(seed), ctypes.c_uint64(env), ctypes.c_int64(ep),
+                               ctypes.c_uint64(step), ctypes.c_int64(low), ctypes.c_int64(high),
+                               ctypes.c_int64(count), _vp(out))
+    return out
+
+
+DISTRIBUTIONS = {"uniform_additive": 0, "uniform_multiplicative": 1, "log_uniform": 2}
+
+
+def randomize_params(nominal, ranges, n, key):
+    """nominal [F]; ranges: list of (field_index, distribution, low, high).
+    Returns (out [n, F], first failing world or -1)."""
+    nom = np.ascontiguousarray(nominal, dtype=np.float64)
+    fld = np.array([r[0] for r in ranges], dtype=np.int32)
+    dst = np.array([DISTRIBUTIONS[r[1]] for r in ranges], dtype=np.int32)
+    lo = np.array([r[2] for r in ranges], dtype=np.float64)
+    hi = np.array([r[3] for r in ranges], dtype=np.float64)
+    out = np.zeros((n, nom.size))
+    seed, env0, ep, step = key
+    lib = _lib()
+    lib.orc_randomize_params.restype = ctypes.c_int64
+    fail = lib.orc_randomize_params(ctypes.c_int64(n), nom.size, _vp(nom), len(ranges), _vp(fld),
+                                    _vp(dst), _vp(lo), _vp(hi), ctypes.c_uint64(seed),
+                                    ctypes.c_int64(env0), ctypes.c_int64(ep),
+                                    ctypes.c_uint64(step), _vp(out))
+    return out, int(fail)
+
+
+class DelayLines:
+    """n batched DelayLine rings (randomization.py:27-62) for oracle checks."""
+
+    def __init__(self, n, dim, min_delay, max_delay, per_step=False):
+        self.n, self.dim, self.lo, self.hi, self.per_step = n, dim, min_delay, max_delay, per_step
+        self.ring = np.zeros((n, max_delay + 1, dim))
+        self.head = np.zeros(n, np.int32)
+        self.count = np.zeros(n, np.int32)
+        self.delay = np.zeros(n, np.int32)
+
+    def reset(self, key):
+        seed, env0, ep, step = key
+        _lib().orc_delay_reset(ctypes.c_int64(self.n), self.lo, self.hi, ctypes.c_uint64(seed),
+                               ctypes.c_int64(env0), ctypes.c_int64(ep), ctypes.c_uint64(step),
+                               _vp(self.delay), _vp(self.count), _vp(self.head))
+
+    def push_pop(self, value, key):
+        v = np.ascontiguousarray(value, dtype=np.float64).reshape(self.n, self.dim)
+        out = np.zeros_like(v)
+        seed, env0, ep, step = key
+        _lib().orc_delay_push_pop(ctypes.c_int64(self.n), self.dim, self.lo, self.hi,
+                                  int(self.per_step), _vp(self.ring), _vp(self.head),
+                                  _vp(self.count), _vp(self.delay), ctypes.c_uint64(seed),
+                                  ctypes.c_int64(env0), ctypes.c_int64(ep), ctypes.c_uint64(step),
+                                  _vp(v), _vp(out))
+        return out
 
 
 def pose_injection(pose, bounds, prob, key):

@@ -109,7 +109,15 @@ _SIGS = {
                                      _vp]),
     "dk_loco_progress_clip": (ctypes.c_int, [ctypes.c_int, _i64, _vp, _vp, _vp, _vp]),
     "dk_dr_sensor_noise": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_int,
-                                          _vp, _vp, _vp, ctypes.POINTER(NoiseKeyC), _vp]),
+                                          _vp, _vp, _vp, _vp, ctypes.POINTER(NoiseKeyC), _vp]),
+    "dk_dr_randomize_params": (ctypes.c_int, [_i64, ctypes.c_int, _vp, ctypes.c_int, _vp, _vp,
+                                              _vp, _vp, ctypes.POINTER(NoiseKeyC), _vp, _vp,
+                                              _vp]),
+    "dk_dr_delay_reset": (ctypes.c_int, [_i64, ctypes.c_int, ctypes.c_int,
+                                         ctypes.POINTER(NoiseKeyC), _vp, _vp, _vp, _vp]),
+    "dk_dr_delay_push_pop": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp,
+                                            ctypes.POINTER(NoiseKeyC), _vp, _vp, _vp]),
     "dk_dr_pose_injection": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp,
                                             ctypes.c_double, ctypes.POINTER(NoiseKeyC), _vp,
                                             _vp]),

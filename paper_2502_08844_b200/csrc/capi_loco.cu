@@ -11,6 +11,14 @@ DK_LOCO_LAUNCHERS(extern, float)
 DK_LOCO_LAUNCHERS(extern, double)
 cudaError_t launch_curriculum(int64_t n, int64_t *state, const uint8_t *success,
                               int64_t max_level, int64_t threshold, cudaStream_t st);
+cudaError_t launch_randomize_params(int64_t n, int nf, const double *nominal, int nr,
+                                    const int *field, const int *dist, const double *lo,
+                                    const double *hi, uint64_t seed, int64_t env0,
+                                    const uint32_t *episode, uint64_t step, double *out,
+                                    unsigned long long *fail, cudaStream_t st);
+cudaError_t launch_delay_reset(int64_t n, int min_delay, int max_delay, uint64_t seed,
+                               int64_t env0, const uint32_t *episode, uint64_t step,
+                               int32_t *delay, int32_t *count, int32_t *head, cudaStream_t st);
 }  // namespace dk
 
 extern "C" int dk_internal_fail(int code, const char *msg);  // capi.cu
@@ -161,20 +169,70 @@ int dk_loco_progress_clip(int dtype, int64_t n, const void *raw, void *hist, voi
 }
 
 int dk_dr_sensor_noise(int dtype, int64_t n, int dim, void *obs, int nspec, const int32_t *off,
-                       const int32_t *len, const double *scale, const dk_noise_key *key,
-                       void *stream) {
+                       const int32_t *len, const double *scale, const int32_t *kind,
+                       const dk_noise_key *key, void *stream) {
     if (!obs || !key || (nspec > 0 && (!off || !len || !scale)))
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_dr_sensor_noise: missing argument");
     cudaStream_t st = (cudaStream_t)stream;
     if (dtype == DK_F64)
         return cuda_rc(dk::launch_sensor_noise<double>(n, dim, (double *)obs, nspec, off, len, scale,
-                                                       key->seed, key->env_index_offset,
+                                                       kind, key->seed, key->env_index_offset,
                                                        key->episode, key->step, st),
                        "sensor noise launch");
     return cuda_rc(dk::launch_sensor_noise<float>(n, dim, (float *)obs, nspec, off, len, scale,
-                                                  key->seed, key->env_index_offset, key->episode,
-                                                  key->step, st),
+                                                  kind, key->seed, key->env_index_offset,
+                                                  key->episode, key->step, st),
                    "sensor noise launch");
+}
+
+int dk_dr_randomize_params(int64_t n, int num_fields, const double *nominal, int num_ranges,
+                           const int32_t *field, const int32_t *distribution, const double *low,
+                           const double *high, const dk_noise_key *key, double *out,
+                           unsigned long long *fail_world, void *stream) {
+    if (!nominal || !out || !key || !fail_world ||
+        (num_ranges > 0 && (!field || !distribution || !low || !high)))
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_dr_randomize_params: missing argument");
+    if (num_fields <= 0 || num_ranges < 0)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_dr_randomize_params: bad sizes");
+    return cuda_rc(dk::launch_randomize_params(n, num_fields, nominal, num_ranges, field,
+                                               distribution, low, high, key->seed,
+                                               key->env_index_offset, key->episode, key->step,
+                                               out, fail_world, (cudaStream_t)stream),
+                   "randomize_params launch");
+}
+
+int dk_dr_delay_reset(int64_t n, int min_delay, int max_delay, const dk_noise_key *key,
+                      int32_t *delay, int32_t *count, int32_t *head, void *stream) {
+    if (!key || !delay || !count || !head)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_dr_delay_reset: missing argument");
+    if (min_delay < 0 || max_delay < min_delay)
+        return dk_internal_fail(DK_ERR_CONFIG, "delay bounds must satisfy 0 <= min <= max");
+    return cuda_rc(dk::launch_delay_reset(n, min_delay, max_delay, key->seed,
+                                          key->env_index_offset, key->episode, key->step, delay,
+                                          count, head, (cudaStream_t)stream),
+                   "delay reset launch");
+}
+
+int dk_dr_delay_push_pop(int dtype, int64_t n, int dim, int min_delay, int max_delay,
+                         int per_step, void *ring, int32_t *head, int32_t *count,
+                         const int32_t *delay, const dk_noise_key *key, const void *value,
+                         void *out, void *stream) {
+    if (!ring || !head || !count || !delay || !key || !value || !out)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_dr_delay_push_pop: missing argument");
+    if (min_delay < 0 || max_delay < min_delay)
+        return dk_internal_fail(DK_ERR_CONFIG, "delay bounds must satisfy 0 <= min <= max");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == DK_F64)
+        return cuda_rc(dk::launch_delay_push_pop<double>(
+                           n, dim, min_delay, max_delay, per_step, (double *)ring, head, count,
+                           delay, key->seed, key->env_index_offset, key->episode, key->step,
+                           (const double *)value, (double *)out, st),
+                       "delay push_pop launch");
+    return cuda_rc(dk::launch_delay_push_pop<float>(
+                       n, dim, min_delay, max_delay, per_step, (float *)ring, head, count, delay,
+                       key->seed, key->env_index_offset, key->episode, key->step,
+                       (const float *)value, (float *)out, st),
+                   "delay push_pop launch");
 }
 
 int dk_dr_pose_injection(int dtype, int64_t n, int dim, void *pose, const double *bounds,

@@ -321,6 +321,9 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
 
     // programmatic dependent launch: everything below may read what the
     // previous grid on the stream wrote (error word, live buffer index, state)
+#ifdef DK_EXP_EARLY_TRIGGER
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef DK_EXP_CLOCK
     const unsigned long long g_dep = gtimer();

@@ -284,11 +284,13 @@ __global__ void progress_kernel(int64_t n, const T *raw, T *hist, T *reward) {
     hist[i] = x > h ? x : h;
 }
 
-// apply_sensor_noise, uniform kind (randomization.py:88-108), in place on rows [N, dim]
+// apply_sensor_noise (randomization.py:88-108), in place on rows [N, dim]:
+// kind 0 uniform U(-s, s), kind 1 gaussian Generator.normal(0, s) = 0 + s * z.
 template <typename T>
 __global__ void sensor_noise_kernel(int64_t n, int dim, T *obs, int nspec, const int *off,
-                                    const int *len, const double *scale, uint64_t seed,
-                                    int64_t env0, const uint32_t *episode, uint64_t step) {
+                                    const int *len, const double *scale, const int *kind,
+                                    uint64_t seed, int64_t env0, const uint32_t *episode,
+                                    uint64_t step) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     Philox4x64 rng;
@@ -296,11 +298,93 @@ __global__ void sensor_noise_kernel(int64_t n, int dim, T *obs, int nspec, const
     for (int s = 0; s < nspec; ++s) {
         const double sc = scale[s];
         if (sc == 0.0) continue;
+        const bool gauss = kind != nullptr && kind[s] == 1;
         for (int k = 0; k < len[s]; ++k) {
             T *x = obs + i * dim + off[s] + k;
-            *x = *x + (T)rng.uniform(-sc, sc);
+            const double z = gauss ? __dadd_rn(0.0, __dmul_rn(sc, rng.standard_normal()))
+                                   : rng.uniform(-sc, sc);
+            *x = (T)__dadd_rn((double)*x, z);
         }
     }
+}
+
+// randomize_params (randomization.py:156-181) for n worlds, f64: out [n, F]
+// starts as nominal [F]; ranges r (spec order) perturb field[r] with
+// distribution 0 additive base + U(lo, hi), 1 multiplicative base * U(lo, hi),
+// 2 log-uniform base * exp(U(log lo, log hi)) (logs precomputed on the host),
+// redrawn up to 100 times while a positive nominal goes non-positive.  A world
+// that exhausts the tries reports world * nr + range through fail (atomicMin:
+// the first such world, then its first such range -> ConfigError).
+static __global__ void randomize_params_kernel(int64_t n, int nf, const double *nominal, int nr,
+                                               const int *field, const int *dist,
+                                               const double *lo, const double *hi,
+                                               uint64_t seed, int64_t env0,
+                                               const uint32_t *episode, uint64_t step,
+                                               double *out, unsigned long long *fail) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double *o = out + i * nf;
+    for (int f = 0; f < nf; ++f) o[f] = nominal[f];
+    Philox4x64 rng;
+    rng.init(seed, (uint64_t)(env0 + i), episode ? episode[i] : 0u, step);
+    for (int r = 0; r < nr; ++r) {
+        const double base = nominal[field[r]];
+        const bool positive = base > 0.0;
+        double value = 0.0;
+        bool ok = false;
+        for (int attempt = 0; attempt < 100 && !ok; ++attempt) {
+            const double u = rng.uniform(lo[r], hi[r]);
+            value = dist[r] == 0 ? __dadd_rn(base, u)
+                  : dist[r] == 1 ? __dmul_rn(base, u)
+                                 : __dmul_rn(base, exp(u));
+            ok = !positive || value > 0.0;
+        }
+        if (!ok) atomicMin(fail, (unsigned long long)(i * nr + r));  // first world, then range
+        o[field[r]] = value;
+    }
+}
+
+// DelayLine (randomization.py:27-62), batched.  ring [n, cap, dim] with
+// cap = max_delay + 1, head = next write slot, count = values held (<= cap).
+static __global__ void delay_reset_kernel(int64_t n, int min_delay, int max_delay, uint64_t seed,
+                                          int64_t env0, const uint32_t *episode, uint64_t step,
+                                          int32_t *delay, int32_t *count, int32_t *head) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    PhiloxInts g;
+    g.px.init(seed, (uint64_t)(env0 + i), episode ? episode[i] : 0u, step);
+    delay[i] = (int32_t)g.integers(min_delay, (int64_t)max_delay + 1);  // randomization.py:46
+    count[i] = 0;
+    head[i] = 0;
+}
+
+template <typename T>
+__global__ void delay_push_pop_kernel(int64_t n, int dim, int min_delay, int max_delay,
+                                      int per_step, T *ring, int32_t *head, int32_t *count,
+                                      const int32_t *delay, uint64_t seed, int64_t env0,
+                                      const uint32_t *episode, uint64_t step, const T *value,
+                                      T *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int cap = max_delay + 1;
+    T *rb = ring + i * (int64_t)cap * dim;
+    int h = head[i], c = count[i];
+    for (int k = 0; k < dim; ++k) rb[(int64_t)h * dim + k] = value[i * dim + k];  // append
+    h = h + 1 == cap ? 0 : h + 1;
+    c = c < cap ? c + 1 : cap;  // deque(maxlen=cap) drops the oldest
+    int d = delay[i];
+    if (per_step) {  // randomization.py:50-51
+        PhiloxInts g;
+        g.px.init(seed, (uint64_t)(env0 + i), episode ? episode[i] : 0u, step);
+        d = (int)g.integers(min_delay, (int64_t)max_delay + 1);
+    }
+    int idx = c - 1 - d;
+    if (idx < 0) idx = 0;  // warm-up: oldest available (randomization.py:60-61)
+    int slot = h - c + idx;
+    slot = slot < 0 ? slot + cap : slot;
+    for (int k = 0; k < dim; ++k) out[i * dim + k] = rb[(int64_t)slot * dim + k];
+    head[i] = h;
+    count[i] = c;
 }
 
 // pose_injection (randomization.py:188-199), in place on rows [N, dim]; bounds [dim, 2]
@@ -395,11 +479,24 @@ cudaError_t launch_progress(int64_t n, const T *raw, T *hist, T *reward, cudaStr
 
 template <typename T>
 cudaError_t launch_sensor_noise(int64_t n, int dim, T *obs, int nspec, const int *off,
-                                const int *len, const double *scale, uint64_t seed, int64_t env0,
-                                const uint32_t *episode, uint64_t step, cudaStream_t st) {
+                                const int *len, const double *scale, const int *kind,
+                                uint64_t seed, int64_t env0, const uint32_t *episode,
+                                uint64_t step, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
     sensor_noise_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
-        n, dim, obs, nspec, off, len, scale, seed, env0, episode, step);
+        n, dim, obs, nspec, off, len, scale, kind, seed, env0, episode, step);
+    return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_delay_push_pop(int64_t n, int dim, int min_delay, int max_delay, int per_step,
+                                  T *ring, int32_t *head, int32_t *count, const int32_t *delay,
+                                  uint64_t seed, int64_t env0, const uint32_t *episode,
+                                  uint64_t step, const T *value, T *out, cudaStream_t st) {
+    if (n == 0) return cudaSuccess;
+    delay_push_pop_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        n, dim, min_delay, max_delay, per_step, ring, head, count, delay, seed, env0, episode,
+        step, value, out);
     return cudaGetLastError();
 }
 
@@ -425,9 +522,13 @@ cudaError_t launch_pose_injection(int64_t n, int dim, T *pose, const double *bou
                                              T *, cudaStream_t);                                \
     EXT template cudaError_t launch_progress<T>(int64_t, const T *, T *, T *, cudaStream_t);     \
     EXT template cudaError_t launch_sensor_noise<T>(int64_t, int, T *, int, const int *,         \
-                                                    const int *, const double *, uint64_t,      \
-                                                    int64_t, const uint32_t *, uint64_t,        \
-                                                    cudaStream_t);                              \
+                                                    const int *, const double *, const int *,    \
+                                                    uint64_t, int64_t, const uint32_t *,        \
+                                                    uint64_t, cudaStream_t);                    \
+    EXT template cudaError_t launch_delay_push_pop<T>(int64_t, int, int, int, int, T *, int32_t *,  \
+                                                      int32_t *, const int32_t *, uint64_t,      \
+                                                      int64_t, const uint32_t *, uint64_t,       \
+                                                      const T *, T *, cudaStream_t);             \
     EXT template cudaError_t launch_pose_injection<T>(int64_t, int, T *, const double *, double, \
                                                       uint64_t, int64_t, const uint32_t *,      \
                                                       uint64_t, uint8_t *, cudaStream_t);

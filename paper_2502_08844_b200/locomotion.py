@@ -12,8 +12,9 @@ as CUDA tensors, computed by the sm_100a kernels of libdeskrl_b200.so:
 * ``advance_phase_batch`` -- ``advance_phase`` + ``phase_encode``
   (mathcore.py:143-177).
 * ``progress_clip_reward_batch`` (envkit.py:196-202).
-* ``apply_sensor_noise_batch`` (uniform kind), ``pose_injection_batch``,
-  ``curriculum_update_batch`` (randomization.py:88-108, 188-199, 224-238).
+* ``apply_sensor_noise_batch`` (uniform and gaussian), ``randomize_params_batch``,
+  ``DelayLineBatch``, ``pose_injection_batch``, ``curriculum_update_batch``
+  (randomization.py:27-62, 88-108, 156-181, 188-199, 224-238).
 
 Randomness: the reference takes caller-supplied numpy Generators; here each
 world's stream is ``stream_rng(seed, env_index_offset + world, episode, step)``
@@ -366,11 +367,16 @@ def progress_clip_reward_batch(raw, history_max):
 # B7: domain randomisation primitives
 
 
+_NOISE_KINDS = {"uniform": 0, "gaussian": 1}
+
+
 def apply_sensor_noise_batch(obs: dict, specs, key: NoiseKey):
-    """randomization.apply_sensor_noise for batched slots (uniform kind).
+    """randomization.apply_sensor_noise for batched slots, both kinds.
 
     ``obs``: slot name -> CUDA tensor [n, d]; ``specs``: objects with
-    ``slot``, ``scale``, ``kind`` (NoiseSpec, randomization.py:73-85).
+    ``slot``, ``scale``, ``kind`` (NoiseSpec, randomization.py:73-85): uniform
+    U(-scale, scale) or gaussian Generator.normal(0, scale), drawn in spec order
+    from each world's stream (bit-compatible with NumPy).
     """
     torch = _torch()
     names = list(obs)
@@ -379,8 +385,11 @@ def apply_sensor_noise_batch(obs: dict, specs, key: NoiseKey):
             raise ConfigError("privileged slots must stay noise-free")
         if spec.slot not in obs:
             raise ConfigError(f"unknown observation slot {spec.slot!r}")
-        if getattr(spec, "kind", "uniform") != "uniform":
-            raise ConfigError("gaussian sensor noise is not provided by the B200 backend")
+        kind = getattr(spec, "kind", "uniform")
+        if kind not in _NOISE_KINDS:
+            raise ConfigError(f"unknown noise kind {kind!r}")
+        if spec.scale < 0:
+            raise ConfigError("noise scale must be non-negative")
     first = obs[names[0]]
     n = first.shape[0]
     dt = first.dtype
@@ -392,19 +401,123 @@ def apply_sensor_noise_batch(obs: dict, specs, key: NoiseKey):
         o += t.shape[1]
         flat.append(t)
     buf = torch.cat(flat, 1).contiguous()
-    off = torch.tensor([offs[s.slot][0] for s in specs], dtype=torch.int32, device=first.device)
-    ln = torch.tensor([offs[s.slot][1] for s in specs], dtype=torch.int32, device=first.device)
-    sc = torch.tensor([float(s.scale) for s in specs], dtype=torch.float64, device=first.device)
-    kc, ep = _key(key, n, first.device)
+    dev = first.device
+    off = torch.tensor([offs[s.slot][0] for s in specs], dtype=torch.int32, device=dev)
+    ln = torch.tensor([offs[s.slot][1] for s in specs], dtype=torch.int32, device=dev)
+    sc = torch.tensor([float(s.scale) for s in specs], dtype=torch.float64, device=dev)
+    kd = torch.tensor([_NOISE_KINDS[getattr(s, "kind", "uniform")] for s in specs],
+                      dtype=torch.int32, device=dev)
+    kc, ep = _key(key, n, dev)
     _check(nat.lib().dk_dr_sensor_noise(_dtype_code(buf), n, buf.shape[1], _ptr(buf), len(specs),
-                                        _ptr(off), _ptr(ln), _ptr(sc), ctypes.byref(kc),
-                                        _stream(first.device)))
+                                        _ptr(off), _ptr(ln), _ptr(sc), _ptr(kd),
+                                        ctypes.byref(kc), _stream(dev)))
     out = dict(obs)
     for k in names:
         a, b = offs[k]
         if any(s.slot == k for s in specs):
             out[k] = buf[:, a:a + b].reshape(obs[k].shape)
     return out
+
+
+_DISTRIBUTIONS = {"uniform_additive": 0, "uniform_multiplicative": 1, "log_uniform": 2}
+
+
+def randomize_params_batch(nominal, spec, key: NoiseKey, num_worlds: int, device=None):
+    """randomization.randomize_params for ``num_worlds`` worlds at once.
+
+    ``nominal``: a dataclass of floats (e.g. DynamicsParams); ``spec``: an
+    object with ``params`` = ParamRange-like (path, distribution, low, high).
+    World w draws from stream_rng(seed, env_index_offset + w, episode, step),
+    so row w equals ``randomize_params(nominal, spec, stream_rng(...))``.
+    Returns (params [num_worlds, F] float64 CUDA tensor, field names).
+    """
+    import dataclasses
+
+    torch = _torch()
+    names = [f.name for f in dataclasses.fields(nominal)]
+    ranges = list(getattr(spec, "params", ()))
+    for pr in ranges:
+        if pr.path not in names:
+            raise ConfigError(f"unknown parameter path {pr.path!r}")
+        if pr.distribution not in _DISTRIBUTIONS:
+            raise ConfigError(f"unknown distribution {pr.distribution!r}")
+        if pr.low > pr.high:
+            raise ConfigError(f"bounds out of order for {pr.path!r}")
+        if pr.distribution != "uniform_additive" and pr.low <= 0:
+            raise ConfigError("multiplicative/log bounds must be positive")
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    nom = torch.tensor([float(getattr(nominal, k)) for k in names], dtype=torch.float64,
+                       device=dev)
+    out = torch.empty((num_worlds, len(names)), dtype=torch.float64, device=dev)
+    if not ranges:
+        out.copy_(nom.expand(num_worlds, -1))
+        return out, names
+    lo = [float(np.log(pr.low)) if pr.distribution == "log_uniform" else float(pr.low)
+          for pr in ranges]  # np.log as the reference computes it (randomization.py:175)
+    hi = [float(np.log(pr.high)) if pr.distribution == "log_uniform" else float(pr.high)
+          for pr in ranges]
+    fld = torch.tensor([names.index(pr.path) for pr in ranges], dtype=torch.int32, device=dev)
+    dst = torch.tensor([_DISTRIBUTIONS[pr.distribution] for pr in ranges], dtype=torch.int32,
+                       device=dev)
+    lo_t = torch.tensor(lo, dtype=torch.float64, device=dev)
+    hi_t = torch.tensor(hi, dtype=torch.float64, device=dev)
+    fail = torch.full((1,), -1, dtype=torch.int64, device=dev)
+    kc, ep = _key(key, num_worlds, dev)
+    _check(nat.lib().dk_dr_randomize_params(num_worlds, len(names), _ptr(nom), len(ranges),
+                                            _ptr(fld), _ptr(dst), _ptr(lo_t), _ptr(hi_t),
+                                            ctypes.byref(kc), _ptr(out), _ptr(fail),
+                                            _stream(dev)))
+    f = int(fail.item())
+    if f != -1:
+        raise ConfigError(f"could not draw a physical value for {ranges[f % len(ranges)].path!r}")
+    return out, names
+
+
+class DelayLineBatch:
+    """``num_worlds`` DelayLines (randomization.py:27-62) of ``dim``-vectors on
+    the GPU: a [num_worlds, max_delay + 1, dim] ring per batch.  ``reset(key)``
+    draws each world's episode delay (Generator.integers(min, max + 1) from its
+    stream); ``push_pop(value, key)`` appends and returns the aged values (a
+    fresh per-step delay from ``key`` when ``per_step``)."""
+
+    def __init__(self, num_worlds: int, dim: int, min_delay: int, max_delay: int,
+                 per_step: bool = False, dtype=None, device=None):
+        torch = _torch()
+        if min_delay < 0 or max_delay < min_delay:
+            raise ConfigError("delay bounds must satisfy 0 <= min <= max")
+        self.num_worlds, self.dim = int(num_worlds), int(dim)
+        self.min_delay, self.max_delay, self.per_step = int(min_delay), int(max_delay), per_step
+        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.device = dev
+        self.dtype = dtype or torch.float32
+        self.ring = torch.zeros((self.num_worlds, max_delay + 1, dim), dtype=self.dtype,
+                                device=dev)
+        self.head = torch.zeros(self.num_worlds, dtype=torch.int32, device=dev)
+        self.count = torch.zeros_like(self.head)
+        self.delay = torch.zeros_like(self.head)
+        self._has_delay = False
+
+    def reset(self, key: NoiseKey):
+        kc, ep = _key(key, self.num_worlds, self.device)
+        _check(nat.lib().dk_dr_delay_reset(self.num_worlds, self.min_delay, self.max_delay,
+                                           ctypes.byref(kc), _ptr(self.delay), _ptr(self.count),
+                                           _ptr(self.head), _stream(self.device)))
+        self._has_delay = True
+
+    def push_pop(self, value, key: NoiseKey | None = None):
+        if not self.per_step and not self._has_delay:
+            raise ConfigError("delay line used before reset")
+        if self.per_step and key is None:
+            raise ConfigError("per-step delay lines need a key per push_pop")
+        v = value.to(self.dtype).reshape(self.num_worlds, self.dim).contiguous()
+        out = _torch().empty_like(v)
+        kc, ep = _key(key or NoiseKey(), self.num_worlds, self.device)
+        _check(nat.lib().dk_dr_delay_push_pop(_dtype_code(v), self.num_worlds, self.dim,
+                                              self.min_delay, self.max_delay, int(self.per_step),
+                                              _ptr(self.ring), _ptr(self.head), _ptr(self.count),
+                                              _ptr(self.delay), ctypes.byref(kc), _ptr(v),
+                                              _ptr(out), _stream(self.device)))
+        return out.reshape(value.shape)
 
 
 def pose_injection_batch(pose, prob: float, bounds, key: NoiseKey):
@@ -434,9 +547,9 @@ def curriculum_update_batch(state, success, max_level: int = 10, promotion_thres
 
 
 __all__ = [
-    "NoiseKey", "ObservationNoise", "PDParams", "RewardBreakdownBatch", "RewardTermConfig",
-    "TERM_NAMES", "advance_phase_batch", "apply_sensor_noise_batch",
+    "DelayLineBatch", "NoiseKey", "ObservationNoise", "PDParams", "RewardBreakdownBatch",
+    "RewardTermConfig", "TERM_NAMES", "advance_phase_batch", "apply_sensor_noise_batch",
     "build_locomotion_observation_batch", "curriculum_update_batch", "frames_from_reference",
     "locomotion_tail", "pd_batch", "pose_injection_batch", "progress_clip_reward_batch",
-    "total_reward_batch",
+    "randomize_params_batch", "total_reward_batch",
 ]

@@ -17,6 +17,7 @@ gaitgen default shape (8 joints, 2 feet).
 
 from __future__ import annotations
 
+import dataclasses
 import math
 import os
 import sys
@@ -193,6 +194,59 @@ def main():
     inj = np.array([randomization.pose_injection(pose[i], envkit.stream_rng(9, i, 3, 0), 0.4,
                                                  bounds) for i in range(64)])
     data["dr/pose_in"], data["dr/pose_bounds"], data["dr/pose_out"] = pose, bounds, inj
+
+    # gaussian + uniform sensor noise (randomization.py:103-106, Generator.normal)
+    obs_g = rng.normal(0, 1, (48, 10))
+    specs_g = (randomization.NoiseSpec("a", 0.2, "gaussian"), randomization.NoiseSpec("b", 0.05),
+               randomization.NoiseSpec("c", 1.5, "gaussian"))
+    noised = []
+    for i in range(48):
+        d = {"a": obs_g[i, :4], "b": obs_g[i, 4:6], "c": obs_g[i, 6:]}
+        o = randomization.apply_sensor_noise(d, specs_g, envkit.stream_rng(6, 100 + i, 1, 7))
+        noised.append(np.concatenate([o["a"], o["b"], o["c"]]))
+    data["dr/gnoise_in"], data["dr/gnoise_out"] = obs_g, np.array(noised)
+
+    # known answers of one stream: Generator.standard_normal / integers
+    data["dr/normal_known"] = envkit.stream_rng(0, 0, 0, 0).standard_normal(4096)
+    g = envkit.stream_rng(0, 0, 0, 0)
+    data["dr/int_known"] = np.array([int(g.integers(1, 4)) for _ in range(64)])
+
+    # randomize_params on DynamicsParams (randomization.py:156-181): additive with
+    # resampling (pole_mass 0.1 + U(-0.3, 0.2) is often non-positive), multiplicative,
+    # log-uniform, and an additive range on a zero field (link_damping: no check)
+    from deskrl import dynamics
+    nominal = dynamics.DynamicsParams()
+    pnames = [f.name for f in dataclasses.fields(nominal)]
+    ranges = (randomization.ParamRange("pole_mass", "uniform_additive", -0.3, 0.2),
+              randomization.ParamRange("cart_mass", "uniform_multiplicative", 0.5, 1.5),
+              randomization.ParamRange("pend_damping", "log_uniform", 0.1, 10.0),
+              randomization.ParamRange("link_damping", "uniform_additive", -0.1, 0.1),
+              randomization.ParamRange("gravity", "uniform_additive", -0.5, 0.5))
+    spec = randomization.RandomizationSpec(params=ranges)
+    rp = []
+    for i in range(64):
+        pp = randomization.randomize_params(nominal, spec, envkit.stream_rng(21, i, 4, 0))
+        rp.append([getattr(pp, k) for k in pnames])
+    data["dr/params_nominal"] = np.array([getattr(nominal, k) for k in pnames])
+    data["dr/params_fields"] = np.array(pnames)
+    data["dr/params_ranges"] = np.array([[pnames.index(r.path), ("uniform_additive",
+                                          "uniform_multiplicative", "log_uniform").index(
+                                              r.distribution), r.low, r.high] for r in ranges])
+    data["dr/params_out"] = np.array(rp)
+
+    # DelayLine: per-episode (1..3) and per-step (0..5) delays over 24 pushes
+    vals = rng.normal(0, 1, (24, 16, 3))
+    for mode, (lo, hi, per_step) in (("ep", (1, 3, False)), ("st", (0, 5, True))):
+        lines = [randomization.DelayLine(lo, hi, per_step) for _ in range(16)]
+        for i, ln in enumerate(lines):
+            ln.reset(envkit.stream_rng(31, i, 2, 0))
+        outs = []
+        for t in range(24):
+            outs.append([np.asarray(ln.push_pop(vals[t, i], envkit.stream_rng(32, i, 2, t)))
+                         for i, ln in enumerate(lines)])
+        data[f"dr/delay_{mode}_out"] = np.array(outs)
+        data[f"dr/delay_{mode}_delay"] = np.array([ln._episode_delay for ln in lines])
+    data["dr/delay_in"] = vals
 
     # curriculum: a success sequence per learner
     seq = rng.uniform(size=(16, 40)) < 0.6

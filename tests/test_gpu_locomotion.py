@@ -177,3 +177,93 @@ def test_dr_primitives(loco, L):
         st = L.curriculum_update_batch(st, seq[:, k], max_level=5, promotion_threshold=2)
         hist.append(st)
     np.testing.assert_array_equal(torch.stack(hist, 1).cpu().numpy(), loco["dr/curr_out"])
+
+
+class _Spec:
+    def __init__(self, slot, scale, kind="uniform"):
+        self.slot, self.scale, self.kind = slot, scale, kind
+
+
+def test_gaussian_sensor_noise(loco, L):
+    # Generator.normal through NumPy's ziggurat on the GPU: bit-exact in f64
+    x = torch.as_tensor(loco["dr/gnoise_in"], device="cuda")
+    obs = {"a": x[:, :4], "b": x[:, 4:6], "c": x[:, 6:]}
+    specs = [_Spec("a", 0.2, "gaussian"), _Spec("b", 0.05), _Spec("c", 1.5, "gaussian")]
+    out = L.apply_sensor_noise_batch(obs, specs, L.NoiseKey(6, 100, torch.full((48,), 1,
+                                                                            device="cuda"), 7))
+    got = torch.cat([out["a"], out["b"], out["c"]], 1).cpu().numpy()
+    np.testing.assert_array_equal(got, loco["dr/gnoise_out"])
+    # f32 rows: the same draws, added in f64 and rounded once
+    o32 = L.apply_sensor_noise_batch({k: v.float() for k, v in obs.items()}, specs,
+                                     L.NoiseKey(6, 100, torch.full((48,), 1, device="cuda"), 7))
+    g32 = torch.cat([o32["a"], o32["b"], o32["c"]], 1).double().cpu().numpy()
+    assert np.max(np.abs(g32 - loco["dr/gnoise_out"]) / np.maximum(np.abs(loco["dr/gnoise_out"]),
+                                                                   0.1)) < 1e-6
+    with pytest.raises(L.ConfigError):
+        L.apply_sensor_noise_batch(obs, [_Spec("a", 0.1, "laplace")], L.NoiseKey())
+
+
+def test_gaussian_noise_many_streams_vs_oracle(L):
+    # 65536 worlds x 32 gaussian draws (wedge and tail paths hit ~2000 times)
+    from oracle import locomotion as orc
+
+    n, d = 65536, 32
+    x = torch.zeros((n, d), dtype=torch.float64, device="cuda")
+    out = L.apply_sensor_noise_batch({"s": x}, [_Spec("s", 1.0, "gaussian")],
+                                     L.NoiseKey(1234, 7, None, 3))["s"].cpu().numpy()
+    ref = orc.sensor_noise(np.zeros((n, d)), [(0, d, 1.0, "gaussian")], key=(1234, 7, 0, 3))
+    # identical draw sequence; the tail's log1p (CUDA vs glibc) may differ by an
+    # ulp (measured: 4 of 2M values, 1 ulp), every other path is bit-exact
+    np.testing.assert_allclose(out, ref, rtol=1e-15, atol=0)
+    assert np.count_nonzero(out != ref) <= 64
+
+
+def test_randomize_params(loco, L):
+    import dataclasses
+
+    names = [str(s) for s in loco["dr/params_fields"]]
+
+    @dataclasses.dataclass
+    class Nominal:
+        pass
+
+    Nom = dataclasses.make_dataclass("Nom", [(k, float) for k in names])
+    nominal = Nom(*[float(v) for v in loco["dr/params_nominal"]])
+
+    class PR:
+        def __init__(self, path, dist, lo, hi):
+            self.path, self.distribution, self.low, self.high = path, dist, lo, hi
+
+    dists = ("uniform_additive", "uniform_multiplicative", "log_uniform")
+    spec = type("Spec", (), {"params": tuple(PR(names[int(r[0])], dists[int(r[1])], r[2], r[3])
+                                             for r in loco["dr/params_ranges"])})()
+    out, fields = L.randomize_params_batch(nominal, spec, L.NoiseKey(21, 0, torch.full(
+        (64,), 4, device="cuda"), 0), 64)
+    assert fields == names
+    # NumPy's SIMD exp vs CUDA exp on the log-uniform field: a few ulps
+    np.testing.assert_allclose(out.cpu().numpy(), loco["dr/params_out"], rtol=1e-14, atol=0)
+    bad = type("Spec", (), {"params": (PR("pend_mass", "uniform_additive", -9, -5),)})()
+    with pytest.raises(L.ConfigError, match="pend_mass"):
+        L.randomize_params_batch(nominal, bad, L.NoiseKey(21, 0, None, 0), 8)
+    with pytest.raises(L.ConfigError):
+        L.randomize_params_batch(nominal, type("S", (), {"params": (PR("nope", dists[0], 0, 1),)})(),
+                                 L.NoiseKey(), 4)
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_delay_lines(loco, L, dtype):
+    tdt = getattr(torch, dtype)
+    vals = torch.as_tensor(loco["dr/delay_in"], device="cuda", dtype=tdt)  # [24, 16, 3]
+    for mode, (lo, hi, per_step) in (("ep", (1, 3, False)), ("st", (0, 5, True))):
+        dl = L.DelayLineBatch(16, 3, lo, hi, per_step, dtype=tdt)
+        ep = torch.full((16,), 2, device="cuda")
+        dl.reset(L.NoiseKey(31, 0, ep, 0))
+        np.testing.assert_array_equal(dl.delay.cpu().numpy(), loco[f"dr/delay_{mode}_delay"])
+        outs = torch.stack([dl.push_pop(vals[t], L.NoiseKey(32, 0, ep, t))
+                            for t in range(vals.shape[0])])
+        np.testing.assert_array_equal(outs.double().cpu().numpy(),
+                                      loco[f"dr/delay_{mode}_out"].astype(dtype).astype(np.float64))
+    with pytest.raises(L.ConfigError):
+        L.DelayLineBatch(4, 1, 3, 2)
+    with pytest.raises(L.ConfigError):
+        L.DelayLineBatch(4, 1, 0, 2).push_pop(torch.zeros(4, 1, device="cuda"))

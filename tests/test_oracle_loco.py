@@ -103,6 +103,44 @@ def test_sensor_noise_and_pose_injection(loco, orc):
     np.testing.assert_array_equal(inj, loco["dr/pose_out"])
 
 
+def test_gaussian_sensor_noise(loco, orc):
+    # Generator.normal through NumPy's ziggurat: bit-exact
+    specs = [(0, 4, 0.2, "gaussian"), (4, 2, 0.05, "uniform"), (6, 4, 1.5, "gaussian")]
+    out = orc.sensor_noise(loco["dr/gnoise_in"], specs, key=(6, 100, 1, 7))
+    np.testing.assert_array_equal(out, loco["dr/gnoise_out"])
+
+
+def test_stream_normal_and_integers_known_answers(loco, orc):
+    # Generator.standard_normal (4096 draws: ~15 take the wedge / tail paths) and
+    # Generator.integers (32-bit Lemire with the half-word buffer), bit-exact
+    np.testing.assert_array_equal(orc.stream_normal((0, 0, 0, 0), 4096), loco["dr/normal_known"])
+    got = orc.stream_integers((0, 0, 0, 0), 1, 4, 64)
+    np.testing.assert_array_equal(got, loco["dr/int_known"][:64])
+
+
+def test_randomize_params(loco, orc):
+    ranges = [(int(r[0]), ("uniform_additive", "uniform_multiplicative", "log_uniform")[int(r[1])],
+               r[2], r[3]) for r in loco["dr/params_ranges"]]
+    out, fail = orc.randomize_params(loco["dr/params_nominal"], ranges, 64, key=(21, 0, 4, 0))
+    assert fail == -1
+    # NumPy's exp/log ufuncs (SIMD) vs glibc: a few ulps on the log-uniform field
+    np.testing.assert_allclose(out, loco["dr/params_out"], rtol=1e-14, atol=0)
+    # a field that can never be drawn positive -> the first world fails (ConfigError)
+    _, fail = orc.randomize_params(loco["dr/params_nominal"], [(2, "uniform_additive", -9, -5)],
+                                   8, key=(21, 0, 4, 0))
+    assert fail == 0
+
+
+def test_delay_lines(loco, orc):
+    vals = loco["dr/delay_in"]
+    for mode, (lo, hi, per_step) in (("ep", (1, 3, False)), ("st", (0, 5, True))):
+        dl = orc.DelayLines(16, 3, lo, hi, per_step)
+        dl.reset((31, 0, 2, 0))
+        np.testing.assert_array_equal(dl.delay, loco[f"dr/delay_{mode}_delay"])
+        outs = np.stack([dl.push_pop(vals[t], (32, 0, 2, t)) for t in range(vals.shape[0])])
+        np.testing.assert_array_equal(outs, loco[f"dr/delay_{mode}_out"])
+
+
 def test_curriculum(loco, orc):
     seq = loco["dr/curr_seq"]
     st = np.zeros((seq.shape[0], 4), dtype=np.int64)
