@@ -230,7 +230,11 @@ struct RolloutShape {
     static constexpr int A = Task::A, O = Task::O, I = Task::I;
     static constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));  // reals per world
     static constexpr int WPC = 32 * TL;                                      // worlds per CTA
-    static constexpr int G = WF * (int)sizeof(T) <= 24 ? 8 : 4;            // steps per group
+    // steps per group: as many as keep two CTAs per SM (<= 113 KB of smem);
+    // each group boundary costs the serial chain ~300 cycles (16 steps per group
+    // measured 8% faster than 8 for cartpole f32)
+    static constexpr int WB = WF * (int)sizeof(T);                           // bytes per world-step
+    static constexpr int G = WB <= 24 ? 16 : WB <= 48 ? 8 : 4;
     static constexpr int M = 4;                                              // consumer warps
     static constexpr int NG = M + 2;                                         // state ring (groups)
     static constexpr int NA = 4;                                             // action ring (groups)
@@ -250,6 +254,7 @@ struct RolloutShape {
     static constexpr size_t OFF_GFLAG = OFF_FLAGS + (size_t)NG * G * WPC;  // [NG] u8: fast group
     static constexpr size_t OFF_CTRL = (OFF_GFLAG + NG + 15) / 16 * 16;
     static constexpr size_t SMEM = OFF_CTRL + 16;
+    static_assert(SMEM <= 113 * 1024, "rollout CTA must leave room for a second CTA per SM");
 };
 
 // One world's registers <-> its column of a [field][worlds] ring slot.
