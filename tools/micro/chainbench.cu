@@ -47,6 +47,29 @@ __global__ void group_body(float *out, long long *cyc, int steps, Params<float> 
     if (lane == 0) cyc[0] = t1 - t0;
 }
 
+// two independent worlds per lane (the TL = 2 producer): does the second chain
+// fill the first one's latency?
+__global__ void chain2(float *out, long long *cyc, int steps, Params<float> p) {
+    Cartpole<float>::W w[2];
+    for (int t = 0; t < 2; ++t) {
+        w[t].x = 0.1f * threadIdx.x / 32.f + t; w[t].th = 0.05f + 0.1f * t; w[t].xd = 0.f;
+        w[t].thd = 0.01f;
+        Cartpole<float>::refresh(w[t]);
+    }
+    float acc = 0.f;
+    long long t0 = clock64();
+    for (int k = 0; k < steps; ++k) {
+        float u[1] = {(k & 1) ? 3.f : -3.f};
+#pragma unroll
+        for (int t = 0; t < 2; ++t) Cartpole<float>::step_u(w[t], u, p);
+        acc += w[0].x + w[1].x;
+    }
+    asm volatile("mov.f32 %0, %0;" : "+f"(acc) :: "memory");
+    long long t1 = clock64();
+    out[threadIdx.x] = acc + w[0].th + w[1].th;
+    if (threadIdx.x == 0) cyc[0] = t1 - t0;
+}
+
 template <int V>
 __global__ void chain(float *out, long long *cyc, int steps, Params<float> p) {
     Cartpole<float>::W w;
@@ -106,5 +129,12 @@ int main() {
         cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
         printf("%-24s %.1f cycles/step\n", names[v], (double)c / steps);
     }
+    for (int rep = 0; rep < 2; ++rep) {
+        chain2<<<1, 32>>>(out, cyc, steps, p);
+        cudaDeviceSynchronize();
+    }
+    long long c;
+    cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
+    printf("%-24s %.1f cycles/step (both worlds)\n", "two chains per lane", (double)c / steps);
     return 0;
 }
