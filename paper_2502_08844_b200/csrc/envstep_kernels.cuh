@@ -658,9 +658,15 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             for (int d = 0; d < NG; ++d) mbar_arrive_u32(empty_b + 8 * d);  // slots start free
         }
         // FULL: all 32 rows of the tile exist -> no per-element bounds checks
-        auto run_tile = [&](auto full_c, int t, int g, const T *ring_g, const T *rp_g,
-                            const uint8_t *fl_g, bool fast) {
+        // FAST (no world of the group truncates, no reset): no flag loads, no
+        // terminal-observation branch, the three flag bytes are constant zeros
+        // per-step strides, hoisted (the compiler otherwise re-derives the
+        // 64-bit products from the constant bank every step)
+        const int64_t step_obs = n * O, step_info = n * I;
+        auto run_tile = [&](auto full_c, auto fast_c, int t, int g, const T *ring_g,
+                            const T *rp_g, const uint8_t *fl_g) {
             constexpr bool FULL = decltype(full_c)::value;
+            constexpr bool FAST = decltype(fast_c)::value;
             const int col = t * 32 + lane;
             const int64_t row0 = cta0 + t * 32;
             const int64_t i = row0 + lane;
@@ -676,14 +682,14 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             for (int s = 0; s < kend; ++s) {
                 typename Task::W wd;
                 slot_to_world<Task, T, WPC>(wd, ring_g + s * WF * WPC, col);
-                const uint8_t fl = fast ? 0 : fl_g[s * WPC + col];
-                const bool reset = (fl & 2) != 0;
+                const uint8_t fl = FAST ? 0 : fl_g[s * WPC + col];
+                const bool reset = !FAST && (fl & 2) != 0;
                 T info[I];
                 const T r = R1 ? (T(0) + Task::reward(wd, p, info))
                                : (rp_g[s * WPC + col] + Task::reward(wd, p, info)) / inv_rep;
                 T o[O];
                 Task::obs(wd, p, o);
-                if (__builtin_expect(reset, 0) && out.term_obs) {
+                if (!FAST && __builtin_expect(reset, 0) && out.term_obs) {
                     T *tt = out.term_obs + (kb + (int64_t)s * n + i) * O;
 #pragma unroll
                     for (int j = 0; j < O; ++j) tt[j] = o[j];
@@ -707,11 +713,11 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
                 if (FULL || in_range) {
                     *rew_p = r;
                     *done_p = 0;
-                    *trunc_p = fl & 1;
-                    if (has_mask) *mask_p = reset ? 1 : 0;
+                    *trunc_p = FAST ? 0 : fl & 1;
+                    if (has_mask) *mask_p = FAST ? 0 : (reset ? 1 : 0);
                 }
-                obs_p += n * O;
-                info_p += n * I;
+                obs_p += step_obs;
+                info_p += step_info;
                 rew_p += n;
                 done_p += n;
                 trunc_p += n;
@@ -729,10 +735,17 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
 #ifndef DK_EXP_NO_CONSUMER
 #pragma unroll
             for (int t = 0; t < TL; ++t) {
-                if (cta0 + t * 32 + 32 <= n)
-                    run_tile(std::true_type{}, t, g, ring_g, rp_g, fl_g, fast);
-                else if (cta0 + t * 32 < n)
-                    run_tile(std::false_type{}, t, g, ring_g, rp_g, fl_g, fast);
+                if (cta0 + t * 32 + 32 <= n) {
+                    if (fast)
+                        run_tile(std::true_type{}, std::true_type{}, t, g, ring_g, rp_g, fl_g);
+                    else
+                        run_tile(std::true_type{}, std::false_type{}, t, g, ring_g, rp_g, fl_g);
+                } else if (cta0 + t * 32 < n) {  // (fast groups write no flags)
+                    if (fast)
+                        run_tile(std::false_type{}, std::true_type{}, t, g, ring_g, rp_g, fl_g);
+                    else
+                        run_tile(std::false_type{}, std::false_type{}, t, g, ring_g, rp_g, fl_g);
+                }
             }
 #endif
             mbar_arrive_u32(empty_b + 8 * sb);
