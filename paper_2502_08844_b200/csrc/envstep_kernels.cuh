@@ -257,13 +257,16 @@ struct RolloutShape {
     static_assert(SMEM <= 113 * 1024, "rollout CTA must leave room for a second CTA per SM");
 };
 
-// One world's registers <-> its column of a [field][worlds] ring slot.
+// One world's registers <-> its column of a [field][worlds] ring slot.  Only
+// the fields the consumers read (Task::SLOT_FIELDS: reward + observation) are
+// passed; e.g. cartpole's raw angle is not (obs and reward use its sin/cos).
 template <class Task, typename T, int STRIDE>
 __device__ __forceinline__ void world_to_slot(const typename Task::W &w, T *slot, int col) {
     constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));
     const T *f = reinterpret_cast<const T *>(&w);
 #pragma unroll
-    for (int j = 0; j < WF; ++j) slot[j * STRIDE + col] = f[j];
+    for (int j = 0; j < WF; ++j)
+        if ((Task::SLOT_FIELDS >> j) & 1u) slot[j * STRIDE + col] = f[j];
 }
 
 template <class Task, typename T, int STRIDE>
@@ -271,7 +274,7 @@ __device__ __forceinline__ void slot_to_world(typename Task::W &w, const T *slot
     constexpr int WF = (int)(sizeof(typename Task::W) / sizeof(T));
     T *f = reinterpret_cast<T *>(&w);
 #pragma unroll
-    for (int j = 0; j < WF; ++j) f[j] = slot[j * STRIDE + col];
+    for (int j = 0; j < WF; ++j) f[j] = ((Task::SLOT_FIELDS >> j) & 1u) ? slot[j * STRIDE + col] : T(0);
 }
 
 // Environment.reset (envkit.py:502-519) of one world inside a rollout: the

@@ -41,6 +41,7 @@ template <typename T>
 struct Pendulum {
     static constexpr int A = 1, O = 3, I = 1, NS = 2;
     struct W { T th, om, s, c; };
+    static constexpr unsigned SLOT_FIELDS = 0xEu;  // om, s, c (reward / obs never read th)
 
     static __device__ __forceinline__ void load(W &w, const T *soa, int64_t i, int64_t n) {
         w.th = soa[i]; w.om = soa[n + i];
@@ -100,6 +101,7 @@ template <typename T>
 struct Cartpole {
     static constexpr int A = 1, O = 5, I = 3, NS = 4;
     struct W { T x, th, xd, thd, s, c; };
+    static constexpr unsigned SLOT_FIELDS = 0x3Du;  // all but th (reward / obs use s, c)
 
     static __device__ __forceinline__ void load(W &w, const T *soa, int64_t i, int64_t n) {
         w.x = soa[i]; w.th = soa[n + i]; w.xd = soa[2 * n + i]; w.thd = soa[3 * n + i];
@@ -224,6 +226,7 @@ __device__ __forceinline__ void twolink_advance(TwoLinkW<T> &w, T tau1, T tau2, 
 template <typename T>
 struct Acrobot {
     static constexpr int A = 1, O = 6, I = 1, NS = 4;
+    static constexpr unsigned SLOT_FIELDS = ~0u;
     using W = TwoLinkW<T>;
 
     static __device__ __forceinline__ void load(W &w, const T *soa, int64_t i, int64_t n) {
@@ -274,6 +277,7 @@ struct Acrobot {
 template <typename T>
 struct Reacher {
     static constexpr int A = 2, O = 10, I = 1, NS = 6;
+    static constexpr unsigned SLOT_FIELDS = ~0u;
     using W = TwoLinkW<T>;
 
     static __device__ __forceinline__ void load(W &w, const T *soa, int64_t i, int64_t n) {
