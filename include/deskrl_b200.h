@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DK_ABI_VERSION 2  /* 2: sensor-noise kinds, randomize_params, delay lines */
+#define DK_ABI_VERSION 3  /* 2: sensor-noise kinds, randomize_params, delay lines; 3: PPO math */
 
 /* Status codes.  The Python host maps them to the reference's exception
  * classes: ConfigError (randomization.py:19), InvalidInputError
@@ -277,6 +277,28 @@ int dk_dr_pose_injection(int dtype, int64_t n, int dim, void *pose, const double
  * (level, successes_at_level, episodes, total_successes). */
 int dk_dr_curriculum(int64_t n, int64_t *state, const uint8_t *success, int64_t max_level,
                      int64_t promotion_threshold, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Rollout-side PPO math, device pointers, float64
+ * arithmetic whatever the storage dtype (the reference converts to float64).
+ *
+ * compute_gae (ppo.py:80-102): rewards / values / dones [T, N], bootstrap [N]
+ * -> advantages, returns (= advantages + values) [T, N]. */
+int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
+               const void *values, const void *dones, const void *bootstrap, double gamma,
+               double lam, void *advantages, void *returns, void *stream);
+
+/* normalizer_update (mathcore.py:234-251): merges batch [rows, dim] into the
+ * running statistics mean / var (device float64 [dim], updated in place);
+ * count is the statistics' count before the update (the caller adds rows). */
+int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double count,
+                   double *mean, double *var, void *stream);
+
+/* normalizer_apply (mathcore.py:254-265) or, with invert, normalizer_invert
+ * (268-272) of batch [rows, dim] into out (same dtype); count == 0 copies. */
+int dk_norm_apply(int dtype, int64_t rows, int dim, const void *batch, double count,
+                  const double *mean, const double *var, double epsilon, int invert, void *out,
+                  void *stream);
 
 int dk_abi_version(void);
 const char *dk_last_error(void);

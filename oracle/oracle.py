@@ -61,7 +61,7 @@ class _Cfg(ctypes.Structure):
 
 
 def build(force: bool = False) -> str:
-    srcs = [os.path.join(_HERE, f) for f in ("oracle.c", "locomotion.c", "Makefile")] + [
+    srcs = [os.path.join(_HERE, f) for f in ("oracle.c", "locomotion.c", "ppo.c", "Makefile")] + [
         os.path.join(os.path.dirname(_HERE), "paper_2502_08844_b200", "csrc", "ziggurat_tables.h")]
     if force or not os.path.exists(_LIB_PATH) or (
         os.path.getmtime(_LIB_PATH) < max(os.path.getmtime(f) for f in srcs)

@@ -122,6 +122,12 @@ _SIGS = {
                                             ctypes.c_double, ctypes.POINTER(NoiseKeyC), _vp,
                                             _vp]),
     "dk_dr_curriculum": (ctypes.c_int, [_i64, _vp, _vp, _i64, _i64, _vp]),
+    "dk_ppo_gae": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_double,
+                                  ctypes.c_double, _vp, _vp, _vp]),
+    "dk_norm_update": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,
+                                      _vp, _vp, _vp]),
+    "dk_norm_apply": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,
+                                     _vp, _vp, ctypes.c_double, ctypes.c_int, _vp, _vp]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

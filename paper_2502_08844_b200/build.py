@@ -36,6 +36,7 @@ UNITS = {
     "locomotion_f64.cu": ["--fmad=false"],
     "capi.cu": [],
     "capi_loco.cu": [],
+    "capi_ppo.cu": ["--fmad=false"],
 }
 
 

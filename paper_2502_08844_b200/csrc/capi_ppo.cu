@@ -1,0 +1,113 @@
+// capi_ppo.cu -- extern "C" entry points of the rollout-side PPO math
+// (include/deskrl_b200.h): GAE and the running
+// observation normaliser.
+#include <cstdio>
+
+#include "../../include/deskrl_b200.h"
+#include "ppo_kernels.cuh"
+
+extern "C" int dk_internal_fail(int code, const char *msg);  // capi.cu
+
+namespace {
+
+int cuda_rc(cudaError_t e, const char *what) {
+    if (e == cudaSuccess) return DK_OK;
+    char buf[256];
+    snprintf(buf, sizeof(buf), "%s: %s", what, cudaGetErrorString(e));
+    return dk_internal_fail(DK_ERR_CUDA, buf);
+}
+
+unsigned blocks(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
+
+// rows are spread over `lanes` strided accumulators per column: enough threads
+// to fill the GPU, each still summing >= 16 rows
+int64_t pick_lanes(int64_t rows, int dim) {
+    int64_t lanes = (148 * 2048 + dim - 1) / dim;
+    const int64_t cap = (rows + 15) / 16;
+    if (lanes > cap) lanes = cap;
+    return lanes < 1 ? 1 : lanes;
+}
+
+template <typename T>
+int norm_update(int64_t rows, int dim, const T *batch, double count, double *mean, double *var,
+                cudaStream_t st) {
+    const int64_t lanes = pick_lanes(rows, dim);
+    double *partial = nullptr, *bstat = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&partial, sizeof(double) * lanes * dim, st);
+    if (e == cudaSuccess) e = cudaMallocAsync((void **)&bstat, sizeof(double) * 2 * dim, st);
+    if (e != cudaSuccess) return cuda_rc(e, "normalizer workspace");
+    double *b_mean = bstat, *b_var = bstat + dim;
+    const int64_t P = lanes * dim;
+    dk::colsum_kernel<T><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes, batch, nullptr, partial);
+    dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, rows, partial, b_mean);
+    dk::colsum_kernel<T><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes, batch, b_mean, partial);
+    dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, rows, partial, b_var);
+    dk::norm_merge_kernel<<<blocks(dim, 128), 128, 0, st>>>(dim, count, (double)rows, b_mean,
+                                                           b_var, mean, var);
+    e = cudaGetLastError();
+    cudaFreeAsync(partial, st);
+    cudaFreeAsync(bstat, st);
+    return cuda_rc(e, "normalizer update launch");
+}
+
+}  // namespace
+
+extern "C" {
+
+int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
+               const void *values, const void *dones, const void *bootstrap, double gamma,
+               double lam, void *advantages, void *returns, void *stream) {
+    if (!rewards || !values || !dones || !bootstrap || !advantages || !returns)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "compute_gae: missing argument");
+    if (num_steps < 0 || num_worlds < 0)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "compute_gae: mismatched shapes");
+    if (num_steps == 0 || num_worlds == 0) return DK_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const unsigned g = blocks(num_worlds, 128);
+    if (dtype == DK_F64)
+        dk::gae_kernel<double><<<g, 128, 0, st>>>(
+            num_steps, num_worlds, (const double *)rewards, (const double *)values,
+            (const double *)dones, (const double *)bootstrap, gamma, lam, (double *)advantages,
+            (double *)returns);
+    else
+        dk::gae_kernel<float><<<g, 128, 0, st>>>(
+            num_steps, num_worlds, (const float *)rewards, (const float *)values,
+            (const float *)dones, (const float *)bootstrap, gamma, lam, (float *)advantages,
+            (float *)returns);
+    return cuda_rc(cudaGetLastError(), "gae launch");
+}
+
+int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double count,
+                   double *mean, double *var, void *stream) {
+    if (!batch || !mean || !var)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer_update: missing argument");
+    if (dim <= 0 || rows < 0)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer dim mismatch");
+    if (rows == 0) return DK_OK;  // (NumPy: mean of an empty batch is NaN; callers pass rows)
+    cudaStream_t st = (cudaStream_t)stream;
+    if (dtype == DK_F64)
+        return norm_update<double>(rows, dim, (const double *)batch, count, mean, var, st);
+    return norm_update<float>(rows, dim, (const float *)batch, count, mean, var, st);
+}
+
+int dk_norm_apply(int dtype, int64_t rows, int dim, const void *batch, double count,
+                  const double *mean, const double *var, double epsilon, int invert, void *out,
+                  void *stream) {
+    if (!batch || !mean || !var || !out)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer_apply: missing argument");
+    if (dim <= 0 || rows < 0)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer dim mismatch");
+    const int64_t total = rows * dim;
+    if (total == 0) return DK_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int copy = count == 0.0 ? 1 : 0;
+    if (dtype == DK_F64)
+        dk::norm_apply_kernel<double><<<blocks(total, 256), 256, 0, st>>>(
+            total, dim, (const double *)batch, mean, var, epsilon, copy, invert, (double *)out);
+    else
+        dk::norm_apply_kernel<float><<<blocks(total, 256), 256, 0, st>>>(
+            total, dim, (const float *)batch, mean, var, epsilon, copy, invert, (float *)out);
+    return cuda_rc(cudaGetLastError(), "normalizer apply launch");
+}
+
+}  // extern "C"
