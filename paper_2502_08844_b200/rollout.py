@@ -1,0 +1,187 @@
+"""On-device PPO rollout collection (ppo.py:295-378).
+
+``collect_rollout_device`` is ``ppo.collect_rollout`` with every tensor kept on
+the GPU: the policy and value networks (the reference's own ``torch.nn``
+modules, moved to CUDA; their GEMMs are cuBLAS), the env step
+(``DeviceBatchEnv.step``, one ``rollout_kernel`` launch per control step), the
+running observation normalisers (``DeviceRunningNormalizer``), the truncation
+bootstrap through the terminal observation, and the reward scaling.  No
+per-step host synchronisation: the terminal-value bootstrap is evaluated for
+all worlds every step and masked (the reference evaluates the truncated rows
+only after a host-side ``trunc.any()``).
+
+Semantics follow the reference line by line (ppo.py:308-378): observations are
+normalised with the pre-phase statistics and stored as the networks saw them;
+the raw observations are folded into the normalisers only after the phase;
+``rewards = reward * reward_scaling + discounting * terminal_value``;
+``dones = done | trunc``.  Sampling noise: ``noise`` [T, N, A] (e.g. the
+reference's CPU ``torch.randn`` draws, for parity tests) or a CUDA generator.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+from .envkit import ConfigError
+
+
+@dataclass
+class DeviceRolloutBatch:
+    """ppo.RolloutBatch (ppo.py:245-256) with CUDA tensors [T, N, ...]."""
+
+    policy_obs: object
+    value_obs: object
+    actions: object
+    pre_tanh: object
+    log_probs: object
+    rewards: object
+    dones: object
+    values: object
+    bootstrap: object
+
+
+_LOG_2 = 0.6931471805599453
+
+
+def _mlp(sizes, out_dim):
+    import torch.nn as nn
+
+    layers = []
+    for a, b in zip(sizes[:-1], sizes[1:]):
+        layers += [nn.Linear(a, b), nn.SiLU()]
+    layers.append(nn.Linear(sizes[-1], out_dim))
+    return nn.Sequential(*layers)
+
+
+def make_policy(obs_dim: int, action_dim: int, hidden=(128, 128, 128, 128),
+                init_std: float = 0.5):
+    """ppo.MLPPolicy (ppo.py:121-133): Linear/Swish trunk + a free log_std;
+    forward(obs) -> (mean, log_std).  Same parameter names, so the reference's
+    state_dict loads unchanged."""
+    import math
+
+    import torch
+    import torch.nn as nn
+
+    class MLPPolicy(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.trunk = _mlp((obs_dim, *hidden), action_dim)
+            self.log_std = nn.Parameter(torch.full((action_dim,), math.log(init_std)))
+            self.action_dim = action_dim
+
+        def forward(self, obs):
+            mean = self.trunk(obs)
+            return mean, self.log_std.expand_as(mean)
+
+    return MLPPolicy()
+
+
+def make_value(obs_dim: int, hidden=(256, 256, 256, 256, 256)):
+    """ppo.MLPValue (ppo.py:136-142): forward(obs) -> [N] values."""
+    import torch.nn as nn
+
+    class MLPValue(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.trunk = _mlp((obs_dim, *hidden), 1)
+
+        def forward(self, obs):
+            return self.trunk(obs).squeeze(-1)
+
+    return MLPValue()
+
+
+def tanh_gaussian_log_prob(mean, log_std, pre_tanh):
+    """ppo.tanh_gaussian_log_prob (the same torch expression, on device)."""
+    import math
+
+    import torch
+
+    std = torch.exp(log_std)
+    base = -0.5 * (((pre_tanh - mean) / std) ** 2) - log_std - 0.5 * math.log(2 * math.pi)
+    correction = 2.0 * (_LOG_2 - pre_tanh - torch.nn.functional.softplus(-2.0 * pre_tanh))
+    return (base - correction).sum(-1)
+
+
+def _route(obs: dict, cfg):
+    for key in (cfg.policy_obs_key, cfg.value_obs_key):
+        if key not in obs:
+            raise ConfigError(f"observation slot {key!r} missing")
+    return obs[cfg.policy_obs_key], obs[cfg.value_obs_key]
+
+
+def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer=None,
+                           value_normalizer=None, noise=None, generator=None):
+    """Unroll ``cfg.unroll_length`` control steps across the batch on the GPU.
+
+    env: DeviceBatchEnv; policy / value: CUDA ``nn.Module``s with the
+    reference's MLPPolicy / MLPValue interfaces; obs: the device observation
+    dict to resume from; normalisers: DeviceRunningNormalizer or None.
+    Returns (DeviceRolloutBatch, next obs dict, mean raw reward tensor).
+    """
+    import torch
+
+    T, N = int(cfg.unroll_length), env.num_envs
+    if noise is not None and tuple(noise.shape[:2]) != (T, N):
+        raise ConfigError("noise must be [unroll_length, num_envs, action_dim]")
+    out = env._outputs((), False)  # reused step buffers (stream-ordered)
+    f32 = torch.float32
+    p_obs, v_obs, acts, pres, lps, rews, dns, vals = [], [], [], [], [], [], [], []
+    raw_p, raw_v = [], []
+    raw_reward_sum = torch.zeros((), dtype=torch.float64, device=env.device)
+
+    def prep(normalizer, x):
+        return (normalizer.apply(x) if normalizer is not None else x).to(f32)
+
+    with torch.no_grad():
+        for t in range(T):
+            pol_in, val_in = _route(obs, cfg)
+            pol_t, val_t = prep(policy_normalizer, pol_in), prep(value_normalizer, val_in)
+            if policy_normalizer is not None:
+                raw_p.append(pol_in.clone())
+            if value_normalizer is not None:
+                raw_v.append(val_in.clone())
+            mean, log_std = policy(pol_t)
+            eps = noise[t].to(mean.dtype) if noise is not None else torch.randn(
+                mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
+            pre_tanh = mean + torch.exp(log_std) * eps
+            action = torch.tanh(pre_tanh)
+            log_prob = tanh_gaussian_log_prob(mean, log_std, pre_tanh)
+            v = value(val_t)
+            step = env.step(action.to(env.dtype), autoreset=True, with_info=False, out=out)
+            reward = step["reward"].to(torch.float64)
+            raw_reward_sum += reward.mean()
+            # truncation bootstraps through the terminal observation (ppo.py:327-341),
+            # for every world at once, masked to the truncated, non-terminated ones
+            boot = step["trunc"] & ~step["done"] & step["terminal_mask"]
+            term_in = torch.where(boot[:, None], step["terminal_obs"],
+                                  torch.zeros((), dtype=env.dtype, device=env.device))
+            _, tv_in = _route({"state": term_in, "privileged_state": term_in}, cfg)
+            tv = value(prep(value_normalizer, tv_in)).to(torch.float64)
+            term_val = torch.where(boot, tv, torch.zeros_like(tv))
+            p_obs.append(pol_t)
+            v_obs.append(val_t)
+            acts.append(action.to(torch.float64))
+            pres.append(pre_tanh)
+            lps.append(log_prob)
+            rews.append(reward * cfg.reward_scaling + cfg.discounting * term_val)
+            dns.append((step["done"] | step["trunc"]).to(torch.float64))
+            vals.append(v.to(torch.float64))
+            nxt = step["obs"].clone()
+            obs = {"state": nxt, "privileged_state": nxt}
+        _, val_in = _route(obs, cfg)
+        bootstrap = value(prep(value_normalizer, val_in)).to(torch.float64)
+    batch = DeviceRolloutBatch(torch.stack(p_obs), torch.stack(v_obs), torch.stack(acts),
+                               torch.stack(pres), torch.stack(lps), torch.stack(rews),
+                               torch.stack(dns), torch.stack(vals), bootstrap)
+    # fold the phase's raw observations into the statistics afterwards (ppo.py:370-377)
+    if raw_p:
+        policy_normalizer.update(torch.cat(raw_p, 0))
+    if raw_v:
+        value_normalizer.update(torch.cat(raw_v, 0))
+    return batch, obs, raw_reward_sum / T
+
+
+__all__ = ["DeviceRolloutBatch", "collect_rollout_device", "make_policy", "make_value",
+           "tanh_gaussian_log_prob"]

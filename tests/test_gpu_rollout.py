@@ -1,0 +1,71 @@
+"""On-device rollout collection against the reference's own
+ppo.collect_rollout (tests/golden/rollout_golden.npz: 64 cartpole worlds,
+episode_length 5 so truncation bootstraps happen inside the 8-step unroll, two
+phases with observation normalisers, the reference's MLP weights and noise).
+
+Tolerance: the networks run in float32 on cuBLAS vs the reference's CPU torch
+(different summation order, ~1e-7 relative per layer) and the env in float64:
+everything agrees to 1e-4 relative (floor 1e-3); truncation / done flags exactly."""
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def gold():
+    from tests.conftest import GOLDEN
+
+    return np.load(os.path.join(GOLDEN, "rollout_golden.npz"))
+
+
+def _close(a, b, floor=1e-3):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor)))
+
+
+def test_collect_rollout_matches_reference(gold):
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+
+    N, T = 64, 8
+    policy = R.make_policy(5, 1, (32, 32)).cuda()
+    value = R.make_value(5, (48, 48)).cuda()
+    policy.load_state_dict({k[7:]: torch.as_tensor(gold[k]) for k in gold.files
+                            if k.startswith("policy/")})
+    value.load_state_dict({k[6:]: torch.as_tensor(gold[k]) for k in gold.files
+                           if k.startswith("value/")})
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = T, 10.0, 0.995
+        policy_obs_key = value_obs_key = "state"
+
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance", episode_length=5), N,
+                            dtype="float64")
+    obs = env.reset(seed=3)
+    np.testing.assert_array_equal(obs["state"].cpu().numpy(), gold["obs0"])
+    pn, vn = P.DeviceRunningNormalizer(5), P.DeviceRunningNormalizer(5)
+    for phase in range(2):
+        g = lambda k: gold[f"p{phase}/{k}"]  # noqa: E731
+        noise = torch.as_tensor(g("noise"), device="cuda")
+        batch, obs, mean_r = R.collect_rollout_device(env, policy, value, Cfg, obs, pn, vn,
+                                                      noise=noise)
+        np.testing.assert_array_equal(batch.dones.cpu().numpy(), g("dones"))
+        for f in ("policy_obs", "value_obs", "actions", "pre_tanh", "log_probs", "rewards",
+                  "values", "bootstrap"):
+            err = _close(getattr(batch, f).cpu().numpy(), g(f))
+            assert err < 1e-4, (phase, f, err)
+        assert _close(obs["state"].cpu().numpy(), g("next_obs")) < 1e-4
+        assert abs(float(mean_r) - float(g("mean_reward"))) < 1e-4
+        for name, nz in (("pn", pn), ("vn", vn)):
+            c, m, v = nz.to_numpy()
+            assert c == float(g(f"{name}_count"))
+            assert _close(m, g(f"{name}_mean"), 1e-6) < 1e-4
+            assert _close(v, g(f"{name}_var"), 1e-6) < 1e-4
+    env.check()
