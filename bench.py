@@ -315,10 +315,11 @@ def run_b200(args, rank, world, local_rank, dist):
     tail = None
     if not args.no_tail:
         tail = bench_go1_tail(args, dev, rank)
-    dropin = sweep = None
+    dropin = sweep = ppo_rollout = None
     if rank == 0 and not args.no_extra:
         dropin = bench_dropin_step(args, dev)
         sweep = bench_sweep(args, dev)
+        ppo_rollout = bench_ppo_rollout(args, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -358,11 +359,58 @@ def run_b200(args, rank, world, local_rank, dist):
             "go1_tail": tail,
             "e2e_dropin_step": dropin,
             "sweep": sweep,
+            "ppo_rollout": ppo_rollout,
             "clocks": clocks.summary(),
             "library": _native.LIB_PATH,
         }
         print(json.dumps(line), flush=True)
     env.close()
+
+
+def bench_ppo_rollout(args, dev, T=30, reps=5):
+    """ppo.collect_rollout on the device (RolloutGraph: the
+    reference's default MLPPolicy 4x128 / MLPValue 5x256 in float32 on cuBLAS,
+    sampling, env step, truncation bootstrap, normalisers) + compute_gae, per
+    phase of T control steps over the bench's worlds.  Reference measured in
+    the build container: 9.7e3 env-steps/s (N=1024, 16 torch threads)."""
+    import torch
+
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = T, 10.0, 0.995
+        policy_obs_key = value_obs_key = "state"
+
+    n = args.num_envs
+    torch.manual_seed(0)
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.task), n, dtype="float32")
+    obs = env.reset(seed=0)
+    od, ad = env.obs_dim, env.action_dim
+    policy, value = R.make_policy(od, ad).cuda(dev), R.make_value(od).cuda(dev)
+    pn, vn = P.DeviceRunningNormalizer(od), P.DeviceRunningNormalizer(od)
+    rg = R.RolloutGraph(env, policy, value, Cfg, obs, pn, vn)
+    for _ in range(2):
+        rg.run()
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        batch, _, _ = rg.run()
+        P.compute_gae_batch(batch.rewards, batch.values, batch.bootstrap, batch.dones,
+                            0.995, 0.95)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    env.check()
+    ms = e0.elapsed_time(e1) / reps
+    env.close()
+    return {"metric": "env-steps/s of on-device PPO rollout collection incl. policy + value "
+                      "inference (float32, CUDA graph)", "value": T * n / (ms / 1e3),
+            "unit": "env_steps/s", "ms_per_phase": ms, "unroll_length": T, "worlds": n,
+            "reference_cpu": {"value": 9.7e3, "unit": "env_steps/s",
+                              "sample": "ppo.collect_rollout, N=1024, T=30, 16 torch threads, "
+                                        "build container (not the GPU box)"}}
 
 
 def bench_dropin_step(args, dev, steps=300):

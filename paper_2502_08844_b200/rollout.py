@@ -38,6 +38,8 @@ class DeviceRolloutBatch:
     dones: object
     values: object
     bootstrap: object
+    raw_policy_obs: object = None  # [T*N, O] raw observations of the phase (normaliser input)
+    raw_value_obs: object = None
 
 
 _LOG_2 = 0.6931471805599453
@@ -112,7 +114,8 @@ def _route(obs: dict, cfg):
 
 
 def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer=None,
-                           value_normalizer=None, noise=None, generator=None):
+                           value_normalizer=None, noise=None, generator=None,
+                           update_normalizers: bool = True):
     """Unroll ``cfg.unroll_length`` control steps across the batch on the GPU.
 
     env: DeviceBatchEnv; policy / value: CUDA ``nn.Module``s with the
@@ -175,13 +178,69 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
     batch = DeviceRolloutBatch(torch.stack(p_obs), torch.stack(v_obs), torch.stack(acts),
                                torch.stack(pres), torch.stack(lps), torch.stack(rews),
                                torch.stack(dns), torch.stack(vals), bootstrap)
+    batch.raw_policy_obs = torch.cat(raw_p, 0) if raw_p else None
+    batch.raw_value_obs = torch.cat(raw_v, 0) if raw_v else None
     # fold the phase's raw observations into the statistics afterwards (ppo.py:370-377)
-    if raw_p:
-        policy_normalizer.update(torch.cat(raw_p, 0))
-    if raw_v:
-        value_normalizer.update(torch.cat(raw_v, 0))
+    if update_normalizers:
+        _update(batch, policy_normalizer, value_normalizer)
     return batch, obs, raw_reward_sum / T
 
 
-__all__ = ["DeviceRolloutBatch", "collect_rollout_device", "make_policy", "make_value",
-           "tanh_gaussian_log_prob"]
+def _update(batch, policy_normalizer, value_normalizer):
+    if batch.raw_policy_obs is not None:
+        policy_normalizer.update(batch.raw_policy_obs)
+    if batch.raw_value_obs is not None:
+        value_normalizer.update(batch.raw_value_obs)
+
+
+class RolloutGraph:
+    """``collect_rollout_device`` captured once as a CUDA graph and replayed
+    per phase: the ~40 small kernels of a control step (two MLPs, sampling,
+    env step, bootstrap, bookkeeping) then cost one graph launch per phase
+    instead of ~40 Python-dispatched launches per step.  The normaliser
+    statistics are device tensors read by the replayed kernels; their update
+    (which needs the host-side count) runs eagerly after each replay.  Capture
+    happens after a first eager phase, so the normalisers' "count == 0: copy"
+    branch is already decided.  Noise comes from torch's default CUDA
+    generator (graph-safe Philox offsets)."""
+
+    def __init__(self, env, policy, value, cfg, obs: dict, policy_normalizer=None,
+                 value_normalizer=None):
+        import torch
+
+        self.env, self.policy, self.value, self.cfg = env, policy, value, cfg
+        self.pn, self.vn = policy_normalizer, value_normalizer
+        # one eager phase: warms up cuBLAS / allocator and fills the statistics
+        batch, obs, self.mean_reward = collect_rollout_device(
+            env, policy, value, cfg, obs, policy_normalizer, value_normalizer)
+        self.obs_in = obs["state"].clone()
+        self.last = batch
+        side = torch.cuda.Stream(device=env.device)
+        side.wait_stream(torch.cuda.current_stream(env.device))
+        with torch.cuda.stream(side):  # capture warm-up on a side stream
+            collect_rollout_device(env, policy, value, cfg,
+                                   {"state": self.obs_in, "privileged_state": self.obs_in},
+                                   policy_normalizer, value_normalizer,
+                                   update_normalizers=False)
+        torch.cuda.current_stream(env.device).wait_stream(side)
+        self.graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.graph):
+            self.batch, self.obs_out, self.reward_out = collect_rollout_device(
+                env, policy, value, cfg, {"state": self.obs_in, "privileged_state": self.obs_in},
+                policy_normalizer, value_normalizer, update_normalizers=False)
+
+    def run(self, obs: dict | None = None):
+        """One phase from ``obs`` (default: where the previous phase stopped).
+        Returns (batch, next obs, mean raw reward); the batch tensors are the
+        graph's static outputs, overwritten by the next ``run``."""
+        if obs is not None and obs["state"].data_ptr() != self.obs_in.data_ptr():
+            self.obs_in.copy_(obs["state"])
+        self.graph.replay()
+        _update(self.batch, self.pn, self.vn)
+        self.obs_in.copy_(self.obs_out["state"])
+        return self.batch, {"state": self.obs_in, "privileged_state": self.obs_in}, \
+            self.reward_out
+
+
+__all__ = ["DeviceRolloutBatch", "RolloutGraph", "collect_rollout_device", "make_policy",
+           "make_value", "tanh_gaussian_log_prob"]

