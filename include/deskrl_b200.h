@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DK_ABI_VERSION 3  /* 2: sensor-noise kinds, randomize_params, delay lines; 3: PPO math */
+#define DK_ABI_VERSION 4  /* 2: DR kinds / params / delays; 3: PPO math; 4: pixels */
 
 /* Status codes.  The Python host maps them to the reference's exception
  * classes: ConfigError (randomization.py:19), InvalidInputError
@@ -299,6 +299,44 @@ int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double c
 int dk_norm_apply(int dtype, int64_t rows, int dim, const void *batch, double count,
                   const double *mean, const double *var, double epsilon, int invert, void *out,
                   void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Cartpole pixel observations: pixelrender.py's
+ * rasteriser, brightness post-process, luma and 3-frame stack.
+ * A frame is drawn from (cart x, cos th, sin th) -- the first three entries
+ * of a cartpole state_obs row -- and 13 visual doubles per world: background,
+ * cart and pole RGB, camera offset x / y, zoom, brightness. */
+typedef struct dk_visual_bounds { /* VisualBounds, pixelrender.py:44-51 */
+    double nominal[13];
+    double color_jitter, camera_offset_range;
+    double zoom_range[2], brightness_range[2];
+} dk_visual_bounds;
+
+/* batch_render (+ brightness_postprocess when brightness != 0): frames
+ * [n, 3] (x, cos, sin) f64, visuals [n, 13] -> RGB out [n, h, w, 3] u8. */
+int dk_pixels_render_rgb(int64_t n, int w, int h, double pole_length, const double *frames,
+                         const double *visuals, int brightness, uint8_t *out, void *stream);
+
+/* Per-world stack bookkeeping after a reset (first != 0) or a step: history
+ * [n, 3, 3] f64 (three frames, oldest first), visuals [n, 13] f64, episode
+ * [n] u32.  Worlds reset this step (reset_mask [n] u8, or all when first)
+ * draw new visuals -- randomize_visuals from stream_rng(seed, env, episode, 0)
+ * after skip_words sample_initial draws, or bounds->nominal -- and refill the
+ * history with the new frame; the others shift it. */
+int dk_pixels_advance(int dtype, int64_t n, int obs_dim, const void *obs,
+                      const uint8_t *reset_mask, int first, double *history, double *visuals,
+                      uint32_t *episode, int randomize, const dk_visual_bounds *bounds,
+                      uint64_t seed, int64_t env_index_offset, int skip_words, void *stream);
+
+/* The stacked grayscale observation [n, h, w, 3] (dtype) of the history. */
+int dk_pixels_stack(int dtype, int64_t n, int w, int h, double pole_length,
+                    const double *history, const double *visuals, void *out, void *stream);
+
+/* Terminal stacks of autoreset worlds (mask [n] u8): [h1, h2, term_obs frame]
+ * with the pre-reset visuals; call before dk_pixels_advance. */
+int dk_pixels_terminal(int dtype, int64_t n, int w, int h, double pole_length, int obs_dim,
+                       const void *term_obs, const uint8_t *mask, const double *history,
+                       const double *visuals, void *out, void *stream);
 
 int dk_abi_version(void);
 const char *dk_last_error(void);

@@ -73,6 +73,12 @@ class NoiseKeyC(ctypes.Structure):
                 ("episode", ctypes.c_void_p), ("step", ctypes.c_uint64)]
 
 
+class VisualBoundsC(ctypes.Structure):
+    _fields_ = [("nominal", ctypes.c_double * 13), ("color_jitter", ctypes.c_double),
+                ("camera_offset_range", ctypes.c_double), ("zoom_range", ctypes.c_double * 2),
+                ("brightness_range", ctypes.c_double * 2)]
+
+
 _vp = ctypes.c_void_p
 _u8p = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -122,6 +128,17 @@ _SIGS = {
                                             ctypes.c_double, ctypes.POINTER(NoiseKeyC), _vp,
                                             _vp]),
     "dk_dr_curriculum": (ctypes.c_int, [_i64, _vp, _vp, _i64, _i64, _vp]),
+    "dk_pixels_render_rgb": (ctypes.c_int, [_i64, ctypes.c_int, ctypes.c_int, ctypes.c_double,
+                                            _vp, _vp, ctypes.c_int, _vp, _vp]),
+    "dk_pixels_advance": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp, ctypes.c_int,
+                                         _vp, _vp, _vp, ctypes.c_int,
+                                         ctypes.POINTER(VisualBoundsC), ctypes.c_uint64, _i64,
+                                         ctypes.c_int, _vp]),
+    "dk_pixels_stack": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, ctypes.c_int,
+                                       ctypes.c_double, _vp, _vp, _vp, _vp]),
+    "dk_pixels_terminal": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, ctypes.c_int,
+                                          ctypes.c_double, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
+                                          _vp]),
     "dk_ppo_gae": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_double,
                                   ctypes.c_double, _vp, _vp, _vp]),
     "dk_norm_update": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,

@@ -37,6 +37,7 @@ UNITS = {
     "capi.cu": [],
     "capi_loco.cu": [],
     "capi_ppo.cu": ["--fmad=false"],
+    "capi_pixels.cu": ["--fmad=false"],
 }
 
 

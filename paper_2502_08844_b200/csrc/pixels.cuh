@@ -1,0 +1,226 @@
+// pixels.cuh -- the cartpole pixel observation path on device (SURVEY.md §8f
+// rank 2): the software rasteriser, brightness post-process, ITU-R 601 luma
+// and the three-frame grayscale stack of `cartpole-balance-pixels`.
+//
+//   batch_render            pixelrender.py:73-131
+//   randomize_visuals       pixelrender.py:134-153 (+ envkit.py:515-518 keying)
+//   brightness_postprocess  pixelrender.py:156-161
+//   rgb_to_gray             pixelrender.py:184-186
+//   FrameStack              pixelrender.py:164-181 / Environment._observe envkit.py:555-577
+//
+// Design: a frame is a function of (cart x, cos th, sin th, visuals) only, so a
+// world's stacked observation is rendered from its last three states instead of
+// being read back from HBM: the kernel writes the [H, W, 3] stack once and reads
+// nothing per pixel (write-only HBM traffic).  Each pixel is one of three
+// colours, so a world's three gray levels are computed once per frame.
+// float64 arithmetic follows the reference's NumPy expression order with one
+// rounding per operation (_rn intrinsics).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "envmath.cuh"
+
+namespace dk {
+
+// VisualParams packed as 12 doubles: background rgb, cart rgb, pole rgb,
+// camera offset x, y, zoom; + brightness = 13.
+constexpr int kVis = 13;
+
+struct PixFrame {  // one state to draw: cart x and the pole direction
+    double x, c, s;
+};
+
+// Classify pixel (row, col) of a w x h view: 0 background, 1 cart, 2 pole.
+__device__ __forceinline__ int pix_class(const double *vis, double pole_len, int w, int h, int row,
+                                         int col, const PixFrame &f) {
+    const double px = __dsub_rn(__dadd_rn((double)col, 0.5), __ddiv_rn((double)w, 2.0));
+    const double py = __dsub_rn(__ddiv_rn((double)h, 2.0), __dadd_rn((double)row, 0.5));
+    // _world_to_pixel_scale: w / (2.0 * _VIEW_HALF_WIDTH) * zoom
+    const double scale = __dmul_rn(__ddiv_rn((double)w, __dmul_rn(2.0, 2.4)), vis[11]);
+    const double wx = __dadd_rn(__ddiv_rn(px, scale), vis[9]);
+    const double wy = __dadd_rn(__ddiv_rn(py, scale), vis[10]);
+    int cls = 0;
+    if (fabs(__dsub_rn(wx, f.x)) <= 0.36 / 2 && fabs(__dsub_rn(wy, 0.0)) <= 0.22 / 2) cls = 1;
+    // pole segment from the pivot (cart top) to pivot + l (sin th, cos th)
+    const double p0 = f.x, p1 = __dadd_rn(0.0, 0.22 / 2);
+    const double d0 = __dsub_rn(__dadd_rn(p0, __dmul_rn(pole_len, f.s)), p0);
+    const double d1 = __dsub_rn(__dadd_rn(p1, __dmul_rn(pole_len, f.c)), p1);
+    const double seg = __dadd_rn(__dmul_rn(d0, d0), __dmul_rn(d1, d1));
+    const double rx = __dsub_rn(wx, p0), ry = __dsub_rn(wy, p1);
+    double t = __ddiv_rn(__dadd_rn(__dmul_rn(rx, d0), __dmul_rn(ry, d1)), seg);
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    const double ex = __dsub_rn(rx, __dmul_rn(t, d0)), ey = __dsub_rn(ry, __dmul_rn(t, d1));
+    const double dist2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+    if (dist2 <= (0.045 / 2) * (0.045 / 2)) cls = 2;
+    return cls;
+}
+
+// colour channel as drawn: np.asarray(color, uint8) truncates the float
+__device__ __forceinline__ uint8_t color_u8(double v) { return (uint8_t)(int)v; }
+
+// brightness_postprocess then rgb_to_gray of one colour
+__device__ __forceinline__ double gray_of(const double *rgb, double bright) {
+    double ch[3];
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        double v = rint(__dmul_rn((double)color_u8(rgb[k]), bright));
+        v = v < 0.0 ? 0.0 : (v > 255.0 ? 255.0 : v);
+        ch[k] = (double)(uint8_t)(int)v;
+    }
+    // img @ _LUMA / 255.0.  NumPy's float64 matmul kernel (this image's NumPy
+    // 2.3 build) evaluates the three-term dot as fma(b, .114, fma(r, .299, g * .587))
+    // -- checked against 70 000 random colours, 0 mismatches (tests/golden fixtures)
+    const double dot =
+        __fma_rn(ch[2], 0.114, __fma_rn(ch[0], 0.299, __dmul_rn(ch[1], 0.587)));
+    return __ddiv_rn(dot, 255.0);
+}
+
+// One CTA per world: threads stride over the h*w pixels; each pixel's three
+// stacked frames (oldest first) are written as three consecutive values.
+// hist: [n, 3] frames (oldest first).  For worlds in `mask` (an autoreset this
+// step) the terminal stack [h1, h2, term] is drawn with the old visuals into
+// term_out, the new episode's visuals are drawn from its stream, and the
+// observation is three copies of the new first frame.
+template <typename T>
+__global__ void pixel_stack_kernel(int64_t n, int w, int h, double pole_len,
+                                   const PixFrame *__restrict__ hist, const double *__restrict__ vis,
+                                   T *__restrict__ out) {
+    const int64_t i = blockIdx.x;
+    if (i >= n) return;
+    __shared__ double g[3];  // gray level of background / cart / pole
+    __shared__ double v[kVis];
+    __shared__ PixFrame fr[3];
+    if (threadIdx.x < kVis) v[threadIdx.x] = vis[i * kVis + threadIdx.x];
+    if (threadIdx.x < 3) fr[threadIdx.x] = hist[i * 3 + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < 3) g[threadIdx.x] = gray_of(v + 3 * threadIdx.x, v[12]);
+    __syncthreads();
+    T *o = out + i * (int64_t)w * h * 3;
+    for (int p = threadIdx.x; p < w * h; p += blockDim.x) {
+        const int row = p / w, col = p - row * w;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * p + k] = (T)g[pix_class(v, pole_len, w, h, row, col, fr[k])];
+    }
+}
+
+// batch_render + brightness_postprocess: RGB uint8 [n, h, w, 3] of one frame.
+static __global__ void pixel_rgb_kernel(int64_t n, int w, int h, double pole_len,
+                                        const PixFrame *__restrict__ frames,
+                                        const double *__restrict__ vis, int brighten,
+                                        uint8_t *__restrict__ out) {
+    const int64_t i = blockIdx.x;
+    if (i >= n) return;
+    __shared__ double v[kVis];
+    __shared__ uint8_t col[3][3];
+    if (threadIdx.x < kVis) v[threadIdx.x] = vis[i * kVis + threadIdx.x];
+    __syncthreads();
+    if (threadIdx.x < 9) {
+        const int c = threadIdx.x / 3, k = threadIdx.x % 3;
+        uint8_t u = color_u8(v[3 * c + k]);
+        if (brighten) {
+            double b = rint(__dmul_rn((double)u, v[12]));
+            b = b < 0.0 ? 0.0 : (b > 255.0 ? 255.0 : b);
+            u = (uint8_t)(int)b;
+        }
+        col[c][k] = u;
+    }
+    __syncthreads();
+    const PixFrame f = frames[i];
+    uint8_t *o = out + i * (int64_t)w * h * 3;
+    for (int p = threadIdx.x; p < w * h; p += blockDim.x) {
+        const int row = p / w, cc = p - row * w;
+        const int cls = pix_class(v, pole_len, w, h, row, cc, f);
+        o[3 * p] = col[cls][0];
+        o[3 * p + 1] = col[cls][1];
+        o[3 * p + 2] = col[cls][2];
+    }
+}
+
+// randomize_visuals (pixelrender.py:134-153) drawn from the episode's stream
+// (envkit.py:506-516: the reset's step-0 stream, after sample_initial's draws).
+struct VisualBoundsC {
+    double nominal[kVis];  // VisualParams nominal (packed as above)
+    double color_jitter, camera_offset_range, zoom_lo, zoom_hi, bright_lo, bright_hi;
+};
+
+__device__ __forceinline__ void draw_visuals(Philox4x64 &rng, const VisualBoundsC &b,
+                                             double *vis) {
+    for (int c = 0; c < 3; ++c)
+        for (int k = 0; k < 3; ++k) {
+            double x = __dadd_rn(b.nominal[3 * c + k], rng.uniform(-b.color_jitter, b.color_jitter));
+            vis[3 * c + k] = x < 0.0 ? 0.0 : (x > 255.0 ? 255.0 : x);  // np.clip(c, 0, 255)
+        }
+    vis[9] = rng.uniform(-b.camera_offset_range, b.camera_offset_range);
+    vis[10] = rng.uniform(-b.camera_offset_range, b.camera_offset_range);
+    vis[11] = rng.uniform(b.zoom_lo, b.zoom_hi);
+    vis[12] = rng.uniform(b.bright_lo, b.bright_hi);
+}
+
+// Per-world bookkeeping after a step (one thread per world): shift the frame
+// history, or on an autoreset draw the new episode's visuals (skipping the
+// `skip` words sample_initial consumed) and refill the history.
+// obs / term_obs rows: [x, cos th, sin th, ...] (cartpole state_obs).
+template <typename T>
+__global__ void pixel_advance_kernel(int64_t n, int obs_dim, const T *__restrict__ obs,
+                                     const uint8_t *__restrict__ reset_mask, int first,
+                                     PixFrame *__restrict__ hist, double *__restrict__ vis,
+                                     uint32_t *__restrict__ episode, int randomize,
+                                     VisualBoundsC bounds, uint64_t seed, int64_t env0, int skip) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const PixFrame f{(double)obs[i * obs_dim], (double)obs[i * obs_dim + 1],
+                     (double)obs[i * obs_dim + 2]};
+    const bool reset = first || (reset_mask && reset_mask[i]);
+    if (reset) {
+        if (!first) episode[i] += 1u;
+        double nv[kVis];
+        if (randomize) {
+            Philox4x64 rng;
+            rng.init(seed, (uint64_t)(env0 + i), episode[i], 0);
+            for (int k = 0; k < skip; ++k) (void)rng.next64();
+            draw_visuals(rng, bounds, nv);
+        } else {
+            for (int k = 0; k < kVis; ++k) nv[k] = bounds.nominal[k];
+        }
+        for (int k = 0; k < kVis; ++k) vis[i * kVis + k] = nv[k];
+        hist[3 * i] = f;
+        hist[3 * i + 1] = f;
+        hist[3 * i + 2] = f;
+    } else {
+        hist[3 * i] = hist[3 * i + 1];
+        hist[3 * i + 1] = hist[3 * i + 2];
+        hist[3 * i + 2] = f;
+    }
+}
+
+// The terminal stack of autoreset worlds: [h1, h2, term] with the old visuals
+// (called before pixel_advance_kernel replaces them).
+template <typename T>
+__global__ void pixel_terminal_kernel(int64_t n, int w, int h, double pole_len, int obs_dim,
+                                      const T *__restrict__ term_obs,
+                                      const uint8_t *__restrict__ mask,
+                                      const PixFrame *__restrict__ hist,
+                                      const double *__restrict__ vis, T *__restrict__ out) {
+    const int64_t i = blockIdx.x;
+    if (i >= n || !mask[i]) return;
+    __shared__ double g[3];
+    __shared__ double v[kVis];
+    __shared__ PixFrame fr[3];
+    if (threadIdx.x < kVis) v[threadIdx.x] = vis[i * kVis + threadIdx.x];
+    if (threadIdx.x < 2) fr[threadIdx.x] = hist[i * 3 + 1 + threadIdx.x];
+    if (threadIdx.x == 2)
+        fr[2] = PixFrame{(double)term_obs[i * obs_dim], (double)term_obs[i * obs_dim + 1],
+                         (double)term_obs[i * obs_dim + 2]};
+    __syncthreads();
+    if (threadIdx.x < 3) g[threadIdx.x] = gray_of(v + 3 * threadIdx.x, v[12]);
+    __syncthreads();
+    T *o = out + i * (int64_t)w * h * 3;
+    for (int p = threadIdx.x; p < w * h; p += blockDim.x) {
+        const int row = p / w, col = p - row * w;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * p + k] = (T)g[pix_class(v, pole_len, w, h, row, col, fr[k])];
+    }
+}
+
+}  // namespace dk
