@@ -140,6 +140,9 @@ class TaskSpec:
     default_dt: float
     info_keys: tuple
     params: DynamicsParams = field(default_factory=DynamicsParams)
+    pixels: bool = False              # cartpole-balance-pixels / obs_mode "pixels"
+    image_size: int = 64
+    visual_randomization: bool = False
 
 
 _TASK_TABLE = {
@@ -167,14 +170,23 @@ def resolve_task(config, params=None) -> TaskSpec:
         name = base
     if name not in _TASK_TABLE:
         raise ConfigError(f"unknown task id {config.task!r}")
-    if pixels:
-        raise ConfigError("pixel observations are not provided by the B200 env-step backend "
-                          "(state observations only)")
+    if pixels and name != "cartpole-balance":
+        raise ConfigError(f"no pixel variant for task {name!r}")
     idx, a, o, s, default_dt, keys = _TASK_TABLE[name]
     base_params = params or DynamicsParams()
     dt = config.dt if config.dt is not None else default_dt
     p = DynamicsParams(**{f: float(getattr(base_params, f)) for f in nat.PARAM_FIELDS})
-    return TaskSpec(name, idx, a, o, s, default_dt, keys, p.with_dt(float(dt)))
+    return TaskSpec(name, idx, a, o, s, default_dt, keys, p.with_dt(float(dt)), pixels,
+                    int(getattr(config, "image_size", 64)),
+                    bool(getattr(config, "visual_randomization", False)))
+
+
+def _pixel_obs(spec, num_envs, seed, env_index_offset, dtype, device):
+    """PixelObservation for a pixel task (pixelrender via paper_2502_08844_b200.pixels)."""
+    from .pixels import PixelObservation
+
+    return PixelObservation(num_envs, spec.image_size, spec.visual_randomization, seed,
+                            env_index_offset, spec.params.pole_length, dtype, device)
 
 
 def _dtype_code(dtype) -> int:
@@ -262,11 +274,12 @@ class _Infos(Sequence):
     infos[i] holds the reward terms of world i (envkit.py:289-453) and, when
     the world auto-reset, ``terminal_observation`` (envkit.py:632-634)."""
 
-    def __init__(self, keys, info, term_mask, term_obs):
+    def __init__(self, keys, info, term_mask, term_obs, term_pixels=None):
         self._keys = keys
         self._info = info
         self._mask = term_mask
         self._term = term_obs
+        self._term_pixels = term_pixels
 
     def __len__(self):
         return self._info.shape[0]
@@ -282,6 +295,8 @@ class _Infos(Sequence):
         if self._mask is not None and self._mask[i]:
             t = np.array(self._term[i], dtype=np.float64)
             d["terminal_observation"] = {"state": t, "privileged_state": t.copy()}
+            if self._term_pixels is not None:
+                d["terminal_observation"]["pixels"] = self._term_pixels[i]
         return d
 
 
@@ -357,6 +372,14 @@ class BatchEnv:
         self.dtype = np.dtype(self._h.np_dtype)
         self._alloc_host_buffers()
         self._envs = None
+        self._pix = None
+        if spec.pixels:  # rendered on the device from the state observations
+            import torch
+
+            self._torch = torch
+            self._pix_dev = torch.device("cuda", device)
+            self._pix = _pixel_obs(spec, self.num_envs, int(config.seed), self.env_index_offset,
+                                   torch.float64, self._pix_dev)
 
     # pinned host staging (allocated once; outputs are copied out per call)
     def _alloc_host_buffers(self):
@@ -387,7 +410,11 @@ class BatchEnv:
                                               0 if seed is None else int(seed) & (2**64 - 1),
                                               self._b_obs.ctypes.data))
         obs = self._b_obs.astype(np.float64)
-        return {"state": obs, "privileged_state": obs.copy()}
+        out = {"state": obs, "privileged_state": obs.copy()}
+        if self._pix is not None:
+            t = self._torch.as_tensor(obs, device=self._pix_dev)
+            out["pixels"] = self._pix.reset(t, seed).cpu().numpy()
+        return out
 
     def step(self, actions, autoreset: bool = True):
         actions = np.asarray(actions, dtype=float)
@@ -410,9 +437,20 @@ class BatchEnv:
         truncs = self._b_trunc.astype(bool)
         mask = self._b_mask.astype(bool)
         term = self._b_term.astype(np.float64) if mask.any() else None
+        out = {"state": obs, "privileged_state": obs.copy()}
+        term_pix = None
+        if self._pix is not None:
+            tt = self._torch
+            d = self._pix_dev
+            so = {"obs": tt.as_tensor(obs, device=d),
+                  "terminal_obs": tt.as_tensor(self._b_term.astype(np.float64), device=d),
+                  "terminal_mask": tt.as_tensor(self._b_mask.astype(bool), device=d)}
+            pix, tp = self._pix.step(so, terminal=term is not None)
+            out["pixels"] = pix.cpu().numpy()
+            term_pix = tp.cpu().numpy() if tp is not None else None
         infos = _Infos(self._h.spec.info_keys, self._b_info.astype(np.float64),
-                       mask if term is not None else None, term)
-        return {"state": obs, "privileged_state": obs.copy()}, rewards, dones, truncs, infos
+                       mask if term is not None else None, term, term_pix)
+        return out, rewards, dones, truncs, infos
 
     def close(self):
         self._h.close()
@@ -452,6 +490,8 @@ class DeviceBatchEnv:
         self.obs_dim = self.spec.obs_dim
         self.info_keys = self.spec.info_keys
         self.dtype = torch.float64 if self._h.dtype_code == nat.DK_F64 else torch.float32
+        self._pix = (_pixel_obs(self.spec, self.num_envs, int(config.seed), self.env_index_offset,
+                                self.dtype, dev) if self.spec.pixels else None)
 
     def _stream(self):
         return ctypes.c_void_p(self._torch.cuda.current_stream(self.device).cuda_stream)
@@ -469,7 +509,10 @@ class DeviceBatchEnv:
         _check(self._h._lib.dk_env_reset(self._h.h, int(seed is not None),
                                          0 if seed is None else int(seed) & (2**64 - 1),
                                          self._ptr(obs), self._stream()))
-        return {"state": obs, "privileged_state": obs}
+        out = {"state": obs, "privileged_state": obs}
+        if self._pix is not None:
+            out["pixels"] = self._pix.reset(obs, seed)
+        return out
 
     def _outputs(self, lead, with_info):
         t, d, n, o = self._torch, self.device, self.num_envs, self.obs_dim
@@ -506,10 +549,14 @@ class DeviceBatchEnv:
             self._ptr(o["reward"]), self._ptr(o["done"]), self._ptr(o["trunc"]),
             self._ptr(o["terminal_obs"]), self._ptr(o["terminal_mask"]), self._ptr(o["info"]),
             self._stream()))
+        if self._pix is not None:  # obs["pixels"] of cartpole-balance-pixels (envkit.py:561-576)
+            o["pixels"], o["terminal_pixels"] = self._pix.step(o)
         return o
 
     def rollout(self, actions, with_info: bool = False, out: dict | None = None):
         """K fused autoreset steps; actions [K, N, A] -> outputs [K, N, ...]."""
+        if self._pix is not None:
+            raise ConfigError("pixel observations are rendered per step: use step()")
         if actions.dim() < 2:
             raise InvalidInputError("rollout actions must be [K, N, A]")
         K = int(actions.shape[0])

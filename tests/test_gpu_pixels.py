@@ -80,3 +80,46 @@ def test_env_pixel_stacks(px, PX, case, dtype):
         if m.any():
             check(term[torch.as_tensor(m, device="cuda")], g("term_pixels")[t][m])
     env.check()
+
+
+@pytest.mark.parametrize("api", ["dropin", "device"])
+def test_pixel_task_through_env_api(px, PX, api):
+    """'cartpole-balance-pixels' through the reference-facing BatchEnv (numpy,
+    infos[i]['terminal_observation']['pixels']) and DeviceBatchEnv."""
+    import paper_2502_08844_b200 as dk
+
+    g = lambda k: px[f"rand/{k}"]  # noqa: E731
+    N = g("state").shape[1]
+    cfg = dk.EnvConfig(task="cartpole-balance-pixels", episode_length=6,
+                       visual_randomization=True)
+    acts = g("actions")
+
+    def close(a, b):
+        assert np.count_nonzero(np.asarray(a) != b) <= max(2, b.size // 10000)
+
+    if api == "dropin":
+        env = dk.BatchEnv(cfg, N)
+        obs = env.reset(seed=4)
+        assert set(obs) == {"state", "privileged_state", "pixels"}
+        close(obs["pixels"], g("pixels")[0])
+        for t in range(acts.shape[0]):
+            obs, r, d, tr, infos = env.step(acts[t])
+            close(obs["pixels"], g("pixels")[t + 1])
+            for i in range(N):
+                if g("term_mask")[t, i]:
+                    close(infos[i]["terminal_observation"]["pixels"], g("term_pixels")[t, i])
+                else:
+                    assert "terminal_observation" not in infos[i]
+    else:
+        env = dk.DeviceBatchEnv(cfg, N, dtype="float64")
+        obs = env.reset(seed=4)
+        close(obs["pixels"].cpu().numpy(), g("pixels")[0])
+        for t in range(acts.shape[0]):
+            out = env.step(torch.as_tensor(acts[t], device="cuda"))
+            close(out["pixels"].cpu().numpy(), g("pixels")[t + 1])
+            m = g("term_mask")[t].astype(bool)
+            if m.any():
+                close(out["terminal_pixels"].cpu().numpy()[m], g("term_pixels")[t][m])
+        with pytest.raises(dk.ConfigError):
+            env.rollout(torch.zeros((2, N, 1), device="cuda", dtype=torch.float64))
+        env.check()
