@@ -315,11 +315,12 @@ def run_b200(args, rank, world, local_rank, dist):
     tail = None
     if not args.no_tail:
         tail = bench_go1_tail(args, dev, rank)
-    dropin = sweep = ppo_rollout = None
+    dropin = sweep = ppo_rollout = pixels = None
     if rank == 0 and not args.no_extra:
         dropin = bench_dropin_step(args, dev)
         sweep = bench_sweep(args, dev)
         ppo_rollout = bench_ppo_rollout(args, dev)
+        pixels = bench_pixels(args, dev)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -360,11 +361,61 @@ def run_b200(args, rank, world, local_rank, dist):
             "e2e_dropin_step": dropin,
             "sweep": sweep,
             "ppo_rollout": ppo_rollout,
+            "pixels": pixels,
             "clocks": clocks.summary(),
             "library": _native.LIB_PATH,
         }
         print(json.dumps(line), flush=True)
     env.close()
+
+
+def bench_pixels(args, dev, steps=50):
+    """cartpole-balance-pixels steps (env step + 64x64 render,
+    brightness, luma, 3-frame stack, visual randomisation at autoreset) through
+    DeviceBatchEnv, float32, 8192 worlds.  Roofline of pixel_stack_kernel:
+    write-only, 64*64*3*4 B per world-step."""
+    import torch
+
+    import paper_2502_08844_b200 as dk
+
+    n = args.num_envs
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance-pixels",
+                                         visual_randomization=True), n, dtype="float32")
+    env.reset(seed=0)
+    acts = torch.rand((steps, n, 1), device=dev) * 2 - 1
+    out = env._outputs((), False)
+    for k in range(5):
+        env.step(acts[k], out=out)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(steps):
+        env.step(acts[k], out=out)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    env.check()
+    ms = e0.elapsed_time(e1) / steps
+    # the stack kernel alone
+    pix = env._pix
+    e0.record()
+    for _ in range(steps):
+        pix._stack()
+    e1.record()
+    torch.cuda.synchronize(dev)
+    ks = e0.elapsed_time(e1) / steps / 1e3
+    peak, src = hbm_peak()
+    bytes_ws = 64 * 64 * 3 * 4
+    env.close()
+    return {"metric": "cartpole-balance-pixels env-steps/s (step + render + 3-frame stack, "
+                      "float32, 64x64)", "value": n / (ms / 1e3), "unit": "env_steps/s",
+            "ms_per_step": ms, "worlds": n,
+            "roofline": {"bound": "hbm", "kernel": "pixel_stack_kernel",
+                         "achieved": n * bytes_ws / ks / 1e9, "peak": peak, "unit": "GB/s",
+                         "frac": n * bytes_ws / ks / 1e9 / peak, "peak_source": src,
+                         "bytes_per_world_step": bytes_ws},
+            "reference_cpu": {"value": 3.4e3, "unit": "env_steps/s",
+                              "sample": "SURVEY.md §8f: BatchEnv('cartpole-balance-pixels'), "
+                                        "N=256, one core"}}
 
 
 def bench_ppo_rollout(args, dev, T=30, reps=5):

@@ -19,6 +19,8 @@ int cuda_rc(cudaError_t e, const char *what) {
 int check_view(int w, int h) {
     if (w <= 0 || h <= 0)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "viewport must have positive area");
+    if (w > dk::kMaxView || h > dk::kMaxView)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "viewport larger than 512 pixels");
     return DK_OK;
 }
 

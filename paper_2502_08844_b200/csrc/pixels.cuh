@@ -56,6 +56,54 @@ __device__ __forceinline__ int pix_class(const double *vis, double pole_len, int
     return cls;
 }
 
+// The same classification with the world coordinates of the pixel centres
+// precomputed (a view has only w distinct wx and h distinct wy, both
+// frame-independent) and the pole's segment constants per frame.  Pixels far
+// from the pole's supporting line skip the clamped projection (and its
+// division): the clamped-segment distance is never below the line distance,
+// and the cut-off keeps a 1e-9 relative margin, so the decision is unchanged.
+struct PoleSeg {
+    double x, p1, d0, d1, seg, band;  // band: reject perp^2 above this
+};
+
+__device__ __forceinline__ PoleSeg pole_seg(const PixFrame &f, double pole_len) {
+    PoleSeg g;
+    g.x = f.x;
+    g.p1 = __dadd_rn(0.0, 0.22 / 2);
+    g.d0 = __dsub_rn(__dadd_rn(f.x, __dmul_rn(pole_len, f.s)), f.x);
+    g.d1 = __dsub_rn(__dadd_rn(g.p1, __dmul_rn(pole_len, f.c)), g.p1);
+    g.seg = __dadd_rn(__dmul_rn(g.d0, g.d0), __dmul_rn(g.d1, g.d1));
+    // line distance^2 = perp^2 / seg  <=  r^2   <=>  perp^2 <= r^2 seg
+    g.band = (0.045 / 2) * (0.045 / 2) * g.seg * (1.0 + 1e-9) + 1e-300;
+    return g;
+}
+
+__device__ __forceinline__ int pix_class_pre(double wx, double wy, const PoleSeg &g) {
+    int cls = 0;
+    if (fabs(__dsub_rn(wx, g.x)) <= 0.36 / 2 && fabs(__dsub_rn(wy, 0.0)) <= 0.22 / 2) cls = 1;
+    const double rx = __dsub_rn(wx, g.x), ry = __dsub_rn(wy, g.p1);
+    const double perp = rx * g.d1 - ry * g.d0;  // (filter only: rounding covered by the margin)
+    if (perp * perp > g.band) return cls;
+    double t = __ddiv_rn(__dadd_rn(__dmul_rn(rx, g.d0), __dmul_rn(ry, g.d1)), g.seg);
+    t = t < 0.0 ? 0.0 : (t > 1.0 ? 1.0 : t);
+    const double ex = __dsub_rn(rx, __dmul_rn(t, g.d0)), ey = __dsub_rn(ry, __dmul_rn(t, g.d1));
+    const double dist2 = __dadd_rn(__dmul_rn(ex, ex), __dmul_rn(ey, ey));
+    if (dist2 <= (0.045 / 2) * (0.045 / 2)) cls = 2;
+    return cls;
+}
+
+// pixel-centre world coordinates of a view (pix_class's wx / wy)
+__device__ __forceinline__ double view_wx(const double *vis, int w, int col) {
+    const double px = __dsub_rn(__dadd_rn((double)col, 0.5), __ddiv_rn((double)w, 2.0));
+    const double scale = __dmul_rn(__ddiv_rn((double)w, __dmul_rn(2.0, 2.4)), vis[11]);
+    return __dadd_rn(__ddiv_rn(px, scale), vis[9]);
+}
+__device__ __forceinline__ double view_wy(const double *vis, int w, int h, int row) {
+    const double py = __dsub_rn(__ddiv_rn((double)h, 2.0), __dadd_rn((double)row, 0.5));
+    const double scale = __dmul_rn(__ddiv_rn((double)w, __dmul_rn(2.0, 2.4)), vis[11]);
+    return __dadd_rn(__ddiv_rn(py, scale), vis[10]);
+}
+
 // colour channel as drawn: np.asarray(color, uint8) truncates the float
 __device__ __forceinline__ uint8_t color_u8(double v) { return (uint8_t)(int)v; }
 
@@ -82,6 +130,59 @@ __device__ __forceinline__ double gray_of(const double *rgb, double bright) {
 // step) the terminal stack [h1, h2, term] is drawn with the old visuals into
 // term_out, the new episode's visuals are drawn from its stream, and the
 // observation is three copies of the new first frame.
+constexpr int kMaxView = 512;  // widest / tallest view the stack kernels stage in smem
+
+// 12 values at a 16-byte-aligned address (3 * 4 pixels * sizeof(T), row start
+// aligned because w % 4 == 0 and each world's image starts 16-byte aligned)
+__device__ __forceinline__ void store12(float *o, const float *v) {
+    float4 *d = reinterpret_cast<float4 *>(o);
+    d[0] = make_float4(v[0], v[1], v[2], v[3]);
+    d[1] = make_float4(v[4], v[5], v[6], v[7]);
+    d[2] = make_float4(v[8], v[9], v[10], v[11]);
+}
+__device__ __forceinline__ void store12(double *o, const double *v) {
+    double2 *d = reinterpret_cast<double2 *>(o);
+#pragma unroll
+    for (int k = 0; k < 6; ++k) d[k] = make_double2(v[2 * k], v[2 * k + 1]);
+}
+
+template <typename T>
+__device__ __forceinline__ void draw_stack(int w, int h, double pole_len, const double *v,
+                                           const PixFrame *fr, double *g, double *wxs,
+                                           double *wys, PoleSeg *ps, T *o) {
+    for (int c = threadIdx.x; c < w; c += blockDim.x) wxs[c] = view_wx(v, w, c);
+    for (int r = threadIdx.x; r < h; r += blockDim.x) wys[r] = view_wy(v, w, h, r);
+    if (threadIdx.x < 3) {
+        g[threadIdx.x] = gray_of(v + 3 * threadIdx.x, v[12]);
+        ps[threadIdx.x] = pole_seg(fr[threadIdx.x], pole_len);
+    }
+    __syncthreads();
+    if ((w & 3) == 0) {
+        // four pixels of a row per thread: 12 consecutive values, stored as
+        // three 16-byte (float) or six 16-byte (double) vectors
+        for (int q = threadIdx.x; q < (w * h) >> 2; q += blockDim.x) {
+            const int p = q << 2, row = p / w, col = p - row * w;
+            const double wy = wys[row];
+            T vals[12];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    vals[3 * j + k] = (T)g[pix_class_pre(wxs[col + j], wy, ps[k])];
+            store12(o + 3 * p, vals);
+        }
+        return;
+    }
+    for (int p = threadIdx.x; p < w * h; p += blockDim.x) {
+        const int row = p / w, col = p - row * w;
+        const double wx = wxs[col], wy = wys[row];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) o[3 * p + k] = (T)g[pix_class_pre(wx, wy, ps[k])];
+    }
+}
+
+// One CTA per world: threads stride over the h*w pixels; each pixel's three
+// stacked frames (oldest first) are written as three consecutive values.
 template <typename T>
 __global__ void pixel_stack_kernel(int64_t n, int w, int h, double pole_len,
                                    const PixFrame *__restrict__ hist, const double *__restrict__ vis,
@@ -91,17 +192,12 @@ __global__ void pixel_stack_kernel(int64_t n, int w, int h, double pole_len,
     __shared__ double g[3];  // gray level of background / cart / pole
     __shared__ double v[kVis];
     __shared__ PixFrame fr[3];
+    __shared__ PoleSeg ps[3];
+    __shared__ double wxs[kMaxView], wys[kMaxView];
     if (threadIdx.x < kVis) v[threadIdx.x] = vis[i * kVis + threadIdx.x];
     if (threadIdx.x < 3) fr[threadIdx.x] = hist[i * 3 + threadIdx.x];
     __syncthreads();
-    if (threadIdx.x < 3) g[threadIdx.x] = gray_of(v + 3 * threadIdx.x, v[12]);
-    __syncthreads();
-    T *o = out + i * (int64_t)w * h * 3;
-    for (int p = threadIdx.x; p < w * h; p += blockDim.x) {
-        const int row = p / w, col = p - row * w;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) o[3 * p + k] = (T)g[pix_class(v, pole_len, w, h, row, col, fr[k])];
-    }
+    draw_stack<T>(w, h, pole_len, v, fr, g, wxs, wys, ps, out + i * (int64_t)w * h * 3);
 }
 
 // batch_render + brightness_postprocess: RGB uint8 [n, h, w, 3] of one frame.
@@ -207,20 +303,15 @@ __global__ void pixel_terminal_kernel(int64_t n, int w, int h, double pole_len, 
     __shared__ double g[3];
     __shared__ double v[kVis];
     __shared__ PixFrame fr[3];
+    __shared__ PoleSeg ps[3];
+    __shared__ double wxs[kMaxView], wys[kMaxView];
     if (threadIdx.x < kVis) v[threadIdx.x] = vis[i * kVis + threadIdx.x];
     if (threadIdx.x < 2) fr[threadIdx.x] = hist[i * 3 + 1 + threadIdx.x];
     if (threadIdx.x == 2)
         fr[2] = PixFrame{(double)term_obs[i * obs_dim], (double)term_obs[i * obs_dim + 1],
                          (double)term_obs[i * obs_dim + 2]};
     __syncthreads();
-    if (threadIdx.x < 3) g[threadIdx.x] = gray_of(v + 3 * threadIdx.x, v[12]);
-    __syncthreads();
-    T *o = out + i * (int64_t)w * h * 3;
-    for (int p = threadIdx.x; p < w * h; p += blockDim.x) {
-        const int row = p / w, col = p - row * w;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) o[3 * p + k] = (T)g[pix_class(v, pole_len, w, h, row, col, fr[k])];
-    }
+    draw_stack<T>(w, h, pole_len, v, fr, g, wxs, wys, ps, out + i * (int64_t)w * h * 3);
 }
 
 }  // namespace dk

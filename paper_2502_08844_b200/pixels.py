@@ -146,8 +146,8 @@ class PixelObservation:
         mask = step_out["terminal_mask"].to(torch.uint8).contiguous()
         term = None
         if terminal:
-            term = torch.zeros((self.n, self.size, self.size, 3), dtype=self.dtype,
-                               device=self.device)
+            term = torch.empty((self.n, self.size, self.size, 3), dtype=self.dtype,
+                               device=self.device)  # rows written where the mask is set
             t_obs = step_out["terminal_obs"].to(self.dtype).contiguous()
             _check(nat.lib().dk_pixels_terminal(
                 _dtype_code(term), self.n, self.size, self.size, self.pole_length,
