@@ -342,7 +342,10 @@ class _EnvView:
 
     def observation_shapes(self) -> dict:
         o = self.task.obs_dim
-        return {"state": (o,), "privileged_state": (o,)}
+        shapes = {"state": (o,), "privileged_state": (o,)}
+        if getattr(self.task, "pixels", False):
+            shapes["pixels"] = (self.task.image_size, self.task.image_size, 3)
+        return shapes
 
 
 class BatchEnv:
@@ -683,7 +686,10 @@ class Environment:
 
     def observation_shapes(self) -> dict:
         o = self.task.obs_dim
-        return {"state": (o,), "privileged_state": (o,)}
+        shapes = {"state": (o,), "privileged_state": (o,)}
+        if getattr(self.task, "pixels", False):
+            shapes["pixels"] = (self.task.image_size, self.task.image_size, 3)
+        return shapes
 
     def close(self):
         self._b.close()
