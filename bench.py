@@ -315,10 +315,11 @@ def run_b200(args, rank, world, local_rank, dist):
     tail = None
     if not args.no_tail:
         tail = bench_go1_tail(args, dev, rank)
-    dropin = sweep = ppo_rollout = pixels = None
+    dropin = sweep = ppo_rollout = pixels = tasks = None
     if rank == 0 and not args.no_extra:
         dropin = bench_dropin_step(args, dev)
         sweep = bench_sweep(args, dev)
+        tasks = bench_tasks(args, dev)
         ppo_rollout = bench_ppo_rollout(args, dev)
         pixels = bench_pixels(args, dev)
 
@@ -362,6 +363,7 @@ def run_b200(args, rank, world, local_rank, dist):
             "sweep": sweep,
             "ppo_rollout": ppo_rollout,
             "pixels": pixels,
+            "all_tasks": tasks,
             "clocks": clocks.summary(),
             "library": _native.LIB_PATH,
         }
@@ -519,6 +521,46 @@ def bench_sweep(args, dev, sizes=(1024, 8192, 65536), K=1000, launches=5):
         env.close()
         del acts, o
     return out
+
+
+def bench_tasks(args, dev, K=1000, launches=5, cpu_seconds=1.0):
+    """All four analytic tasks at the bench's world count,
+    f32 and f64, device-resident; with each task's CPU-port rate (oracle, all
+    host threads, ~1 s sample) beside it when CPU legs are enabled."""
+    import torch
+
+    import paper_2502_08844_b200 as dk
+
+    n = args.num_envs
+    peak, _ = hbm_peak()
+    out = {}
+    for task in ("cartpole-balance", "pendulum-swingup", "acrobot-swingup", "reacher-easy"):
+        row = {}
+        for dtype in ("float32", "float64"):
+            env = dk.DeviceBatchEnv(dk.EnvConfig(task=task), n, dtype=dtype, device=dev.index)
+            env.reset(seed=0)
+            esz = 8 if env.dtype == torch.float64 else 4
+            acts = torch.rand((K, n, env.action_dim), device=dev, dtype=env.dtype) * 2 - 1
+            o = env._outputs((K,), True)
+            env.rollout(acts, with_info=True, out=o)
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(launches):
+                env.rollout(acts, with_info=True, out=o)
+            b.record()
+            torch.cuda.synchronize(dev)
+            env.check()
+            rate = n * K * launches / (a.elapsed_time(b) / 1e3)
+            bpw = bytes_per_world_step(env.action_dim, env.obs_dim, len(env.info_keys), esz)
+            row[dtype] = {"value": rate, "frac": rate * bpw / 1e9 / peak}
+            env.close()
+            del acts, o
+        if not args.no_cpu:
+            rate, threads, _, _ = cpu_rate(task, n, cpu_seconds)
+            row["cpu_port"] = {"value": rate, "cores": threads}
+        out[task] = row
+    return {"unit": UNIT, "worlds": n, "tasks": out}
 
 
 def synthetic_frames(R, J, F, dev, dtype, seed):
