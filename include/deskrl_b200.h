@@ -34,7 +34,7 @@
 extern "C" {
 #endif
 
-#define DK_ABI_VERSION 4  /* 2: DR kinds / params / delays; 3: PPO math; 4: pixels */
+#define DK_ABI_VERSION 5  /* 2: DR kinds / params / delays; 3: PPO math; 4: pixels; 5: distributed normaliser */
 
 /* Status codes.  The Python host maps them to the reference's exception
  * classes: ConfigError (randomization.py:19), InvalidInputError
@@ -293,6 +293,15 @@ int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rew
  * count is the statistics' count before the update (the caller adds rows). */
 int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double count,
                    double *mean, double *var, void *stream);
+
+/* The two halves of normalizer_update for data-parallel ranks: column sums
+ * (or, with center [dim], sums of squared deviations) of the local batch in
+ * float64 -- all-reduce them across ranks -- then the reference's merge of
+ * the global batch mean / var (mathcore.py:245-251) into mean / var. */
+int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const double *center,
+                   double *sums, void *stream);
+int dk_norm_merge(int dim, double count, double batch_count, const double *batch_mean,
+                  const double *batch_var, double *mean, double *var, void *stream);
 
 /* normalizer_apply (mathcore.py:254-265) or, with invert, normalizer_invert
  * (268-272) of batch [rows, dim] into out (same dtype); count == 0 copies. */

@@ -143,6 +143,9 @@ _SIGS = {
                                   ctypes.c_double, _vp, _vp, _vp]),
     "dk_norm_update": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,
                                       _vp, _vp, _vp]),
+    "dk_norm_colsum": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+    "dk_norm_merge": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_double, _vp, _vp,
+                                     _vp, _vp, _vp]),
     "dk_norm_apply": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,
                                      _vp, _vp, ctypes.c_double, ctypes.c_int, _vp, _vp]),
 }

@@ -90,6 +90,44 @@ int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double c
     return norm_update<float>(rows, dim, (const float *)batch, count, mean, var, st);
 }
 
+int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const double *center,
+                   double *sums, void *stream) {
+    if (!batch || !sums)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer colsum: missing argument");
+    if (dim <= 0 || rows < 0)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer dim mismatch");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (rows == 0) return cuda_rc(cudaMemsetAsync(sums, 0, sizeof(double) * dim, st), "memset");
+    const int64_t lanes = pick_lanes(rows, dim);
+    double *partial = nullptr;
+    cudaError_t e = cudaMallocAsync((void **)&partial, sizeof(double) * lanes * dim, st);
+    if (e != cudaSuccess) return cuda_rc(e, "normalizer workspace");
+    const int64_t P = lanes * dim;
+    if (dtype == DK_F64)
+        dk::colsum_kernel<double><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes,
+                                                                 (const double *)batch, center,
+                                                                 partial);
+    else
+        dk::colsum_kernel<float><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes,
+                                                                (const float *)batch, center,
+                                                                partial);
+    // rows = 1: colreduce divides by it, so out = the plain column sums
+    dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, 1, partial, sums);
+    e = cudaGetLastError();
+    cudaFreeAsync(partial, st);
+    return cuda_rc(e, "normalizer colsum launch");
+}
+
+int dk_norm_merge(int dim, double count, double batch_count, const double *batch_mean,
+                  const double *batch_var, double *mean, double *var, void *stream) {
+    if (!batch_mean || !batch_var || !mean || !var)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer merge: missing argument");
+    if (dim <= 0) return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer dim mismatch");
+    dk::norm_merge_kernel<<<blocks(dim, 128), 128, 0, (cudaStream_t)stream>>>(
+        dim, count, batch_count, batch_mean, batch_var, mean, var);
+    return cuda_rc(cudaGetLastError(), "normalizer merge launch");
+}
+
 int dk_norm_apply(int dtype, int64_t rows, int dim, const void *batch, double count,
                   const double *mean, const double *var, double epsilon, int invert, void *out,
                   void *stream) {

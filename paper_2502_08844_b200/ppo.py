@@ -105,13 +105,40 @@ class DeviceRunningNormalizer:
                 f"normalizer dim mismatch: expected {self.dim}, got {b.shape[-1]}")
         return b.reshape(-1, self.dim).contiguous()
 
-    def update(self, batch):
-        """normalizer_update: merge the rows of ``batch`` (float32/64 CUDA tensor)."""
+    def update(self, batch, dist=None, group=None):
+        """normalizer_update: merge the rows of ``batch`` (float32/64 CUDA tensor).
+
+        With an initialised ``torch.distributed`` (``dist``) of several ranks,
+        the merged batch is the concatenation of every rank's rows, as if one
+        process had called normalizer_update on all of them (the
+        rollout-statistic reduction): column sums, then squared deviations
+        from the global mean, are all-reduced (NCCL between GPUs) and every
+        rank applies the same merge.  Tree / rank summation order: 1e-13."""
+        torch = _torch()
         b = self._rows(batch)
         rows = b.shape[0]
-        _check(nat.lib().dk_norm_update(_dtype_code(b), rows, self.dim, _ptr(b), self.count,
-                                        _ptr(self.mean), _ptr(self.var), _stream(b.device)))
-        self.count += rows
+        st = _stream(b.device)
+        if dist is None or not dist.is_initialized() or dist.get_world_size(group) == 1:
+            _check(nat.lib().dk_norm_update(_dtype_code(b), rows, self.dim, _ptr(b), self.count,
+                                            _ptr(self.mean), _ptr(self.var), st))
+            self.count += rows
+            return self
+        lib = nat.lib()
+        n = torch.tensor([float(rows)], dtype=torch.float64, device=b.device)
+        dist.all_reduce(n, group=group)
+        total = float(n.item())
+        sums = torch.empty(self.dim, dtype=torch.float64, device=b.device)
+        _check(lib.dk_norm_colsum(_dtype_code(b), rows, self.dim, _ptr(b), None, _ptr(sums), st))
+        dist.all_reduce(sums, group=group)
+        b_mean = sums / total
+        sq = torch.empty_like(sums)
+        _check(lib.dk_norm_colsum(_dtype_code(b), rows, self.dim, _ptr(b), _ptr(b_mean),
+                                  _ptr(sq), st))
+        dist.all_reduce(sq, group=group)
+        b_var = sq / total
+        _check(lib.dk_norm_merge(self.dim, self.count, total, _ptr(b_mean), _ptr(b_var),
+                                 _ptr(self.mean), _ptr(self.var), st))
+        self.count += total
         return self
 
     def _apply(self, batch, invert):
