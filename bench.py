@@ -198,6 +198,29 @@ def cpu_model():
 # ---------------------------------------------------------------------------
 
 
+TASK_DIMS = {"cartpole-balance": (1, 5, 3), "pendulum-swingup": (1, 3, 1),
+             "acrobot-swingup": (1, 6, 1), "reacher-easy": (2, 10, 1)}  # (A, O, info terms)
+
+
+def headline_config(args, world):
+    """The `config` object of the headline line, shared by both arms."""
+    A, O, I = TASK_DIMS[args.task]
+    esz = 8 if args.dtype == "float64" else 4
+    U = min(args.unroll, args.steps)
+    R = max(2, args.ring)
+    bpw = bytes_per_world_step(A, O, I, esz)
+    return {
+        "workload": f"{args.task} BatchEnv.step (dynamics, reward + info terms, obs, "
+                    "truncation, Philox autoreset), episode_length 1000; BASELINE's Go1 "
+                    "joystick physics does not exist in the reference (SURVEY.md §0)",
+        "task": args.task, "worlds_per_gpu": args.num_envs,
+        "global_worlds": args.num_envs * world, "steps_per_launch": U,
+        "parallelism": f"worlds sharded dp{world}",
+        "l2": f"flushed before the timed region; {R}-chunk ring of "
+              f"{U * args.num_envs * (bpw + A * esz) / 1e6:.0f} MB chunks > 126 MB L2",
+    }
+
+
 def run_reference(args, rank):
     if rank != 0:
         return
@@ -214,9 +237,7 @@ def run_reference(args, rank):
         "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
         "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic U(-1,1) actions",
-        "config": {"workload": f"{args.task} BatchEnv.step, {args.num_envs} worlds, autoreset, "
-                               "episode_length 1000, reward info terms", "num_envs": args.num_envs,
-                   "task": args.task},
+        "config": headline_config(args, args.gpus),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": f"{steps} steps x {args.num_envs} worlds on {cores} threads "
                                    f"({cpu_model()}); oracle/oracle.c, the bit-exact C "
@@ -341,15 +362,7 @@ def run_b200(args, rank, world, local_rank, dist):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if esz == 4 else "f64",
             "data": "synthetic U(-1,1) actions pre-generated in HBM",
-            "config": {
-                "workload": f"{args.task} BatchEnv.step (dynamics, reward + info terms, obs, "
-                            "truncation, Philox autoreset), episode_length 1000; BASELINE's Go1 "
-                            "joystick physics does not exist in the reference (SURVEY.md §0)",
-                "task": args.task, "worlds_per_gpu": n, "global_worlds": n * world,
-                "steps_per_launch": U, "parallelism": f"worlds sharded dp{world}",
-                "l2": f"flushed before the timed region; {R}-chunk ring of "
-                      f"{U * n * (bpw + A * esz) / 1e6:.0f} MB chunks > 126 MB L2",
-            },
+            "config": headline_config(args, world),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "traffic": ncu_traffic(args.task, args.dtype, n, U),
