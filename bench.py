@@ -209,6 +209,13 @@ def headline_config(args, world):
     U = min(args.unroll, args.steps)
     R = max(2, args.ring)
     bpw = bytes_per_world_step(A, O, I, esz)
+    chunk_mb = U * args.num_envs * (bpw + A * esz) / 1e6
+    nlaunch = -(-args.steps // U)
+    if nlaunch == 1:
+        l2_note = "flushed before the timed region (a single launch)"
+    else:
+        l2_note = (f"flushed before the timed region; {R}-chunk ring of {chunk_mb:.0f} MB "
+                   f"chunks ({'>' if chunk_mb * min(R, nlaunch) > 126 else '<'} 126 MB L2)")
     return {
         "workload": f"{args.task} BatchEnv.step (dynamics, reward + info terms, obs, "
                     "truncation, Philox autoreset), episode_length 1000; BASELINE's Go1 "
@@ -216,8 +223,7 @@ def headline_config(args, world):
         "task": args.task, "worlds_per_gpu": args.num_envs,
         "global_worlds": args.num_envs * world, "steps_per_launch": U,
         "parallelism": f"worlds sharded dp{world}",
-        "l2": f"flushed before the timed region; {R}-chunk ring of "
-              f"{U * args.num_envs * (bpw + A * esz) / 1e6:.0f} MB chunks > 126 MB L2",
+        "l2": l2_note,
     }
 
 
