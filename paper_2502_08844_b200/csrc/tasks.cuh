@@ -221,12 +221,25 @@ __device__ __forceinline__ void twolink_advance(TwoLinkW<T> &w, T tau1, T tau2, 
     const T rhs1 = tau1 - cor1 - g1 - p.link_damping * d1;
     const T rhs2 = tau2 - cor2 - g2 - p.link_damping * d2;
     const T det = m11 * m22 - m12 * m12;
-    const T a1 = RealOps<T>::div_(m22 * rhs1 - m12 * rhs2, det);
-    const T a2 = RealOps<T>::div_(m11 * rhs2 - m12 * rhs1, det);
-    w.d1 = d1 + p.dt * a1;
-    w.d2 = d2 + p.dt * a2;
-    w.t1 = w.t1 + p.dt * w.d1;
-    w.t2 = w.t2 + p.dt * w.d2;
+    if constexpr (std::is_same<T, float>::value) {
+        // f32 (tolerance-checked): one reciprocal; angles folded as
+        // t + dt d + dt^2 a so one FFMA follows the reciprocal (as cartpole)
+        const float rdet = RealOps<float>::div_(1.0f, det);
+        const float n1 = m22 * rhs1 - m12 * rhs2, n2 = m11 * rhs2 - m12 * rhs1;
+        const float dt = p.dt, dt2 = dt * dt;
+        const float t1b = fmaf(dt, d1, w.t1), t2b = fmaf(dt, d2, w.t2);
+        w.d1 = fmaf(dt * n1, rdet, d1);
+        w.d2 = fmaf(dt * n2, rdet, d2);
+        w.t1 = fmaf(dt2 * n1, rdet, t1b);
+        w.t2 = fmaf(dt2 * n2, rdet, t2b);
+    } else {
+        const T a1 = RealOps<T>::div_(m22 * rhs1 - m12 * rhs2, det);
+        const T a2 = RealOps<T>::div_(m11 * rhs2 - m12 * rhs1, det);
+        w.d1 = d1 + p.dt * a1;
+        w.d2 = d2 + p.dt * a2;
+        w.t1 = w.t1 + p.dt * w.d1;
+        w.t2 = w.t2 + p.dt * w.d2;
+    }
     twolink_refresh(w);
 }
 
