@@ -1,21 +1,26 @@
 // envstep_kernels.cuh -- fused batched env step / rollout kernels.
 //
-// One thread owns one world for the whole launch: the state is read from HBM
-// once, advanced K control steps in registers (dynamics -> reward -> obs ->
+// One CTA owns a tile of 32 worlds for the whole launch: the state is read
+// from HBM once, advanced K control steps on chip (dynamics -> reward -> obs ->
 // truncation -> Philox autoreset, the whole of Environment.step +
 // BatchEnv.step's autoreset, envkit.py:526-552, 630-635), and written back
 // once.  Per step the only HBM traffic is the algorithmic I/O: the action in,
 // obs / reward / done / trunc (and optionally the info terms) out.
 //
-//  - Warp-specialised: a producer warp runs the serial dynamics chain of 32
-//    worlds, consumer warps turn its ring of states into outputs (below).
-//  - Actions are prefetched CH steps ahead into registers (double-buffered
-//    chunks), so the dependent chain of the dynamics never waits on HBM.
-//  - Validation is fused and batch-atomic: each world checks its own actions
-//    as it consumes them (and knows up front at which step it would need a
-//    reset); the first error in reference order (step-major, then world) is
-//    kept in a sticky key, and the state buffers are double-buffered so the
-//    launch commits only when the whole batch was valid.
+//  - Warp-specialised (rollout_kernel below): a stager warp streams and
+//    validates actions through a cp.async ring, a producer warp runs only the
+//    serial dynamics chain of the 32 worlds, consumer warps turn its ring of
+//    post-step states into rewards, observations and every global store.
+//  - Validation is fused and batch-atomic: the stager checks each action as it
+//    stages it (and knows up front at which step a world would need a reset);
+//    the first error in reference order (step-major, then world) is kept in a
+//    sticky key, and the state buffers are double-buffered so the launch
+//    commits only when the whole batch was valid.
+//
+// Development hooks (off in the product build; tools/exp_variants.sh builds
+// them as separate libraries): DK_EXP_CLOCK (%globaltimer / %clock64 timeline
+// printed per launch), DK_EXP_NO_STAGER / DK_EXP_NO_CONSUMER (drop a role's
+// work to measure its share), DK_EXP_EARLY_TRIGGER (PDL trigger at kernel start).
 #pragma once
 #include <type_traits>
 #include <cstdio>
