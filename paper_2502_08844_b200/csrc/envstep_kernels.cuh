@@ -765,6 +765,7 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
         // per-step strides, hoisted (the compiler otherwise re-derives the
         // 64-bit products from the constant bank every step)
         const int64_t step_obs = n * O, step_info = n * I;
+        const bool idx32 = (int64_t)K32 * n * (O > I ? O : I) < (int64_t)1 << 31;
         auto run_tile = [&](auto full_c, auto fast_c, int t, int g, const T *ring_g,
                             const T *rp_g, const uint8_t *fl_g) {
             constexpr bool FULL = decltype(full_c)::value;
@@ -775,6 +776,39 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             const bool in_range = i < n;
             const int kend = min(G, K32 - g * G);
             const int64_t kb = (int64_t)g * G * n;  // element row of step g*G
+            // fast full tiles of the wider-observation tasks: a 32-bit element
+            // index with each store address one IMAD.WIDE, instead of six 64-bit
+            // pointer streams (+2-3% for cartpole / acrobot / reacher; the
+            // 3-value pendulum row measured 3% slower, so it keeps the pointers)
+            if constexpr (FAST && FULL && O >= 5) {
+                if (idx32) {
+                    uint32_t e = (uint32_t)(kb + i);
+#pragma unroll 1
+                    for (int s = 0; s < kend; ++s) {
+                        typename Task::W wd;
+                        slot_to_world<Task, T, WPC>(wd, ring_g + s * WF * WPC, col);
+                        T info[I];
+                        const T r = R1 ? (T(0) + Task::reward(wd, p, info))
+                                       : (rp_g[s * WPC + col] + Task::reward(wd, p, info)) / inv_rep;
+                        T o[O];
+                        Task::obs(wd, p, o);
+                        T *ob = out.obs + (uint64_t)e * O;
+#pragma unroll
+                        for (int j = 0; j < O; ++j) ob[j] = o[j];
+                        if (has_info) {
+                            T *ib = out.info + (uint64_t)e * I;
+#pragma unroll
+                            for (int j = 0; j < I; ++j) ib[j] = info[j];
+                        }
+                        out.reward[e] = r;
+                        out.done[e] = 0;
+                        out.trunc[e] = 0;
+                        if (has_mask) out.term_mask[e] = 0;
+                        e += (uint32_t)n;
+                    }
+                    return;
+                }
+            }
             T *obs_p = out.obs + (kb + row0) * O;
             T *info_p = has_info ? out.info + (kb + row0) * I : nullptr;
             T *rew_p = out.reward + kb + i;
