@@ -69,3 +69,26 @@ def test_device_step_is_cuda_graph_capturable():
     s1, *_ = graphed.state()
     s2, *_ = eager.state()
     np.testing.assert_array_equal(s1, s2)
+
+
+def test_no_leak_over_create_close_cycles():
+    """no leaks over 10^3 create / close cycles of
+    the bindings handle (device memory and pinned host staging)."""
+    import torch
+
+    import paper_2502_08844_b200 as dk
+
+    def cycle(k):
+        for _ in range(k):
+            env = dk.BatchEnv(dk.EnvConfig(task="cartpole-balance"), 64)
+            env.reset(seed=1)
+            env.step(np.zeros((64, 1)))
+            env.close()
+
+    cycle(20)
+    torch.cuda.synchronize()
+    free0, _ = torch.cuda.mem_get_info()
+    cycle(1000)
+    torch.cuda.synchronize()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < 4 * 1024 * 1024, (free0, free1)
