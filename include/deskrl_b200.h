@@ -28,13 +28,14 @@
 #ifndef DESKRL_B200_H
 #define DESKRL_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
 extern "C" {
 #endif
 
-#define DK_ABI_VERSION 5  /* 2: DR kinds / params / delays; 3: PPO math; 4: pixels; 5: distributed normaliser */
+#define DK_ABI_VERSION 6  /* 2: DR kinds / params / delays; 3: PPO math; 4: pixels; 5-6: normaliser halves, workspace */
 
 /* Status codes.  The Python host maps them to the reference's exception
  * classes: ConfigError (randomization.py:19), InvalidInputError
@@ -292,14 +293,18 @@ int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rew
  * running statistics mean / var (device float64 [dim], updated in place);
  * count is the statistics' count before the update (the caller adds rows). */
 int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double count,
-                   double *mean, double *var, void *stream);
+                   double *mean, double *var, void *workspace, size_t workspace_bytes,
+                   void *stream);
+/* Device scratch dk_norm_update / dk_norm_colsum use for [rows, dim]; a
+ * smaller (or NULL) workspace makes them allocate stream-ordered scratch. */
+size_t dk_norm_workspace_bytes(int64_t rows, int dim);
 
 /* The two halves of normalizer_update for data-parallel ranks: column sums
  * (or, with center [dim], sums of squared deviations) of the local batch in
  * float64 -- all-reduce them across ranks -- then the reference's merge of
  * the global batch mean / var (mathcore.py:245-251) into mean / var. */
 int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const double *center,
-                   double *sums, void *stream);
+                   double *sums, void *workspace, size_t workspace_bytes, void *stream);
 int dk_norm_merge(int dim, double count, double batch_count, const double *batch_mean,
                   const double *batch_var, double *mean, double *var, void *stream);
 

@@ -142,8 +142,10 @@ _SIGS = {
     "dk_ppo_gae": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_double,
                                   ctypes.c_double, _vp, _vp, _vp]),
     "dk_norm_update": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,
-                                      _vp, _vp, _vp]),
-    "dk_norm_colsum": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]),
+                                      _vp, _vp, _vp, ctypes.c_size_t, _vp]),
+    "dk_norm_workspace_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int]),
+    "dk_norm_colsum": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, _vp, _vp, _vp,
+                                      ctypes.c_size_t, _vp]),
     "dk_norm_merge": (ctypes.c_int, [ctypes.c_int, ctypes.c_double, ctypes.c_double, _vp, _vp,
                                      _vp, _vp, _vp]),
     "dk_norm_apply": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,

@@ -28,15 +28,37 @@ int64_t pick_lanes(int64_t rows, int dim) {
     return lanes < 1 ? 1 : lanes;
 }
 
+size_t ws_bytes(int64_t rows, int dim) {
+    return sizeof(double) * ((size_t)pick_lanes(rows, dim) * dim + 2 * (size_t)dim);
+}
+
+// caller workspace (>= ws_bytes) or a stream-ordered allocation
+struct Workspace {
+    double *p = nullptr;
+    bool owned = false;
+    cudaStream_t st;
+    cudaError_t init(void *ws, size_t ws_size, size_t need, cudaStream_t s) {
+        st = s;
+        if (ws && ws_size >= need) {
+            p = (double *)ws;
+            return cudaSuccess;
+        }
+        owned = true;
+        return cudaMallocAsync((void **)&p, need, st);
+    }
+    ~Workspace() {
+        if (owned && p) cudaFreeAsync(p, st);
+    }
+};
+
 template <typename T>
 int norm_update(int64_t rows, int dim, const T *batch, double count, double *mean, double *var,
-                cudaStream_t st) {
+                void *ws, size_t ws_size, cudaStream_t st) {
     const int64_t lanes = pick_lanes(rows, dim);
-    double *partial = nullptr, *bstat = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&partial, sizeof(double) * lanes * dim, st);
-    if (e == cudaSuccess) e = cudaMallocAsync((void **)&bstat, sizeof(double) * 2 * dim, st);
+    Workspace w;
+    cudaError_t e = w.init(ws, ws_size, ws_bytes(rows, dim), st);
     if (e != cudaSuccess) return cuda_rc(e, "normalizer workspace");
-    double *b_mean = bstat, *b_var = bstat + dim;
+    double *partial = w.p, *b_mean = w.p + lanes * dim, *b_var = b_mean + dim;
     const int64_t P = lanes * dim;
     dk::colsum_kernel<T><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes, batch, nullptr, partial);
     dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, rows, partial, b_mean);
@@ -44,10 +66,7 @@ int norm_update(int64_t rows, int dim, const T *batch, double count, double *mea
     dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, rows, partial, b_var);
     dk::norm_merge_kernel<<<blocks(dim, 128), 128, 0, st>>>(dim, count, (double)rows, b_mean,
                                                            b_var, mean, var);
-    e = cudaGetLastError();
-    cudaFreeAsync(partial, st);
-    cudaFreeAsync(bstat, st);
-    return cuda_rc(e, "normalizer update launch");
+    return cuda_rc(cudaGetLastError(), "normalizer update launch");
 }
 
 }  // namespace
@@ -77,8 +96,13 @@ int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rew
     return cuda_rc(cudaGetLastError(), "gae launch");
 }
 
+size_t dk_norm_workspace_bytes(int64_t rows, int dim) {
+    return rows > 0 && dim > 0 ? ws_bytes(rows, dim) : 0;
+}
+
 int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double count,
-                   double *mean, double *var, void *stream) {
+                   double *mean, double *var, void *workspace, size_t workspace_bytes,
+                   void *stream) {
     if (!batch || !mean || !var)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer_update: missing argument");
     if (dim <= 0 || rows < 0)
@@ -86,12 +110,14 @@ int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double c
     if (rows == 0) return DK_OK;  // (NumPy: mean of an empty batch is NaN; callers pass rows)
     cudaStream_t st = (cudaStream_t)stream;
     if (dtype == DK_F64)
-        return norm_update<double>(rows, dim, (const double *)batch, count, mean, var, st);
-    return norm_update<float>(rows, dim, (const float *)batch, count, mean, var, st);
+        return norm_update<double>(rows, dim, (const double *)batch, count, mean, var, workspace,
+                                   workspace_bytes, st);
+    return norm_update<float>(rows, dim, (const float *)batch, count, mean, var, workspace,
+                              workspace_bytes, st);
 }
 
 int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const double *center,
-                   double *sums, void *stream) {
+                   double *sums, void *workspace, size_t workspace_bytes, void *stream) {
     if (!batch || !sums)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer colsum: missing argument");
     if (dim <= 0 || rows < 0)
@@ -99,9 +125,10 @@ int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const do
     cudaStream_t st = (cudaStream_t)stream;
     if (rows == 0) return cuda_rc(cudaMemsetAsync(sums, 0, sizeof(double) * dim, st), "memset");
     const int64_t lanes = pick_lanes(rows, dim);
-    double *partial = nullptr;
-    cudaError_t e = cudaMallocAsync((void **)&partial, sizeof(double) * lanes * dim, st);
+    Workspace w;
+    cudaError_t e = w.init(workspace, workspace_bytes, ws_bytes(rows, dim), st);
     if (e != cudaSuccess) return cuda_rc(e, "normalizer workspace");
+    double *partial = w.p;
     const int64_t P = lanes * dim;
     if (dtype == DK_F64)
         dk::colsum_kernel<double><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes,
@@ -113,9 +140,7 @@ int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const do
                                                                 partial);
     // rows = 1: colreduce divides by it, so out = the plain column sums
     dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, 1, partial, sums);
-    e = cudaGetLastError();
-    cudaFreeAsync(partial, st);
-    return cuda_rc(e, "normalizer colsum launch");
+    return cuda_rc(cudaGetLastError(), "normalizer colsum launch");
 }
 
 int dk_norm_merge(int dim, double count, double batch_count, const double *batch_mean,

@@ -184,7 +184,7 @@ __device__ __forceinline__ void draw_stack(int w, int h, double pole_len, const 
 // One CTA per world: threads stride over the h*w pixels; each pixel's three
 // stacked frames (oldest first) are written as three consecutive values.
 template <typename T>
-__global__ void pixel_stack_kernel(int64_t n, int w, int h, double pole_len,
+__global__ void __launch_bounds__(256, 4) pixel_stack_kernel(int64_t n, int w, int h, double pole_len,
                                    const PixFrame *__restrict__ hist, const double *__restrict__ vis,
                                    T *__restrict__ out) {
     const int64_t i = blockIdx.x;

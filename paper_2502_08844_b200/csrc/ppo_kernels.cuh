@@ -33,15 +33,48 @@ __global__ void gae_kernel(int64_t Tn, int64_t n, const T *__restrict__ rewards,
     const double gl = __dmul_rn(gamma, lam);  // gamma * lam * nonterm * last: left to right
     double next_v = to_f64(bootstrap[i]);
     double last = 0.0;
-    for (int64_t t = Tn - 1; t >= 0; --t) {
-        const int64_t e = t * n + i;
-        const double r = to_f64(rewards[e]), v = to_f64(values[e]), d = to_f64(dones[e]);
+    auto step = [&](int64_t e, double r, double v, double d) {
         const double nonterm = __dsub_rn(1.0, d);
         const double delta = __dsub_rn(__dadd_rn(r, __dmul_rn(__dmul_rn(gamma, nonterm), next_v)), v);
         last = __dadd_rn(delta, __dmul_rn(__dmul_rn(gl, nonterm), last));
         adv[e] = (T)last;
         ret[e] = (T)__dadd_rn(last, v);  // advantages + values
         next_v = v;
+    };
+    // CH time steps of loads in flight per thread before the serial recurrence
+    // consumes them (one world per thread leaves few warps per SM: without
+    // this, every step waited a full DRAM round trip)
+    // ... double-buffered (two register buffers with static indices, so nothing
+    // spills to local memory): the next chunk's loads are issued before this
+    // chunk's recurrence runs
+    constexpr int CH = 16;
+    int64_t t = Tn - 1;
+    T ra[CH], va[CH], da[CH], rb[CH], vb[CH], db[CH];
+    auto load = [&](T *r, T *v, T *d, int64_t t0) {
+#pragma unroll
+        for (int k = 0; k < CH; ++k) {
+            const int64_t e = (t0 - k) * n + i;
+            r[k] = rewards[e]; v[k] = values[e]; d[k] = dones[e];
+        }
+    };
+    auto run = [&](const T *r, const T *v, const T *d, int64_t t0) {
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+            step((t0 - k) * n + i, to_f64(r[k]), to_f64(v[k]), to_f64(d[k]));
+    };
+    if (t + 1 >= CH) load(ra, va, da, t);
+    while (t + 1 >= CH) {
+        if (t + 1 >= 2 * CH) load(rb, vb, db, t - CH);
+        run(ra, va, da, t);
+        t -= CH;
+        if (t + 1 < CH) break;
+        if (t + 1 >= 2 * CH) load(ra, va, da, t - CH);
+        run(rb, vb, db, t);
+        t -= CH;
+    }
+    for (; t >= 0; --t) {
+        const int64_t e = t * n + i;
+        step(e, to_f64(rewards[e]), to_f64(values[e]), to_f64(dones[e]));
     }
 }
 
@@ -59,7 +92,8 @@ __global__ void colsum_kernel(int64_t rows, int dim, int64_t lanes, const T *__r
     const int j = (int)(k - l * dim);
     const double c = center ? center[j] : 0.0;
     double s = 0.0;
-    for (int64_t r = l; r < rows; r += lanes) {
+#pragma unroll 8
+    for (int64_t r = l; r < rows; r += lanes) {  // (loads run ahead; the sum stays in order)
         const double x = to_f64(batch[r * dim + j]);
         if (center) {
             const double d = __dsub_rn(x, c);

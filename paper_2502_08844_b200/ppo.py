@@ -118,22 +118,26 @@ class DeviceRunningNormalizer:
         b = self._rows(batch)
         rows = b.shape[0]
         st = _stream(b.device)
+        lib = nat.lib()
+        # scratch from torch's caching allocator (stream-ordered, reused)
+        wsb = int(lib.dk_norm_workspace_bytes(rows, self.dim))
+        ws = torch.empty(max(wsb, 8), dtype=torch.uint8, device=b.device)
         if dist is None or not dist.is_initialized() or dist.get_world_size(group) == 1:
-            _check(nat.lib().dk_norm_update(_dtype_code(b), rows, self.dim, _ptr(b), self.count,
-                                            _ptr(self.mean), _ptr(self.var), st))
+            _check(lib.dk_norm_update(_dtype_code(b), rows, self.dim, _ptr(b), self.count,
+                                      _ptr(self.mean), _ptr(self.var), _ptr(ws), wsb, st))
             self.count += rows
             return self
-        lib = nat.lib()
         n = torch.tensor([float(rows)], dtype=torch.float64, device=b.device)
         dist.all_reduce(n, group=group)
         total = float(n.item())
         sums = torch.empty(self.dim, dtype=torch.float64, device=b.device)
-        _check(lib.dk_norm_colsum(_dtype_code(b), rows, self.dim, _ptr(b), None, _ptr(sums), st))
+        _check(lib.dk_norm_colsum(_dtype_code(b), rows, self.dim, _ptr(b), None, _ptr(sums),
+                                  _ptr(ws), wsb, st))
         dist.all_reduce(sums, group=group)
         b_mean = sums / total
         sq = torch.empty_like(sums)
         _check(lib.dk_norm_colsum(_dtype_code(b), rows, self.dim, _ptr(b), _ptr(b_mean),
-                                  _ptr(sq), st))
+                                  _ptr(sq), _ptr(ws), wsb, st))
         dist.all_reduce(sq, group=group)
         b_var = sq / total
         _check(lib.dk_norm_merge(self.dim, self.count, total, _ptr(b_mean), _ptr(b_var),
