@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define DK_ABI_VERSION 6  /* 2: DR kinds / params / delays; 3: PPO math; 4: pixels; 5-6: normaliser halves, workspace */
+#define DK_ABI_VERSION 7  /* 2: DR kinds / params / delays; 3: PPO math; 4: pixels; 5-6: normaliser halves, workspace; 7: pixel_normalize */
 
 /* Status codes.  The Python host maps them to the reference's exception
  * classes: ConfigError (randomization.py:19), InvalidInputError
@@ -351,6 +351,14 @@ int dk_pixels_stack(int dtype, int64_t n, int w, int h, double pole_length,
 int dk_pixels_terminal(int dtype, int64_t n, int w, int h, double pole_length, int obs_dim,
                        const void *term_obs, const uint8_t *mask, const double *history,
                        const double *visuals, void *out, void *stream);
+
+/* ppo.pixel_normalize (ppo.py:232-238): per-sample, per-channel
+ * standardisation of x [n, h, w, c] (in_dtype) into out (out_dtype), laid out
+ * [n, h, w, c] or, with channels_first, [n, c, h, w]; stats: device float64
+ * scratch [n, c, 2] (receives mean, std). */
+int dk_pixels_normalize(int in_dtype, int out_dtype, int64_t n, int h, int w, int c,
+                        const void *x, int channels_first, double *stats, void *out,
+                        void *stream);
 
 int dk_abi_version(void);
 const char *dk_last_error(void);

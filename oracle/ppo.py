@@ -1,6 +1,7 @@
 """ctypes wrappers of oracle/ppo.c (TEST INFRASTRUCTURE ONLY: tests, smoke, bench).
 
-compute_gae (ppo.py:80-102) and the RunningNormalizer update / apply / invert
+compute_gae (ppo.py:80-102), pixel_normalize (ppo.py:232-238) and the
+RunningNormalizer update / apply / invert
 (mathcore.py:234-272) restated in float64."""
 import ctypes
 
@@ -44,4 +45,13 @@ def norm_apply(count, mean, var, eps, batch, invert=False):
     out = np.zeros_like(x)
     _lib().orc_norm_apply(ctypes.c_int64(x.size // D), D, _vp(x), ctypes.c_double(count), _vp(m),
                           _vp(v), ctypes.c_double(eps), int(invert), _vp(out))
+    return out
+
+
+def pixel_normalize(img):
+    """ppo.pixel_normalize on [n, h, w, c]: float64 [n, h, w, c]."""
+    x = np.ascontiguousarray(img, dtype=np.float64)
+    n, h, w, c = x.shape
+    out = np.zeros_like(x)
+    _lib().orc_pixel_normalize(ctypes.c_int64(n), ctypes.c_int64(h * w), c, _vp(x), _vp(out))
     return out

@@ -104,4 +104,65 @@ int dk_pixels_terminal(int dtype, int64_t n, int w, int h, double pole_length, i
     return cuda_rc(cudaGetLastError(), "pixels terminal launch");
 }
 
+int dk_pixels_normalize(int in_dtype, int out_dtype, int64_t n, int h, int w, int c,
+                        const void *x, int channels_first, double *stats, void *out,
+                        void *stream) {
+    if (int rc = check_view(w, h)) return rc;
+    if (c <= 0 || n < 0) return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixel_normalize: shape");
+    if (n == 0) return DK_OK;
+    if (!x || !stats || !out)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixel_normalize: missing argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const int hw = h * w;
+    const unsigned gs = (unsigned)((n * c + 127) / 128);
+    if (in_dtype == DK_F32 && c == 3 && hw % dk::pixnorm::PN == 0 && ((uintptr_t)x & 15) == 0 &&
+        ((uintptr_t)out & 15) == 0) {
+        static unsigned long long attr_set = 0;  // per device (bit = ordinal)
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev >= 64 || !((attr_set >> dev) & 1ull)) {
+            cudaError_t e = cudaFuncSetAttribute(dk::pixnorm_stats3_kernel,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 dk::pixnorm::SMEM);
+            if (e != cudaSuccess) return cuda_rc(e, "pixel_normalize attribute");
+            if (dev < 64) __atomic_fetch_or(&attr_set, 1ull << dev, __ATOMIC_RELAXED);
+        }
+        dk::pixnorm_stats3_kernel<<<(unsigned)((n + 31) / 32), 32, dk::pixnorm::SMEM, st>>>(
+            n, hw, (const float *)x, stats);
+        const dim3 g((unsigned)((hw / 4 + 255) / 256), (unsigned)(n < 65535 ? n : 65535));
+        const float *xf = (const float *)x;
+        if (out_dtype == DK_F64) {
+            if (channels_first)
+                dk::pixnorm_apply3_kernel<double, true><<<g, 256, 0, st>>>(n, hw, xf, stats, (double *)out);
+            else
+                dk::pixnorm_apply3_kernel<double, false><<<g, 256, 0, st>>>(n, hw, xf, stats, (double *)out);
+        } else {
+            if (channels_first)
+                dk::pixnorm_apply3_kernel<float, true><<<g, 256, 0, st>>>(n, hw, xf, stats, (float *)out);
+            else
+                dk::pixnorm_apply3_kernel<float, false><<<g, 256, 0, st>>>(n, hw, xf, stats, (float *)out);
+        }
+        return cuda_rc(cudaGetLastError(), "pixel_normalize launch");
+    }
+    if (in_dtype == DK_F64)
+        dk::pixnorm_stats_kernel<double><<<gs, 128, 0, st>>>(n, hw, c, (const double *)x, stats);
+    else
+        dk::pixnorm_stats_kernel<float><<<gs, 128, 0, st>>>(n, hw, c, (const float *)x, stats);
+    const int64_t total = n * (int64_t)hw * c;
+    const unsigned ga = (unsigned)((total + 255) / 256);
+    if (in_dtype == DK_F64 && out_dtype == DK_F64)
+        dk::pixnorm_apply_kernel<double, double><<<ga, 256, 0, st>>>(
+            n, hw, c, (const double *)x, stats, channels_first, (double *)out);
+    else if (in_dtype == DK_F64)
+        dk::pixnorm_apply_kernel<double, float><<<ga, 256, 0, st>>>(
+            n, hw, c, (const double *)x, stats, channels_first, (float *)out);
+    else if (out_dtype == DK_F64)
+        dk::pixnorm_apply_kernel<float, double><<<ga, 256, 0, st>>>(
+            n, hw, c, (const float *)x, stats, channels_first, (double *)out);
+    else
+        dk::pixnorm_apply_kernel<float, float><<<ga, 256, 0, st>>>(
+            n, hw, c, (const float *)x, stats, channels_first, (float *)out);
+    return cuda_rc(cudaGetLastError(), "pixel_normalize launch");
+}
+
 }  // extern "C"

@@ -314,4 +314,249 @@ __global__ void pixel_terminal_kernel(int64_t n, int w, int h, double pole_len, 
     draw_stack<T>(w, h, pole_len, v, fr, g, wxs, wys, ps, out + i * (int64_t)w * h * 3);
 }
 
+// ppo.pixel_normalize (ppo.py:232-238): per-sample, per-channel
+// standardisation of [n, h, w, c] stacks.  NumPy's mean / std over axes (1, 2)
+// sum each (sample, channel) sequentially in row-major pixel order, so one
+// thread per (sample, channel) does exactly that in float64 (bit-exact), then
+// a second, elementwise kernel writes (x - mean) / std (0 where std == 0) as
+// float64 [n, h, w, c] or float32 [n, c, h, w] (the policy's input layout,
+// ppo.py:281-283).
+template <typename T>
+__global__ void pixnorm_stats_kernel(int64_t n, int hw, int c, const T *__restrict__ x,
+                                     double *__restrict__ stats) {
+    const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n * c) return;
+    const int64_t s = k / c;
+    const int ch = (int)(k - s * c);
+    const T *p = x + s * (int64_t)hw * c + ch;
+    double sum = 0.0;
+    for (int i = 0; i < hw; ++i) sum = __dadd_rn(sum, (double)p[(int64_t)i * c]);
+    const double mean = __ddiv_rn(sum, (double)hw);
+    double sq = 0.0;
+    for (int i = 0; i < hw; ++i) {
+        const double d = __dsub_rn((double)p[(int64_t)i * c], mean);
+        sq = __dadd_rn(sq, __dmul_rn(d, d));
+    }
+    stats[2 * k] = mean;
+    stats[2 * k + 1] = __dsqrt_rn(__ddiv_rn(sq, (double)hw));
+}
+
+// The [n, h, w, 3] float32 stacks the pixel env produces.
+// The statistics are two sequential float64 chains per (sample, channel) --
+// the order NumPy sums in, so no tree reduction is allowed -- 8192 dependent
+// adds per chain.  To hide their latency every chain of the batch runs at
+// once: a CTA is one warp, lane = sample, each lane running its three channel
+// chains side by side, fed from shared memory by 1-D bulk copies
+// (cp.async.bulk, TMA engine, mbarrier tx-count completion): stage k holds
+// PN pixels of each of the warp's 32 samples (32 contiguous 768-byte runs),
+// NS stages in flight.  Pass 1 (sums) and pass 2 (squared deviations from the
+// mean) stream the stack twice; the second stream is issued while pass 1
+// drains.
+namespace pixnorm {
+constexpr int PN = 64;                      // pixels per sample per stage
+constexpr int ROW = PN * 3 * 4;             // 768 bytes of one sample
+constexpr int ROW_PAD = ROW + 16;           // 196 words: conflict-free LDS.128 quarter-warps
+constexpr int NS = 4;                       // stages
+constexpr int STAGE = 32 * ROW_PAD;         // 25088 bytes
+constexpr int SMEM = NS * STAGE;            // 100352 bytes: two CTAs per SM
+
+__device__ __forceinline__ uint32_t su32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(uint64_t *b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void bar_expect(uint64_t *b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
+    uint32_t done = 0;
+    do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(su32(b)), "r"(parity)
+            : "memory");
+    } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(su32(dst)),
+        "l"(src), "r"(bytes), "r"(su32(b))
+        : "memory");
+}
+}  // namespace pixnorm
+
+// four pixels (three float4) of the three channels in float64
+struct Quad64 {
+    double x[12];
+};
+__device__ __forceinline__ Quad64 quad_to_f64(float4 u, float4 v, float4 w) {
+    return Quad64{{u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w, w.x, w.y, w.z, w.w}};
+}
+
+__global__ void __launch_bounds__(32) pixnorm_stats3_kernel(int64_t n, int hw,
+                                                            const float *__restrict__ x,
+                                                            double *__restrict__ stats) {
+    using namespace pixnorm;
+    extern __shared__ __align__(128) unsigned char sm[];
+    __shared__ __align__(8) uint64_t full[NS];
+    const int lane = threadIdx.x;
+    const int64_t s0 = (int64_t)blockIdx.x * 32;
+    const int ns = (int)(n - s0 < 32 ? n - s0 : 32);
+    const int tiles = hw / PN, total = 2 * tiles;
+    const unsigned char *src =
+        reinterpret_cast<const unsigned char *>(x + (s0 + lane) * (int64_t)hw * 3);
+    if (lane == 0) {
+        for (int k = 0; k < NS; ++k) bar_init(&full[k], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    auto issue = [&](int k) {  // stage k % NS <- tile k % tiles of every sample
+        uint64_t *b = &full[k % NS];
+        if (lane == 0) bar_expect(b, (uint32_t)(ns * ROW));
+        __syncwarp();
+        if (lane < ns)
+            bulk_g2s(sm + (k % NS) * STAGE + lane * ROW_PAD, src + (int64_t)(k % tiles) * ROW, ROW,
+                     b);
+    };
+    for (int k = 0; k < NS && k < total; ++k) issue(k);
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+    const double rn = (double)hw;
+    for (int k = 0; k < total; ++k) {
+        bar_wait(&full[k % NS], (uint32_t)(k / NS) & 1u);
+        const float4 *row = reinterpret_cast<const float4 *>(sm + (k % NS) * STAGE + lane * ROW_PAD);
+        if (k == tiles) {  // pass 1 done: means, then the squared-deviation chains
+            m0 = __ddiv_rn(a0, rn); m1 = __ddiv_rn(a1, rn); m2 = __ddiv_rn(a2, rn);
+            a0 = a1 = a2 = 0.0;
+        }
+        if (k < tiles) {
+#pragma unroll 4
+            for (int q = 0; q < PN / 4; ++q) {
+                const Quad64 d = quad_to_f64(row[3 * q], row[3 * q + 1], row[3 * q + 2]);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    a0 = __dadd_rn(a0, d.x[3 * p]);
+                    a1 = __dadd_rn(a1, d.x[3 * p + 1]);
+                    a2 = __dadd_rn(a2, d.x[3 * p + 2]);
+                }
+            }
+        } else {
+#pragma unroll 4
+            for (int q = 0; q < PN / 4; ++q) {
+                const Quad64 d = quad_to_f64(row[3 * q], row[3 * q + 1], row[3 * q + 2]);
+#pragma unroll
+                for (int p = 0; p < 4; ++p) {
+                    const double e0 = __dsub_rn(d.x[3 * p], m0), e1 = __dsub_rn(d.x[3 * p + 1], m1),
+                                 e2 = __dsub_rn(d.x[3 * p + 2], m2);
+                    a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
+                    a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
+                    a2 = __dadd_rn(a2, __dmul_rn(e2, e2));
+                }
+            }
+        }
+        __syncwarp();  // every lane is done with stage k % NS before it is refilled
+        if (k + NS < total) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(k + NS);
+        }
+    }
+    if (lane < ns) {
+        double *o = stats + 6 * (s0 + lane);
+        o[0] = m0; o[1] = __dsqrt_rn(__ddiv_rn(a0, rn));
+        o[2] = m1; o[3] = __dsqrt_rn(__ddiv_rn(a1, rn));
+        o[4] = m2; o[5] = __dsqrt_rn(__ddiv_rn(a2, rn));
+    }
+}
+
+// Elementwise (x - mean) / std for the 3-channel float32 stacks: one thread per
+// four pixels (three 16-byte loads), writing four pixels of each channel plane
+// (channels_first) or the same 48 bytes back (NHWC); grid.y walks samples.
+template <typename U, bool CF>
+__global__ void __launch_bounds__(256) pixnorm_apply3_kernel(int64_t n, int hw,
+                                                             const float *__restrict__ x,
+                                                             const double *__restrict__ stats,
+                                                             U *__restrict__ out) {
+    const int q = blockIdx.x * blockDim.x + threadIdx.x;
+    if (q >= (hw >> 2)) return;
+    for (int64_t s = blockIdx.y; s < n; s += gridDim.y) {
+        const double *st = stats + 6 * s;
+        const double m[3] = {st[0], st[2], st[4]}, sd[3] = {st[1], st[3], st[5]};
+        const float4 *p = reinterpret_cast<const float4 *>(x + (s * hw + 4 * q) * 3);
+        const float4 u = p[0], v = p[1], w = p[2];
+        const float f[12] = {u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w, w.x, w.y, w.z, w.w};
+        // one IEEE reciprocal per channel, then each quotient by Markstein's
+        // correction q1 = q0 + (a - q0 sd) r: correctly rounded (= __ddiv_rn) for
+        // r = RN(1/sd) and a faithful q0 while nothing under/overflows; outside
+        // that range (and for sd = inf / NaN) the IEEE division
+        double r[3];
+        bool safe[3];
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            r[c] = __ddiv_rn(1.0, sd[c]);
+            safe[c] = sd[c] > 0x1p-500 && sd[c] < 0x1p500;
+        }
+        U y[12];
+#pragma unroll
+        for (int e = 0; e < 12; ++e) {
+            const int c = e % 3;
+            const double a = __dsub_rn((double)f[e], m[c]);
+            double qv;
+            if (safe[c] && (fabs(a) > 0x1p-900 || a == 0.0) && fabs(a) < 0x1p500) {
+                const double q0 = __dmul_rn(a, r[c]);
+                qv = __fma_rn(__fma_rn(-q0, sd[c], a), r[c], q0);
+            } else {
+                qv = __ddiv_rn(a, sd[c]);
+            }
+            y[e] = (U)(sd[c] > 0.0 ? qv : 0.0);
+        }
+        if (CF) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                U *o = out + (s * 3 + c) * hw + 4 * q;
+                if constexpr (sizeof(U) == 4) {
+                    *reinterpret_cast<float4 *>(o) = make_float4(y[c], y[3 + c], y[6 + c], y[9 + c]);
+                } else {
+                    reinterpret_cast<double2 *>(o)[0] = make_double2(y[c], y[3 + c]);
+                    reinterpret_cast<double2 *>(o)[1] = make_double2(y[6 + c], y[9 + c]);
+                }
+            }
+        } else {
+            U *o = out + (s * hw + 4 * q) * 3;
+#pragma unroll
+            for (int e = 0; e < 12; ++e) o[e] = y[e];
+        }
+    }
+}
+
+template <typename T, typename U>
+__global__ void pixnorm_apply_kernel(int64_t n, int hw, int c, const T *__restrict__ x,
+                                     const double *__restrict__ stats, int channels_first,
+                                     U *__restrict__ out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // output element
+    const int64_t total = n * (int64_t)hw * c;
+    if (e >= total) return;
+    int64_t s, pix;
+    int ch;
+    if (channels_first) {  // e = (s * c + ch) * hw + pix
+        const int64_t sc = e / hw;
+        pix = e - sc * hw;
+        s = sc / c;
+        ch = (int)(sc - s * c);
+    } else {  // e = (s * hw + pix) * c + ch
+        const int64_t sp = e / c;
+        ch = (int)(e - sp * c);
+        s = sp / hw;
+        pix = sp - s * hw;
+    }
+    const double mean = stats[2 * (s * c + ch)], sd = stats[2 * (s * c + ch) + 1];
+    const double v = (double)x[(s * hw + pix) * c + ch];
+    out[e] = (U)(sd > 0.0 ? __ddiv_rn(__dsub_rn(v, mean), sd) : 0.0);
+}
+
 }  // namespace dk

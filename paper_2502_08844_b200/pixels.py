@@ -157,4 +157,26 @@ class PixelObservation:
         return self._stack(), term
 
 
-__all__ = ["NOMINAL", "PixelObservation", "batch_render", "pack_visuals"]
+def pixel_normalize(x, channels_first: bool = True, out_dtype=None):
+    """ppo.pixel_normalize (ppo.py:232-238) on a CUDA [n, h, w, c] stack:
+    per-sample, per-channel (x - mean) / std over the pixels (0 where std is
+    0), computed in float64 in NumPy's summation order.  Default output: the
+    policy's input, float32 [n, c, h, w] (ppo.py:281-283); channels_first=False
+    and out_dtype=torch.float64 give NumPy's own result."""
+    torch = _torch()
+    x = x.contiguous()
+    if x.dim() != 4:
+        raise InvalidInputError("pixel_normalize expects [n, h, w, c]")
+    n, h, w, c = x.shape
+    od = out_dtype or torch.float32
+    out = torch.empty((n, c, h, w) if channels_first else (n, h, w, c), dtype=od,
+                      device=x.device)
+    stats = torch.empty((n, c, 2), dtype=torch.float64, device=x.device)
+    _check(nat.lib().dk_pixels_normalize(_dtype_code(x), nat.DK_F64 if od == torch.float64
+                                         else nat.DK_F32, n, h, w, c, _ptr(x),
+                                         int(bool(channels_first)), _ptr(stats), _ptr(out),
+                                         _stream(x.device)))
+    return out
+
+
+__all__ = ["NOMINAL", "PixelObservation", "batch_render", "pack_visuals", "pixel_normalize"]

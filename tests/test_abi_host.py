@@ -31,7 +31,7 @@ def test_header_symbols_exported_and_bound():
     assert sorted(_native.EXPORTED_SYMBOLS) == declared
     for s in declared:
         assert getattr(lib, s) is not None
-    assert lib.dk_abi_version() == 6
+    assert lib.dk_abi_version() == 7
 
 
 def test_task_ids_and_dims():

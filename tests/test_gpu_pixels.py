@@ -123,3 +123,36 @@ def test_pixel_task_through_env_api(px, PX, api):
         with pytest.raises(dk.ConfigError):
             env.rollout(torch.zeros((2, N, 1), device="cuda", dtype=torch.float64))
         env.check()
+
+
+@pytest.mark.parametrize("case", ["stack", "const", "f32", "f64", "single"])
+def test_pixel_normalize_bit_exact(PX, case):
+    """ppo.pixel_normalize (ppo.py:232-238) and the policy input built from it
+    (_prep_policy_obs, ppo.py:278-283): float64 NHWC and float32 NCHW bit-exact."""
+    from tests.conftest import GOLDEN
+
+    z = np.load(os.path.join(GOLDEN, "pixnorm_golden.npz"))
+    x = torch.as_tensor(z[f"{case}/x"], device="cuda")
+    y = PX.pixel_normalize(x, channels_first=False, out_dtype=torch.float64)
+    np.testing.assert_array_equal(y.cpu().numpy(), z[f"{case}/y"])
+    pol = PX.pixel_normalize(x)
+    assert pol.dtype == torch.float32 and pol.shape == z[f"{case}/policy"].shape
+    np.testing.assert_array_equal(pol.cpu().numpy(), z[f"{case}/policy"])
+
+
+def test_pixel_normalize_env_stacks_match_oracle(PX):
+    """At rollout size: the device env's own 8192-world stacks through the
+    device normaliser equal the oracle's normalisation of the same stacks."""
+    from oracle import ppo as orc
+    from paper_2502_08844_b200 import envkit
+
+    env = envkit.DeviceBatchEnv(envkit.EnvConfig(task="cartpole-balance-pixels",
+                                                 visual_randomization=True), 512)
+    obs = env.reset(seed=9)
+    for _ in range(3):
+        obs = env.step(torch.rand(512, 1, device="cuda") * 2 - 1)
+    x = obs["pixels"]
+    y = PX.pixel_normalize(x, channels_first=False, out_dtype=torch.float64).cpu().numpy()
+    np.testing.assert_array_equal(y, orc.pixel_normalize(x.cpu().numpy()))
+    empty = PX.pixel_normalize(x[:0])
+    assert empty.shape == (0, 3, 64, 64)

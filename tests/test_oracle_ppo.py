@@ -43,3 +43,11 @@ def test_normalizer_bit_exact(ppo_g, orc):
                                       ppo_g[f"norm/apply{k + 1}"])
         np.testing.assert_array_equal(orc.norm_apply(count, mean, var, 1e-8, probe, True),
                                       ppo_g[f"norm/invert{k + 1}"])
+
+
+@pytest.mark.parametrize("case", ["stack", "const", "f32", "f64", "single"])
+def test_pixel_normalize_bit_exact(orc, case):
+    """ppo.pixel_normalize (ppo.py:232-238): sequential per-(sample, channel)
+    sums reproduce NumPy's mean / std bit for bit, constant channels -> 0."""
+    z = np.load(os.path.join(GOLDEN, "pixnorm_golden.npz"))
+    np.testing.assert_array_equal(orc.pixel_normalize(z[f"{case}/x"]), z[f"{case}/y"])
