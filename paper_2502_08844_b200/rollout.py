@@ -79,6 +79,53 @@ def make_policy(obs_dim: int, action_dim: int, hidden=(128, 128, 128, 128),
     return MLPPolicy()
 
 
+def make_cnn_policy(in_channels: int, image_size: int, action_dim: int, dense=(256, 256),
+                    init_std: float = 0.5):
+    """ppo.CNNPolicy (ppo.py:143-178): conv trunk 32@8x8/4, 64@4x4/2, 64@3x3/1
+    (Swish), dense layers, a linear head and a free log_std; input the
+    pixel_normalize'd [N, C, H, W] float32 stack.  Same parameter names as the
+    reference (trunk.convs.*, trunk.dense.*, head.*, log_std)."""
+    import math
+
+    import torch
+    import torch.nn as nn
+
+    class CNNTrunk(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.convs = nn.Sequential(
+                nn.Conv2d(in_channels, 32, 8, stride=4), nn.SiLU(),
+                nn.Conv2d(32, 64, 4, stride=2), nn.SiLU(),
+                nn.Conv2d(64, 64, 3, stride=1, padding=1), nn.SiLU(),
+                nn.Flatten(),
+            )
+            with torch.no_grad():
+                flat = self.convs(torch.zeros(1, in_channels, image_size, image_size)).shape[1]
+            layers = []
+            sizes = (flat, *dense)
+            for a, b in zip(sizes[:-1], sizes[1:]):
+                layers += [nn.Linear(a, b), nn.SiLU()]
+            self.dense = nn.Sequential(*layers)
+            self.out_dim = dense[-1]
+
+        def forward(self, img):
+            return self.dense(self.convs(img))
+
+    class CNNPolicy(nn.Module):
+        def __init__(self):
+            super().__init__()
+            self.trunk = CNNTrunk()
+            self.head = nn.Linear(self.trunk.out_dim, action_dim)
+            self.log_std = nn.Parameter(torch.full((action_dim,), math.log(init_std)))
+            self.action_dim = action_dim
+
+        def forward(self, img):
+            mean = self.head(self.trunk(img))
+            return mean, self.log_std.expand_as(mean)
+
+    return CNNPolicy()
+
+
 def make_value(obs_dim: int, hidden=(256, 256, 256, 256, 256)):
     """ppo.MLPValue (ppo.py:136-142): forward(obs) -> [N] values."""
     import torch.nn as nn
@@ -134,14 +181,21 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
     raw_p, raw_v = [], []
     raw_reward_sum = torch.zeros((), dtype=torch.float64, device=env.device)
 
+    pixel_policy = cfg.policy_obs_key == "pixels"
+    if pixel_policy:
+        from .pixels import pixel_normalize
+
     def prep(normalizer, x):
         return (normalizer.apply(x) if normalizer is not None else x).to(f32)
+
+    def prep_policy(x):  # ppo._prep_policy_obs (ppo.py:278-285)
+        return pixel_normalize(x) if pixel_policy else prep(policy_normalizer, x)
 
     with torch.no_grad():
         for t in range(T):
             pol_in, val_in = _route(obs, cfg)
-            pol_t, val_t = prep(policy_normalizer, pol_in), prep(value_normalizer, val_in)
-            if policy_normalizer is not None:
+            pol_t, val_t = prep_policy(pol_in), prep(value_normalizer, val_in)
+            if policy_normalizer is not None and not pixel_policy:
                 raw_p.append(pol_in.clone())
             if value_normalizer is not None:
                 raw_v.append(val_in.clone())
@@ -160,8 +214,7 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             boot = step["trunc"] & ~step["done"] & step["terminal_mask"]
             term_in = torch.where(boot[:, None], step["terminal_obs"],
                                   torch.zeros((), dtype=env.dtype, device=env.device))
-            _, tv_in = _route({"state": term_in, "privileged_state": term_in}, cfg)
-            tv = value(prep(value_normalizer, tv_in)).to(torch.float64)
+            tv = value(prep(value_normalizer, term_in)).to(torch.float64)
             term_val = torch.where(boot, tv, torch.zeros_like(tv))
             p_obs.append(pol_t)
             v_obs.append(val_t)
@@ -173,6 +226,8 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             vals.append(v.to(torch.float64))
             nxt = step["obs"].clone()
             obs = {"state": nxt, "privileged_state": nxt}
+            if "pixels" in step:
+                obs["pixels"] = step["pixels"].clone()
         _, val_in = _route(obs, cfg)
         bootstrap = value(prep(value_normalizer, val_in)).to(torch.float64)
     batch = DeviceRolloutBatch(torch.stack(p_obs), torch.stack(v_obs), torch.stack(acts),
@@ -208,6 +263,8 @@ class RolloutGraph:
                  value_normalizer=None):
         import torch
 
+        if cfg.policy_obs_key == "pixels":
+            raise ConfigError("RolloutGraph: pixel policies run eagerly (collect_rollout_device)")
         self.env, self.policy, self.value, self.cfg = env, policy, value, cfg
         self.pn, self.vn = policy_normalizer, value_normalizer
         # one eager phase: warms up cuBLAS / allocator and fills the statistics
@@ -242,5 +299,5 @@ class RolloutGraph:
             self.reward_out
 
 
-__all__ = ["DeviceRolloutBatch", "RolloutGraph", "collect_rollout_device", "make_policy",
-           "make_value", "tanh_gaussian_log_prob"]
+__all__ = ["DeviceRolloutBatch", "RolloutGraph", "collect_rollout_device", "make_cnn_policy",
+           "make_policy", "make_value", "tanh_gaussian_log_prob"]

@@ -103,3 +103,62 @@ def test_rollout_graph_replay():
         for f in ("policy_obs", "actions", "log_probs", "rewards", "values", "bootstrap"):
             assert torch.isfinite(getattr(batch, f)).all(), f
     env.check()
+
+
+def test_pixel_policy_rollout_matches_reference():
+    """collect_rollout_device with the reference's CNNPolicy on pixel_normalize'd
+    cartpole pixel stacks (tests/golden/rollout_pixels_golden.npz): the policy
+    inputs equal the reference's (float32 of the float64 standardisation), the
+    rest agrees to the network tolerance above (cuDNN convolutions in float32,
+    TF32 off as on the reference's CPU)."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+    from tests.conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, "rollout_pixels_golden.npz"))
+    N, T = 4, 6
+    policy = R.make_cnn_policy(3, 64, 1, (32,)).cuda()
+    value = R.make_value(5, (48, 48)).cuda()
+    policy.load_state_dict({k[7:]: torch.as_tensor(g[k]) for k in g.files
+                            if k.startswith("policy/")})
+    value.load_state_dict({k[6:]: torch.as_tensor(g[k]) for k in g.files
+                           if k.startswith("value/")})
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = T, 10.0, 0.995
+        policy_obs_key, value_obs_key = "pixels", "state"
+
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance-pixels", episode_length=4,
+                                         visual_randomization=True), N, dtype="float64")
+    obs = env.reset(seed=6)
+    np.testing.assert_array_equal(obs["state"].cpu().numpy(), g["obs0"])
+    vn = P.DeviceRunningNormalizer(5)
+    tf32 = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        batch, obs, mean_r = R.collect_rollout_device(
+            env, policy, value, Cfg, obs, None, vn,
+            noise=torch.as_tensor(g["noise"], device="cuda"))
+    finally:
+        torch.backends.cudnn.allow_tf32 = tf32
+    po = batch.policy_obs.cpu().numpy()
+    assert po.shape == (T, N, 3, 64, 64) and po.dtype == np.float32
+    np.testing.assert_array_equal(po[0], g["policy_obs_first"])
+    np.testing.assert_array_equal(po[-1], g["policy_obs_last"])
+    np.testing.assert_allclose(po.astype(np.float64).sum(axis=(3, 4)), g["policy_obs_sums"],
+                               rtol=0, atol=1e-9)
+    np.testing.assert_array_equal(batch.dones.cpu().numpy(), g["dones"])
+    for f in ("value_obs", "actions", "pre_tanh", "log_probs", "rewards", "values", "bootstrap"):
+        err = _close(getattr(batch, f).cpu().numpy(), g[f])
+        assert err < 1e-4, (f, err)
+    assert _close(obs["state"].cpu().numpy(), g["next_obs"]) < 1e-4
+    assert abs(float(mean_r) - float(g["mean_reward"])) < 1e-4
+    c, m, v = vn.to_numpy()
+    assert c == float(g["vn_count"])
+    assert _close(m, g["vn_mean"], 1e-6) < 1e-4 and _close(v, g["vn_var"], 1e-6) < 1e-4
+    with pytest.raises(dk.ConfigError):
+        R.RolloutGraph(env, policy, value, Cfg, obs, None, vn)
+    env.check()
