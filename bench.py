@@ -426,7 +426,48 @@ def bench_pixels(args, dev, steps=50):
     ks = e0.elapsed_time(e1) / steps / 1e3
     peak, src = hbm_peak()
     bytes_ws = 64 * 64 * 3 * 4
+    # ppo.pixel_normalize of the step's stacks into the CNN policy's NCHW input
+    from paper_2502_08844_b200.pixels import pixel_normalize
+
+    px = out["pixels"]
+    for _ in range(3):
+        pixel_normalize(px)
+    e0.record()
+    for _ in range(steps):
+        pixel_normalize(px)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    pn_s = e0.elapsed_time(e1) / steps / 1e3
+    pn_bytes = 2 * bytes_ws  # the stack read once + the NCHW float32 input written once
+    # a pixel-policy PPO rollout phase (ppo.collect_rollout with the reference's
+    # default CNNPolicy 32@8x8/4-64@4x4/2-64@3x3 + 2x256 dense, MLPValue 5x256 on
+    # the state, value normaliser), eager, T control steps
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = 10, 10.0, 0.995
+        policy_obs_key, value_obs_key = "pixels", "state"
+
+    torch.manual_seed(0)
+    policy = R.make_cnn_policy(3, 64, 1).to(dev)
+    value = R.make_value(5).to(dev)
+    vn = P.DeviceRunningNormalizer(5, device=dev)
+    obs = env.reset(seed=1)
+    _, obs, _ = R.collect_rollout_device(env, policy, value, Cfg, obs, None, vn)
+    torch.cuda.synchronize(dev)
+    e0.record()
+    reps = 3
+    for _ in range(reps):
+        _, obs, _ = R.collect_rollout_device(env, policy, value, Cfg, obs, None, vn)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    roll_s = e0.elapsed_time(e1) / 1e3 / reps
     env.close()
+    pn = {"ms": pn_s * 1e3, "achieved": n * pn_bytes / pn_s / 1e9, "peak": peak, "unit": "GB/s",
+          "frac": n * pn_bytes / pn_s / 1e9 / peak, "bytes_per_world": pn_bytes,
+          "note": "two kernels: float64 sequential stats chains (streams the stack twice) "
+                  "+ elementwise apply"}
     return {"metric": "cartpole-balance-pixels env-steps/s (step + render + 3-frame stack, "
                       "float32, 64x64)", "value": n / (ms / 1e3), "unit": "env_steps/s",
             "ms_per_step": ms, "worlds": n,
@@ -434,6 +475,11 @@ def bench_pixels(args, dev, steps=50):
                          "achieved": n * bytes_ws / ks / 1e9, "peak": peak, "unit": "GB/s",
                          "frac": n * bytes_ws / ks / 1e9 / peak, "peak_source": src,
                          "bytes_per_world_step": bytes_ws},
+            "pixel_normalize": pn,
+            "pixel_policy_rollout": {"value": n * Cfg.unroll_length / roll_s,
+                                     "unit": "env_steps/s", "ms_per_phase": roll_s * 1e3,
+                                     "phase": f"T={Cfg.unroll_length} x {n} worlds, eager, "
+                                              "CNN policy float32 (cuDNN)"},
             "reference_cpu": {"value": 3.4e3, "unit": "env_steps/s",
                               "sample": "SURVEY.md §8f: BatchEnv('cartpole-balance-pixels'), "
                                         "N=256, one core"}}
