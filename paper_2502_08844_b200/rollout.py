@@ -241,6 +241,52 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
     return batch, obs, raw_reward_sum / T
 
 
+def evaluate_device(policy, env, cfg, episodes: int | None = None, max_steps: int | None = None,
+                    policy_normalizer=None) -> dict:
+    """ppo.evaluate (ppo.py:479-502) on the device: a deterministic-policy
+    rollout (action = tanh(mean)), one episode per world, from ``env.reset()``
+    until every world has finished once (done | trunc) or ``max_steps`` /
+    ``episode_length`` steps.  Returns the reference's dict; stops at exactly
+    the reference's step (one 1-byte device→host read per step), so the env's
+    episode counters end where the reference's do."""
+    import torch
+
+    pixel_policy = cfg.policy_obs_key == "pixels"
+    if pixel_policy:
+        from .pixels import pixel_normalize
+    obs = env.reset()
+    n = env.num_envs
+    returns = torch.zeros(n, dtype=torch.float64, device=env.device)
+    finished = torch.zeros(n, dtype=torch.bool, device=env.device)
+    out = env._outputs((), False)
+    steps = 0
+    limit = max_steps or env.config.episode_length
+    with torch.no_grad():
+        while steps < limit:
+            x = obs[cfg.policy_obs_key]
+            if pixel_policy:
+                x = pixel_normalize(x)
+            else:
+                x = (policy_normalizer.apply(x) if policy_normalizer is not None else x)
+                x = x.to(torch.float32)
+            mean, _ = policy(x)
+            if torch.isnan(mean).any():
+                raise RuntimeError("policy produced NaN mean")
+            step = env.step(torch.tanh(mean).to(env.dtype), autoreset=True, with_info=False,
+                            out=out)
+            returns += step["reward"].to(torch.float64) * (~finished)
+            finished |= step["done"] | step["trunc"]
+            steps += 1
+            obs = {"state": step["obs"], "privileged_state": step["obs"]}
+            if "pixels" in step:
+                obs["pixels"] = step["pixels"]
+            if bool(finished.all()):
+                break
+    return {"eval_return_mean": float(returns.mean()),
+            "eval_return_std": float(returns.std(unbiased=False)),
+            "eval_episode_steps": steps}
+
+
 def _update(batch, policy_normalizer, value_normalizer):
     if batch.raw_policy_obs is not None:
         policy_normalizer.update(batch.raw_policy_obs)
@@ -299,5 +345,6 @@ class RolloutGraph:
             self.reward_out
 
 
-__all__ = ["DeviceRolloutBatch", "RolloutGraph", "collect_rollout_device", "make_cnn_policy",
+__all__ = ["DeviceRolloutBatch", "RolloutGraph", "collect_rollout_device", "evaluate_device",
+           "make_cnn_policy",
            "make_policy", "make_value", "tanh_gaussian_log_prob"]

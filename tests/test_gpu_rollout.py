@@ -162,3 +162,57 @@ def test_pixel_policy_rollout_matches_reference():
     with pytest.raises(dk.ConfigError):
         R.RolloutGraph(env, policy, value, Cfg, obs, None, vn)
     env.check()
+
+
+def test_evaluate_device_matches_reference():
+    """rollout.evaluate_device against ppo.evaluate (tests/golden/evaluate_golden.*):
+    MLP policy with a policy normaliser (full episodes, then max_steps=10 continuing
+    the episode counters) and the CNN policy on pixel stacks; returns within the
+    network tolerance, the step counts exactly."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import json
+
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+    from tests.conftest import GOLDEN
+
+    g = np.load(os.path.join(GOLDEN, "evaluate_golden.npz"))
+    with open(os.path.join(GOLDEN, "evaluate_golden.json")) as f:
+        res = json.load(f)
+
+    def check(got, want):
+        assert got["eval_episode_steps"] == want["eval_episode_steps"]
+        for k in ("eval_return_mean", "eval_return_std"):
+            assert abs(got[k] - want[k]) <= 1e-5 * max(abs(want[k]), 1e-2), (k, got, want)
+
+    policy = R.make_policy(5, 1, (32, 32)).cuda()
+    policy.load_state_dict({k[4:]: torch.as_tensor(g[k]) for k in g.files if k.startswith("mlp/")})
+    pn = P.DeviceRunningNormalizer(5, count=100.0, mean=g["pn/mean"], var=g["pn/var"])
+
+    class Cfg:
+        policy_obs_key = value_obs_key = "state"
+
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance", episode_length=25, seed=5), 32,
+                            dtype="float64")
+    check(R.evaluate_device(policy, env, Cfg, policy_normalizer=pn), res["mlp"][0])
+    check(R.evaluate_device(policy, env, Cfg, max_steps=10, policy_normalizer=pn), res["mlp"][1])
+    env.check()
+
+    cnn = R.make_cnn_policy(3, 64, 1, (16,)).cuda()
+    cnn.load_state_dict({k[4:]: torch.as_tensor(g[k]) for k in g.files if k.startswith("cnn/")})
+
+    class PCfg:
+        policy_obs_key, value_obs_key = "pixels", "state"
+
+    penv = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance-pixels", episode_length=6,
+                                          visual_randomization=True, seed=2), 4, dtype="float64")
+    tf32 = torch.backends.cudnn.allow_tf32
+    torch.backends.cudnn.allow_tf32 = False
+    try:
+        check(R.evaluate_device(cnn, penv, PCfg), res["cnn"][0])
+        check(R.evaluate_device(cnn, penv, PCfg), res["cnn"][1])
+    finally:
+        torch.backends.cudnn.allow_tf32 = tf32
+    penv.check()
