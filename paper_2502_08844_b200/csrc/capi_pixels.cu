@@ -127,7 +127,7 @@ int dk_pixels_normalize(int in_dtype, int out_dtype, int64_t n, int h, int w, in
             if (e != cudaSuccess) return cuda_rc(e, "pixel_normalize attribute");
             if (dev < 64) __atomic_fetch_or(&attr_set, 1ull << dev, __ATOMIC_RELAXED);
         }
-        dk::pixnorm_stats3_kernel<<<(unsigned)((n + 31) / 32), 32, dk::pixnorm::SMEM, st>>>(
+        dk::pixnorm_stats3_kernel<<<(unsigned)((n + 31) / 32), 96, dk::pixnorm::SMEM, st>>>(
             n, hw, (const float *)x, stats);
         const dim3 g((unsigned)((hw / 4 + 255) / 256), (unsigned)(n < 65535 ? n : 65535));
         const float *xf = (const float *)x;

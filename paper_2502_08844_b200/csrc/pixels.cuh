@@ -345,13 +345,13 @@ __global__ void pixnorm_stats_kernel(int64_t n, int hw, int c, const T *__restri
 // The statistics are two sequential float64 chains per (sample, channel) --
 // the order NumPy sums in, so no tree reduction is allowed -- 8192 dependent
 // adds per chain.  To hide their latency every chain of the batch runs at
-// once: a CTA is one warp, lane = sample, each lane running its three channel
-// chains side by side, fed from shared memory by 1-D bulk copies
-// (cp.async.bulk, TMA engine, mbarrier tx-count completion): stage k holds
-// PN pixels of each of the warp's 32 samples (32 contiguous 768-byte runs),
-// NS stages in flight.  Pass 1 (sums) and pass 2 (squared deviations from the
-// mean) stream the stack twice; the second stream is issued while pass 1
-// drains.
+// once (24 576 chains at 8192 samples): a CTA holds 32 samples, warp c runs
+// channel c, lane = sample.  The stack streams through shared memory in stages
+// of PN pixels of each of the 32 samples (32 row runs of 768 bytes, padded
+// rows), NS - 1 stages in flight; pass 1 (sums) and pass 2 (squared deviations
+// from the mean) stream it twice.  Measured alternatives: one warp
+// per 32 samples with three chains per lane, and per-row cp.async.bulk copies
+// (the TMA engine serialises 32 small copies per stage).
 namespace pixnorm {
 constexpr int PN = 64;                      // pixels per sample per stage
 constexpr int ROW = PN * 3 * 4;             // 768 bytes of one sample
@@ -363,114 +363,83 @@ constexpr int SMEM = NS * STAGE;            // 100352 bytes: two CTAs per SM
 __device__ __forceinline__ uint32_t su32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
-__device__ __forceinline__ void bar_init(uint64_t *b, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void bar_expect(uint64_t *b, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(b)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void bar_wait(uint64_t *b, uint32_t parity) {
-    uint32_t done = 0;
-    do {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(su32(b)), "r"(parity)
-            : "memory");
-    } while (!done);
-}
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *b) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(su32(dst)),
-        "l"(src), "r"(bytes), "r"(su32(b))
-        : "memory");
-}
 }  // namespace pixnorm
 
-// four pixels (three float4) of the three channels in float64
-struct Quad64 {
-    double x[12];
-};
-__device__ __forceinline__ Quad64 quad_to_f64(float4 u, float4 v, float4 w) {
-    return Quad64{{u.x, u.y, u.z, u.w, v.x, v.y, v.z, v.w, w.x, w.y, w.z, w.w}};
+// Warp c of a 96-thread CTA runs channel c of the CTA's 32 samples (lane =
+// sample, one chain per lane): it reads the 16-byte words of its lane's row and
+// keeps its channel's four values of every four pixels.
+template <int C>
+__device__ __forceinline__ void pixnorm_chan(const float4 *row, double &a, double m, bool pass2) {
+#pragma unroll 4
+    for (int q = 0; q < pixnorm::PN / 4; ++q) {
+        const float4 u = row[3 * q], v = row[3 * q + 1], w = row[3 * q + 2];
+        float e[4];
+        if (C == 0) { e[0] = u.x; e[1] = u.w; e[2] = v.z; e[3] = w.y; }
+        if (C == 1) { e[0] = u.y; e[1] = v.x; e[2] = v.w; e[3] = w.z; }
+        if (C == 2) { e[0] = u.z; e[1] = v.y; e[2] = w.x; e[3] = w.w; }
+        if (!pass2) {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) a = __dadd_rn(a, (double)e[p]);
+        } else {
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const double d = __dsub_rn((double)e[p], m);
+                a = __dadd_rn(a, __dmul_rn(d, d));
+            }
+        }
+    }
 }
 
-__global__ void __launch_bounds__(32) pixnorm_stats3_kernel(int64_t n, int hw,
-                                                            const float *__restrict__ x,
-                                                            double *__restrict__ stats) {
+// Staging: all 96 threads copy the stage with 16-byte cp.async (each sample's
+// 768-byte run coalesced), NS - 1 stages in flight, two CTA barriers per stage.
+__global__ void __launch_bounds__(96) pixnorm_stats3_kernel(int64_t n, int hw,
+                                                             const float *__restrict__ x,
+                                                             double *__restrict__ stats) {
     using namespace pixnorm;
     extern __shared__ __align__(128) unsigned char sm[];
-    __shared__ __align__(8) uint64_t full[NS];
-    const int lane = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, c = tid >> 5;
     const int64_t s0 = (int64_t)blockIdx.x * 32;
     const int ns = (int)(n - s0 < 32 ? n - s0 : 32);
     const int tiles = hw / PN, total = 2 * tiles;
-    const unsigned char *src =
-        reinterpret_cast<const unsigned char *>(x + (s0 + lane) * (int64_t)hw * 3);
-    if (lane == 0) {
-        for (int k = 0; k < NS; ++k) bar_init(&full[k], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    auto issue = [&](int k) {  // stage k % NS <- tile k % tiles of every sample
-        uint64_t *b = &full[k % NS];
-        if (lane == 0) bar_expect(b, (uint32_t)(ns * ROW));
-        __syncwarp();
-        if (lane < ns)
-            bulk_g2s(sm + (k % NS) * STAGE + lane * ROW_PAD, src + (int64_t)(k % tiles) * ROW, ROW,
-                     b);
+    const unsigned char *base = reinterpret_cast<const unsigned char *>(x + s0 * (int64_t)hw * 3);
+    const int64_t sample_bytes = (int64_t)hw * 12;
+    constexpr int CHUNKS = ROW / 16;  // 48 16-byte chunks per row
+    auto load = [&](int k) {
+        if (k < total) {
+            unsigned char *dst = sm + (k % NS) * STAGE;
+            const unsigned char *src = base + (int64_t)(k % tiles) * ROW;
+            for (int i = tid; i < ns * CHUNKS; i += 96) {
+                const int r = i / CHUNKS, ch = i - r * CHUNKS;
+                asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                                 su32(dst + r * ROW_PAD + ch * 16)),
+                             "l"(src + r * sample_bytes + ch * 16)
+                             : "memory");
+            }
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    for (int k = 0; k < NS && k < total; ++k) issue(k);
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, m0 = 0.0, m1 = 0.0, m2 = 0.0;
+    for (int k = 0; k < NS - 1; ++k) load(k);
+    double a = 0.0, m = 0.0;
     const double rn = (double)hw;
     for (int k = 0; k < total; ++k) {
-        bar_wait(&full[k % NS], (uint32_t)(k / NS) & 1u);
+        load(k + NS - 1);  // its stage was released by the barrier that ended iteration k - 1
+        asm volatile("cp.async.wait_group %0;" ::"n"(NS - 1) : "memory");
+        __syncthreads();
         const float4 *row = reinterpret_cast<const float4 *>(sm + (k % NS) * STAGE + lane * ROW_PAD);
-        if (k == tiles) {  // pass 1 done: means, then the squared-deviation chains
-            m0 = __ddiv_rn(a0, rn); m1 = __ddiv_rn(a1, rn); m2 = __ddiv_rn(a2, rn);
-            a0 = a1 = a2 = 0.0;
+        if (k == tiles) {
+            m = __ddiv_rn(a, rn);
+            a = 0.0;
         }
-        if (k < tiles) {
-#pragma unroll 4
-            for (int q = 0; q < PN / 4; ++q) {
-                const Quad64 d = quad_to_f64(row[3 * q], row[3 * q + 1], row[3 * q + 2]);
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    a0 = __dadd_rn(a0, d.x[3 * p]);
-                    a1 = __dadd_rn(a1, d.x[3 * p + 1]);
-                    a2 = __dadd_rn(a2, d.x[3 * p + 2]);
-                }
-            }
-        } else {
-#pragma unroll 4
-            for (int q = 0; q < PN / 4; ++q) {
-                const Quad64 d = quad_to_f64(row[3 * q], row[3 * q + 1], row[3 * q + 2]);
-#pragma unroll
-                for (int p = 0; p < 4; ++p) {
-                    const double e0 = __dsub_rn(d.x[3 * p], m0), e1 = __dsub_rn(d.x[3 * p + 1], m1),
-                                 e2 = __dsub_rn(d.x[3 * p + 2], m2);
-                    a0 = __dadd_rn(a0, __dmul_rn(e0, e0));
-                    a1 = __dadd_rn(a1, __dmul_rn(e1, e1));
-                    a2 = __dadd_rn(a2, __dmul_rn(e2, e2));
-                }
-            }
-        }
-        __syncwarp();  // every lane is done with stage k % NS before it is refilled
-        if (k + NS < total) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            issue(k + NS);
-        }
+        const bool p2 = k >= tiles;
+        if (c == 0) pixnorm_chan<0>(row, a, m, p2);
+        else if (c == 1) pixnorm_chan<1>(row, a, m, p2);
+        else pixnorm_chan<2>(row, a, m, p2);
+        __syncthreads();
     }
     if (lane < ns) {
-        double *o = stats + 6 * (s0 + lane);
-        o[0] = m0; o[1] = __dsqrt_rn(__ddiv_rn(a0, rn));
-        o[2] = m1; o[3] = __dsqrt_rn(__ddiv_rn(a1, rn));
-        o[4] = m2; o[5] = __dsqrt_rn(__ddiv_rn(a2, rn));
+        double *o = stats + 6 * (s0 + lane) + 2 * c;
+        o[0] = m;
+        o[1] = __dsqrt_rn(__ddiv_rn(a, rn));
     }
 }
 
