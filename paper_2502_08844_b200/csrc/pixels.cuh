@@ -495,10 +495,18 @@ __global__ void __launch_bounds__(256) pixnorm_apply3_kernel(int64_t n, int hw,
                     reinterpret_cast<double2 *>(o)[1] = make_double2(y[6 + c], y[9 + c]);
                 }
             }
-        } else {
+        } else {  // the same 12 values back in place: 16-byte stores
             U *o = out + (s * hw + 4 * q) * 3;
+            if constexpr (sizeof(U) == 4) {
 #pragma unroll
-            for (int e = 0; e < 12; ++e) o[e] = y[e];
+                for (int v4 = 0; v4 < 3; ++v4)
+                    reinterpret_cast<float4 *>(o)[v4] =
+                        make_float4(y[4 * v4], y[4 * v4 + 1], y[4 * v4 + 2], y[4 * v4 + 3]);
+            } else {
+#pragma unroll
+                for (int v2 = 0; v2 < 6; ++v2)
+                    reinterpret_cast<double2 *>(o)[v2] = make_double2(y[2 * v2], y[2 * v2 + 1]);
+            }
         }
     }
 }

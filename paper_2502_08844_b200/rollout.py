@@ -189,7 +189,9 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
         return (normalizer.apply(x) if normalizer is not None else x).to(f32)
 
     def prep_policy(x):  # ppo._prep_policy_obs (ppo.py:278-285)
-        return pixel_normalize(x) if pixel_policy else prep(policy_normalizer, x)
+        if pixel_policy:  # NCHW view of an NHWC (channels_last) tensor: 2x faster cuDNN convs
+            return pixel_normalize(x, channels_first=False).permute(0, 3, 1, 2)
+        return prep(policy_normalizer, x)
 
     with torch.no_grad():
         for t in range(T):
@@ -265,7 +267,7 @@ def evaluate_device(policy, env, cfg, episodes: int | None = None, max_steps: in
         while steps < limit:
             x = obs[cfg.policy_obs_key]
             if pixel_policy:
-                x = pixel_normalize(x)
+                x = pixel_normalize(x, channels_first=False).permute(0, 3, 1, 2)
             else:
                 x = (policy_normalizer.apply(x) if policy_normalizer is not None else x)
                 x = x.to(torch.float32)
