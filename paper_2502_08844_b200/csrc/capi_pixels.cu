@@ -77,10 +77,10 @@ int dk_pixels_stack(int dtype, int64_t n, int w, int h, double pole_length,
     if (n == 0) return DK_OK;
     cudaStream_t st = (cudaStream_t)stream;
     if (dtype == DK_F64)
-        dk::pixel_stack_kernel<double><<<(unsigned)n, 256, 0, st>>>(
+        dk::pixel_stack_kernel<double><<<(unsigned)n, dk::kPixStackThreads, 0, st>>>(
             n, w, h, pole_length, (const dk::PixFrame *)history, visuals, (double *)out);
     else
-        dk::pixel_stack_kernel<float><<<(unsigned)n, 256, 0, st>>>(
+        dk::pixel_stack_kernel<float><<<(unsigned)n, dk::kPixStackThreads, 0, st>>>(
             n, w, h, pole_length, (const dk::PixFrame *)history, visuals, (float *)out);
     return cuda_rc(cudaGetLastError(), "pixels stack launch");
 }

@@ -146,58 +146,179 @@ __device__ __forceinline__ void store12(double *o, const double *v) {
     for (int k = 0; k < 6; ++k) d[k] = make_double2(v[2 * k], v[2 * k + 1]);
 }
 
+// Per-world shared scratch of the stack kernels.  The exact per-pixel test
+// (pix_class_pre, float64 in the reference's order) runs only where its answer
+// is not already decided by per-row / per-column facts:
+//  * cart: |wx - x| <= 0.18 depends on the column only, |wy| <= 0.11 on the row
+//    only -- the same float64 tests, evaluated w * 3 + h times per world;
+//  * pole: a pixel can be pole only if its row is within 0.0225 of the
+//    segment's y extent and its line distance is <= 0.0225, i.e.
+//    |(wx - x) d1 - ry d0| <= 0.0225 sqrt(seg): per (frame, row) a column
+//    interval, computed in float64 and widened by two columns, outside which
+//    the exact test can only answer "not pole".  Inside it the exact test
+//    decides, so the classes are unchanged.
+struct StackScratch {
+    double g[3];  // gray level of background / cart / pole
+    double wxs[kMaxView], wys[kMaxView];
+    PoleSeg ps[3];
+    uint8_t cart_col[3][kMaxView], cart_row[kMaxView];
+    uint8_t row_any[kMaxView];  // 0: every pixel of the row is background in all three frames
+    int16_t pole_lo[3][kMaxView], pole_hi[3][kMaxView];  // candidate columns (inclusive)
+};
+
+// candidate columns [lo, hi] of frame f's pole on the view row whose world y is wy
+__device__ __forceinline__ void pole_cols(const PoleSeg &g, double wy, const double *v, int w,
+                                          double scale, int &lo, int &hi) {
+    const double ry = wy - g.p1;
+    const double R = 0.045 / 2 * sqrt(g.seg) * (1.0 + 1e-6) + 1e-300;
+    lo = 0;  // default (non-finite inputs): every column exact
+    hi = w - 1;
+    if (!(isfinite(g.x) && isfinite(g.d0) && isfinite(g.d1) && isfinite(ry))) return;
+    // rows farther than the radius from the segment's y extent [0, d1]: no pole
+    const double ry_lo = fmin(0.0, g.d1) - (0.045 / 2 * (1.0 + 1e-6) + 1e-9);
+    const double ry_hi = fmax(0.0, g.d1) + (0.045 / 2 * (1.0 + 1e-6) + 1e-9);
+    if (ry < ry_lo || ry > ry_hi) {
+        lo = 1;
+        hi = 0;
+        return;
+    }
+    if (g.d1 != 0.0) {
+        const double ctr = g.x + ry * g.d0 / g.d1, half = R / fabs(g.d1);
+        const double cl = (ctr - half - v[9]) * scale + 0.5 * w - 0.5;
+        const double ch = (ctr + half - v[9]) * scale + 0.5 * w - 0.5;
+        if (cl == cl && ch == ch) {
+            lo = cl < -8.0 ? 0 : (cl > w + 8.0 ? w : max(0, (int)floor(cl) - 2));
+            hi = ch > w + 8.0 ? w - 1 : (ch < -8.0 ? -1 : min(w - 1, (int)ceil(ch) + 2));
+        }
+    } else if (fabs(ry * g.d0) > R * (1.0 + 1e-6)) {
+        lo = 1;  // horizontal pole off this row: no candidate
+        hi = 0;
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void draw_stack(int w, int h, double pole_len, const double *v,
-                                           const PixFrame *fr, double *g, double *wxs,
-                                           double *wys, PoleSeg *ps, T *o) {
-    for (int c = threadIdx.x; c < w; c += blockDim.x) wxs[c] = view_wx(v, w, c);
-    for (int r = threadIdx.x; r < h; r += blockDim.x) wys[r] = view_wy(v, w, h, r);
-    if (threadIdx.x < 3) {
-        g[threadIdx.x] = gray_of(v + 3 * threadIdx.x, v[12]);
-        ps[threadIdx.x] = pole_seg(fr[threadIdx.x], pole_len);
+                                           const PixFrame *fr, StackScratch &S, T *o) {
+    // one set-up phase (a single barrier): column facts, row facts (incl. the
+    // pole's candidate columns of the three frames), gray levels, segments
+    const double scale = (double)w / (2.0 * 2.4) * v[11];
+    for (int idx = threadIdx.x; idx < w + h; idx += blockDim.x) {
+        if (idx < w) {
+            const double wx = view_wx(v, w, idx);
+            S.wxs[idx] = wx;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                S.cart_col[k][idx] = fabs(__dsub_rn(wx, fr[k].x)) <= 0.36 / 2;
+        } else {
+            const int r = idx - w;
+            const double wy = view_wy(v, w, h, r);
+            S.wys[r] = wy;
+            const bool cart_r = fabs(__dsub_rn(wy, 0.0)) <= 0.22 / 2;
+            S.cart_row[r] = cart_r;
+            bool any = cart_r;
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                int lo, hi;
+                pole_cols(pole_seg(fr[k], pole_len), wy, v, w, scale, lo, hi);
+                S.pole_lo[k][r] = (int16_t)lo;
+                S.pole_hi[k][r] = (int16_t)hi;
+                any = any || lo <= hi;
+            }
+            S.row_any[r] = any;
+        }
+    }
+    if (threadIdx.x >= blockDim.x - 3) {
+        const int k = threadIdx.x - (blockDim.x - 3);
+        S.g[k] = gray_of(v + 3 * k, v[12]);
+        S.ps[k] = pole_seg(fr[k], pole_len);
     }
     __syncthreads();
+    const T g0 = (T)S.g[0], g1 = (T)S.g[1], g2 = (T)S.g[2];
+    auto cls_of = [&](int k, int row, int col, double wy) {
+        int cls = S.cart_col[k][col] & S.cart_row[row];
+        if (col >= S.pole_lo[k][row] && col <= S.pole_hi[k][row])
+            cls = pix_class_pre(S.wxs[col], wy, S.ps[k]);
+        return cls;
+    };
     if ((w & 3) == 0) {
-        // four pixels of a row per thread: 12 consecutive values, stored as
-        // three 16-byte (float) or six 16-byte (double) vectors
+        // four pixels of a row per thread: the 12 (pixel, frame) classes packed
+        // two bits each from the row / column facts, the few pole candidates
+        // then resolved exactly in one loop over their bits (one divergent
+        // region per thread instead of twelve); 12 consecutive values stored
+        // as three 16-byte (float) or six 16-byte (double) vectors
         for (int q = threadIdx.x; q < (w * h) >> 2; q += blockDim.x) {
             const int p = q << 2, row = p / w, col = p - row * w;
-            const double wy = wys[row];
+            if (!S.row_any[row]) {  // most rows: background in every frame
+                T vals[12];
+#pragma unroll
+                for (int b = 0; b < 12; ++b) vals[b] = g0;
+                store12(o + 3 * p, vals);
+                continue;
+            }
+            const uint32_t cr = S.cart_row[row];
+            uint32_t packed = 0, cand = 0;  // bit pair / bit (3 * j + k)
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const uint32_t cc = *reinterpret_cast<const uint32_t *>(&S.cart_col[k][col]) &
+                                    (cr ? 0x01010101u : 0u);
+                const int lo = S.pole_lo[k][row], hi = S.pole_hi[k][row];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    packed |= ((cc >> (8 * j)) & 1u) << (2 * (3 * j + k));
+                    cand |= (uint32_t)(col + j >= lo && col + j <= hi) << (3 * j + k);
+                }
+            }
+            if (cand) {
+                const double wy = S.wys[row];
+                do {
+                    const int b = __ffs(cand) - 1;
+                    cand &= cand - 1;
+                    const int j = b / 3, k = b - 3 * j;
+                    const uint32_t cls = (uint32_t)pix_class_pre(S.wxs[col + j], wy, S.ps[k]);
+                    packed = (packed & ~(3u << (2 * b))) | (cls << (2 * b));
+                } while (cand);
+            }
             T vals[12];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int k = 0; k < 3; ++k)
-                    vals[3 * j + k] = (T)g[pix_class_pre(wxs[col + j], wy, ps[k])];
+            for (int b = 0; b < 12; ++b) {
+                const uint32_t cls = (packed >> (2 * b)) & 3u;
+                vals[b] = cls == 0 ? g0 : (cls == 1 ? g1 : g2);
+            }
             store12(o + 3 * p, vals);
         }
         return;
     }
     for (int p = threadIdx.x; p < w * h; p += blockDim.x) {
         const int row = p / w, col = p - row * w;
-        const double wx = wxs[col], wy = wys[row];
+        const double wy = S.wys[row];
 #pragma unroll
-        for (int k = 0; k < 3; ++k) o[3 * p + k] = (T)g[pix_class_pre(wx, wy, ps[k])];
+        for (int k = 0; k < 3; ++k) {
+            const int cls = cls_of(k, row, col, wy);
+            o[3 * p + k] = cls == 0 ? g0 : (cls == 1 ? g1 : g2);
+        }
     }
 }
 
 // One CTA per world: threads stride over the h*w pixels; each pixel's three
 // stacked frames (oldest first) are written as three consecutive values.
+#ifndef DK_PIXSTACK_THREADS
+#define DK_PIXSTACK_THREADS 64
+#define DK_PIXSTACK_MINB 16
+#endif
+constexpr int kPixStackThreads = DK_PIXSTACK_THREADS;
 template <typename T>
-__global__ void __launch_bounds__(256, 4) pixel_stack_kernel(int64_t n, int w, int h, double pole_len,
+__global__ void __launch_bounds__(DK_PIXSTACK_THREADS, DK_PIXSTACK_MINB) pixel_stack_kernel(int64_t n, int w, int h, double pole_len,
                                    const PixFrame *__restrict__ hist, const double *__restrict__ vis,
                                    T *__restrict__ out) {
     const int64_t i = blockIdx.x;
     if (i >= n) return;
-    __shared__ double g[3];  // gray level of background / cart / pole
     __shared__ double v[kVis];
     __shared__ PixFrame fr[3];
-    __shared__ PoleSeg ps[3];
-    __shared__ double wxs[kMaxView], wys[kMaxView];
+    __shared__ StackScratch S;
     if (threadIdx.x < kVis) v[threadIdx.x] = vis[i * kVis + threadIdx.x];
     if (threadIdx.x < 3) fr[threadIdx.x] = hist[i * 3 + threadIdx.x];
     __syncthreads();
-    draw_stack<T>(w, h, pole_len, v, fr, g, wxs, wys, ps, out + i * (int64_t)w * h * 3);
+    draw_stack<T>(w, h, pole_len, v, fr, S, out + i * (int64_t)w * h * 3);
 }
 
 // batch_render + brightness_postprocess: RGB uint8 [n, h, w, 3] of one frame.
@@ -300,18 +421,16 @@ __global__ void pixel_terminal_kernel(int64_t n, int w, int h, double pole_len, 
                                       const double *__restrict__ vis, T *__restrict__ out) {
     const int64_t i = blockIdx.x;
     if (i >= n || !mask[i]) return;
-    __shared__ double g[3];
     __shared__ double v[kVis];
     __shared__ PixFrame fr[3];
-    __shared__ PoleSeg ps[3];
-    __shared__ double wxs[kMaxView], wys[kMaxView];
+    __shared__ StackScratch S;
     if (threadIdx.x < kVis) v[threadIdx.x] = vis[i * kVis + threadIdx.x];
     if (threadIdx.x < 2) fr[threadIdx.x] = hist[i * 3 + 1 + threadIdx.x];
     if (threadIdx.x == 2)
         fr[2] = PixFrame{(double)term_obs[i * obs_dim], (double)term_obs[i * obs_dim + 1],
                          (double)term_obs[i * obs_dim + 2]};
     __syncthreads();
-    draw_stack<T>(w, h, pole_len, v, fr, g, wxs, wys, ps, out + i * (int64_t)w * h * 3);
+    draw_stack<T>(w, h, pole_len, v, fr, S, out + i * (int64_t)w * h * 3);
 }
 
 // ppo.pixel_normalize (ppo.py:232-238): per-sample, per-channel
