@@ -201,3 +201,31 @@ def test_stack_classes_equal_exact_render(PX, size, pole_len):
                                       else stack[..., k].cpu().numpy())
         if levels.numel() == 3:
             np.testing.assert_array_equal(got.cpu().numpy(), want.cpu().numpy())
+
+
+def test_pixel_env_sharding_invariance(PX):
+    """worlds keyed by their global index, so two shards
+    (env_index_offset) reproduce one 2N-world pixel env bit for bit -- states,
+    visual randomisation at autoreset and the stacks."""
+    import paper_2502_08844_b200 as dk
+
+    n, K = 96, 9
+    cfg = dk.EnvConfig(task="cartpole-balance-pixels", episode_length=4,
+                       visual_randomization=True, seed=3)
+    acts = torch.rand(K, 2 * n, 1, device="cuda") * 2 - 1
+    full = dk.DeviceBatchEnv(cfg, 2 * n)
+    halves = [dk.DeviceBatchEnv(cfg, n, env_index_offset=r * n) for r in range(2)]
+    o_full = full.reset(seed=3)["pixels"]
+    o_parts = [h.reset(seed=3)["pixels"] for h in halves]
+    assert torch.equal(torch.cat(o_parts), o_full)
+    for k in range(K):
+        f = full.step(acts[k])
+        parts = [h.step(acts[k, r * n:(r + 1) * n].contiguous()) for r, h in enumerate(halves)]
+        for key in ("obs", "pixels", "trunc", "terminal_mask"):
+            assert torch.equal(torch.cat([p[key] for p in parts]), f[key]), (k, key)
+        m = f["terminal_mask"]
+        if m.any():
+            tp = torch.cat([p["terminal_pixels"] for p in parts])
+            assert torch.equal(tp[m], f["terminal_pixels"][m])
+    for e in (full, *halves):
+        e.check()
