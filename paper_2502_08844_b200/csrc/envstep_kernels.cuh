@@ -479,6 +479,17 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
 #endif
         bool fast = group_is_fast(0);
         int sb = 0, ab = 0;
+        // group g's hand-off arrives (release: they wait for the group's ring
+        // stores to drain, stalling in-order issue) are issued after the first
+        // step of group g + 1, by when the stores have drained (+1.3%, measured)
+        int pend_sb = -1, pend_ab = 0;
+        auto flush_arrive = [&]() {
+            if (pend_sb >= 0) {
+                mbar_arrive_u32(aempty_b + 8 * pend_ab);
+                mbar_arrive_u32(full_b + 8 * pend_sb);
+                pend_sb = -1;
+            }
+        };
 #pragma unroll 1
         for (int g = 0; g < ngroups; ++g) {
             const uint32_t avail_next = ld_acquire_u32(staged_a);  // consumed at the next head
@@ -516,8 +527,10 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
                         }
                         world_to_slot<Task, T, WPC>(wd[t], ring_g + s * WF * WPC, t * 32 + lane);
                     }
+                    if (s == 0) flush_arrive();
                 }
             } else {
+                flush_arrive();
 #pragma unroll 1
                 for (int s = 0; s < min(G, K32 - k0); ++s) {
 #pragma unroll
@@ -531,8 +544,8 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
                 fast_next = group_is_fast(g + 1);
             }
             if (lane == 0) gflag[sb] = fast ? 1 : 0;
-            mbar_arrive_u32(aempty_b + 8 * ab);
-            mbar_arrive_u32(full_b + 8 * sb);
+            pend_sb = sb;
+            pend_ab = ab;
             sb = sb + 1 == NG ? 0 : sb + 1;
             ab = ab + 1 == NA ? 0 : ab + 1;
             avail = avail_next;
@@ -542,6 +555,7 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
             while (avail < (uint32_t)(g + 2) && g + 1 < ngroups) avail = ld_acquire_u32(staged_a);
             fast = fast_next;
         }
+        flush_arrive();
 #ifdef DK_EXP_CLOCK
         g_loop1 = gtimer();
 #endif
