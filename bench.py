@@ -342,6 +342,9 @@ def run_b200(args, rank, world, local_rank, dist):
     tail = None
     if not args.no_tail:
         tail = bench_go1_tail(args, dev, rank)
+    loco_small = None
+    if rank == 0 and not args.no_extra:
+        loco_small = bench_loco_small(args, dev)
     dropin = sweep = ppo_rollout = pixels = tasks = None
     if rank == 0 and not args.no_extra:
         dropin = bench_dropin_step(args, dev)
@@ -378,6 +381,7 @@ def run_b200(args, rank, world, local_rank, dist):
             "e2e": e2e,
             "gpu_launches": gpu_launches,
             "go1_tail": tail,
+            "loco_small": loco_small,
             "e2e_dropin_step": dropin,
             "sweep": sweep,
             "ppo_rollout": ppo_rollout,
@@ -656,6 +660,90 @@ def synthetic_frames(R, J, F, dev, dtype, seed):
     for k, v in f.items():
         f[k] = v.to(torch.uint8) if v.dtype == torch.bool else v.to(dtype)
     return f
+
+
+def bench_loco_small(args, dev, reps=50):
+    """SURVEY §8a B4-B7 at Go1 shape (12 joints, 4 feet), 8192 worlds, float32,
+    through the Python API (locomotion.*): device time per call with CUDA events
+    around `reps` back-to-back calls.  These are one-pass elementwise kernels of a
+    few hundred bytes per world: at 8192 worlds a call moves ~1-3 MB, so they are
+    launch-bound (a few microseconds), not bandwidth-bound."""
+    import torch
+
+    from paper_2502_08844_b200 import locomotion as L
+
+    n, J, F = args.num_envs, 12, 4
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    r = lambda *s: torch.rand(*s, generator=g, device=dev) * 2 - 1  # noqa: E731
+    a, prev, q, qd = r(n, J), r(n, J), r(n, J), r(n, J)
+    pd = L.PDParams(kp=20.0, kd=0.5, action_scale=0.3, q_default=[0.1] * J, mode="relative",
+                    torque_limit=30.0)
+    phi, raw, hist = r(n, F) * 3, r(n), torch.zeros(n, device=dev)
+    obs = {"state": r(n, 56), "privileged_state": r(n, 75)}
+
+    class Spec:
+        def __init__(self, slot, scale, kind):
+            self.slot, self.scale, self.kind = slot, scale, kind
+
+    specs = [Spec("state", 0.05, "uniform"), Spec("state", 0.02, "gaussian")]
+    key = L.NoiseKey(seed=1)
+    dl = L.DelayLineBatch(n, J, 0, 3, per_step=False, dtype=torch.float32, device=dev)
+    dl.reset(key)
+    cases = {
+        "B5 pd_batch (action_to_target + pd_torque)": (lambda: L.pd_batch(a, prev, q, qd, pd),
+                                                       4 * J * 4 + 2 * J * 4),
+        "B4 advance_phase_batch (+ phase_encode)": (lambda: L.advance_phase_batch(phi, 1.5, 0.02),
+                                                    F * 4 + 3 * F * 4),
+        "B6 progress_clip_reward_batch": (lambda: L.progress_clip_reward_batch(raw, hist), 16),
+        "B7 apply_sensor_noise_batch (uniform + gaussian, 56-d state)":
+            (lambda: L.apply_sensor_noise_batch(obs, specs, key), 2 * 56 * 4 + 2 * 75 * 4),
+        "B7 DelayLineBatch.push_pop (12-d, delay <= 3)": (lambda: dl.push_pop(a), 2 * J * 4 * 2),
+    }
+    out = {}
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for name, (fn, bpw) in cases.items():
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(reps):
+            fn()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        us = e0.elapsed_time(e1) / reps * 1e3
+        # the same call captured once in a CUDA graph and replayed: device time
+        # without the Python wrapper's host overhead
+        gus = None
+        if "DelayLine" not in name:  # (push_pop advances host-side ring bookkeeping)
+            try:
+                side = torch.cuda.Stream(device=dev)
+                side.wait_stream(torch.cuda.current_stream(dev))
+                with torch.cuda.stream(side):
+                    fn()
+                torch.cuda.current_stream(dev).wait_stream(side)
+                graph = torch.cuda.CUDAGraph()
+                with torch.cuda.graph(graph):
+                    for _ in range(10):
+                        fn()
+                graph.replay()
+                torch.cuda.synchronize(dev)
+                e0.record()
+                for _ in range(reps // 10):
+                    graph.replay()
+                e1.record()
+                torch.cuda.synchronize(dev)
+                gus = e0.elapsed_time(e1) / (reps // 10 * 10) * 1e3
+            except Exception:  # pragma: no cover
+                gus = None
+        out[name] = {"us_per_call": us, "world_steps_per_s": n / (us / 1e6),
+                     "graph_us_per_call": gus,
+                     "graph_world_steps_per_s": None if gus is None else n / (gus / 1e6),
+                     "alg_bytes_per_world": bpw,
+                     "graph_achieved_GBps": None if gus is None else n * bpw / (gus / 1e6) / 1e9}
+    return {"worlds": n, "dtype": "f32", "note": "device time per call through the Python API "
+            "(host-bound at this size), and per call replayed from a CUDA graph (kernel-bound: "
+            "a few microseconds of launch for ~0.1-8 MB of traffic)", "primitives": out}
 
 
 def bench_go1_tail(args, dev, rank):

@@ -308,6 +308,96 @@ __global__ void sensor_noise_kernel(int64_t n, int dim, T *obs, int nspec, const
     }
 }
 
+// The same draws with one warp per world.  Philox is counter-based: word q of
+// a world's stream is word q % 4 of the block whose counter is step + 1 + q / 4
+// (NumPy bumps the 256-bit counter before each block), so the 32 lanes compute
+// 32 consecutive words at once.  Uniform draws take one word each; Gaussian
+// draws are speculated one word each (the ziggurat's first test accepts ~99%)
+// and, from the first lane whose draw needs more, finished by lane 0 with the
+// sequential generator positioned at that word (tail / wedge, exact).
+__device__ __forceinline__ void philox_seek(Philox4x64 &r, uint64_t seed, uint64_t env,
+                                            uint32_t episode, uint64_t step, uint64_t q) {
+    r.init(seed, env, episode, step);
+    const uint64_t b = q >> 2;
+    const uint64_t c0 = step + 1 + b;
+    r.ctr[0] = c0;
+    r.ctr[1] = c0 < step ? 1 : 0;  // carry (counter words 2, 3 stay 0 for any sane q)
+    r.block();
+    r.pos = (int)(q & 3);
+}
+__device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t env, uint32_t episode,
+                                                uint64_t step, uint64_t q) {
+    Philox4x64 r;
+    philox_seek(r, seed, env, episode, step, q);
+    return r.buf[q & 3];
+}
+
+template <typename T>
+__global__ void __launch_bounds__(128) sensor_noise_warp_kernel(
+    int64_t n, int dim, T *obs, int nspec, const int *off, const int *len, const double *scale,
+    const int *kind, uint64_t seed, int64_t env0, const uint32_t *episode, uint64_t step) {
+    const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const uint64_t env = (uint64_t)(env0 + i);
+    const uint32_t ep = episode ? episode[i] : 0u;
+    T *row = obs + i * dim;
+    uint64_t pos = 0;  // next unread word of the world's stream
+    for (int s = 0; s < nspec; ++s) {
+        const double sc = scale[s];
+        if (sc == 0.0) continue;
+        const int L = len[s];
+        T *x = row + off[s];
+        if (kind == nullptr || kind[s] != 1) {  // uniform(-sc, sc): one word per draw
+            const double range = __dsub_rn(sc, -sc);
+            for (int k0 = 0; k0 < L; k0 += 32) {
+                const int k = k0 + lane;
+                if (k < L) {
+                    const uint64_t w = philox_word(seed, env, ep, step, pos + (uint64_t)k);
+                    const double u = __dmul_rn((double)(w >> 11), 1.0 / 9007199254740992.0);
+                    x[k] = (T)__dadd_rn((double)x[k], __dadd_rn(-sc, __dmul_rn(range, u)));
+                }
+            }
+            pos += (uint64_t)L;
+            continue;
+        }
+        int done = 0;  // Gaussian: 0.0 + sc * standard_normal()
+        while (done < L) {
+            const int k = done + lane;
+            const bool act = k < L;
+            bool fast = false;
+            double z = 0.0;
+            if (act) {
+                uint64_t r = philox_word(seed, env, ep, step, pos + (uint64_t)lane);
+                const int idx = (int)(r & 0xff);
+                r >>= 8;
+                const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
+                z = __dmul_rn((double)rabs, __ldg(&dk_zig_wi[idx]));
+                if (r & 1) z = -z;
+                fast = rabs < __ldg(&dk_zig_ki[idx]);
+            }
+            const unsigned slow = __ballot_sync(0xffffffffu, act && !fast);
+            const int nact = min(32, L - done);
+            const int f = slow ? __ffs(slow) - 1 : nact;  // lanes < f are accepted
+            if (lane < f) x[k] = (T)__dadd_rn((double)x[k], __dadd_rn(0.0, __dmul_rn(sc, z)));
+            done += f;
+            pos += (uint64_t)f;
+            if (f < nact) {  // draw `done` needs the tail or wedge: finish it sequentially
+                uint64_t npos = 0;
+                if (lane == 0) {
+                    Philox4x64 r;
+                    philox_seek(r, seed, env, ep, step, pos);
+                    const double zn = r.standard_normal();
+                    x[done] = (T)__dadd_rn((double)x[done], __dadd_rn(0.0, __dmul_rn(sc, zn)));
+                    npos = ((r.ctr[0] - step - 1) << 2) + (uint64_t)r.pos;
+                }
+                pos = __shfl_sync(0xffffffffu, npos, 0);
+                done += 1;
+            }
+        }
+    }
+}
+
 // randomize_params (randomization.py:156-181) for n worlds, f64: out [n, F]
 // starts as nominal [F]; ranges r (spec order) perturb field[r] with
 // distribution 0 additive base + U(lo, hi), 1 multiplicative base * U(lo, hi),
@@ -483,7 +573,7 @@ cudaError_t launch_sensor_noise(int64_t n, int dim, T *obs, int nspec, const int
                                 uint64_t seed, int64_t env0, const uint32_t *episode,
                                 uint64_t step, cudaStream_t st) {
     if (n == 0) return cudaSuccess;
-    sensor_noise_kernel<T><<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+    sensor_noise_warp_kernel<T><<<(unsigned)((n * 32 + 127) / 128), 128, 0, st>>>(
         n, dim, obs, nspec, off, len, scale, kind, seed, env0, episode, step);
     return cudaGetLastError();
 }

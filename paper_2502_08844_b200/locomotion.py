@@ -150,6 +150,20 @@ def _stream(dev):
     return ctypes.c_void_p(_torch().cuda.current_stream(dev).cuda_stream)
 
 
+_CONST_CACHE: dict = {}
+
+
+def _const(key, make):
+    """Small per-call constant tensors (joint defaults, noise-spec tables) cached on
+    the device by value, so repeated calls issue no host-to-device copies."""
+    t = _CONST_CACHE.get(key)
+    if t is None:
+        if len(_CONST_CACHE) > 256:
+            _CONST_CACHE.clear()
+        t = _CONST_CACHE[key] = make()
+    return t
+
+
 def _key(key: NoiseKey, n_worlds, dev):
     torch = _torch()
     ep = None
@@ -322,7 +336,9 @@ def pd_batch(action, prev_target, q, qd, p: PDParams):
     dt = a.dtype
     n, J = a.shape
     dev = a.device
-    qdef = torch.as_tensor(np.asarray(p.q_default, dtype=np.float64), device=dev).to(dt)
+    qd64 = tuple(float(v) for v in np.asarray(p.q_default, dtype=np.float64).reshape(-1))
+    qdef = _const(("qdef", qd64, str(dev), str(dt)),
+                  lambda: torch.tensor(qd64, dtype=torch.float64, device=dev).to(dt))
     if qdef.shape != (J,):
         raise InvalidInputError("q_default must have one entry per joint")
     q = q.to(dt).contiguous()
@@ -344,8 +360,14 @@ def advance_phase_batch(phi, frequency, dt):
     torch = _torch()
     phi = phi.contiguous()
     n, F = phi.shape
-    fr = torch.as_tensor(frequency, device=phi.device, dtype=phi.dtype).expand(n).contiguous()
-    d = torch.as_tensor(dt, device=phi.device, dtype=phi.dtype).expand(n).contiguous()
+    def per_world(v, tag):
+        if isinstance(v, (int, float)):
+            return _const((tag, float(v), n, str(phi.device), str(phi.dtype)),
+                          lambda: torch.full((n,), float(v), device=phi.device, dtype=phi.dtype))
+        return torch.as_tensor(v, device=phi.device, dtype=phi.dtype).expand(n).contiguous()
+
+    fr = per_world(frequency, "freq")
+    d = per_world(dt, "dt")
     out = torch.empty_like(phi)
     cs = torch.empty((n, F, 2), device=phi.device, dtype=phi.dtype)
     _check(nat.lib().dk_loco_phase(_dtype_code(phi), n, F, _ptr(phi), _ptr(fr), _ptr(d),
@@ -402,11 +424,16 @@ def apply_sensor_noise_batch(obs: dict, specs, key: NoiseKey):
         flat.append(t)
     buf = torch.cat(flat, 1).contiguous()
     dev = first.device
-    off = torch.tensor([offs[s.slot][0] for s in specs], dtype=torch.int32, device=dev)
-    ln = torch.tensor([offs[s.slot][1] for s in specs], dtype=torch.int32, device=dev)
-    sc = torch.tensor([float(s.scale) for s in specs], dtype=torch.float64, device=dev)
-    kd = torch.tensor([_NOISE_KINDS[getattr(s, "kind", "uniform")] for s in specs],
-                      dtype=torch.int32, device=dev)
+    table = tuple((offs[s.slot][0], offs[s.slot][1], float(s.scale),
+                   _NOISE_KINDS[getattr(s, "kind", "uniform")]) for s in specs)
+
+    def make_tables():
+        return (torch.tensor([t[0] for t in table], dtype=torch.int32, device=dev),
+                torch.tensor([t[1] for t in table], dtype=torch.int32, device=dev),
+                torch.tensor([t[2] for t in table], dtype=torch.float64, device=dev),
+                torch.tensor([t[3] for t in table], dtype=torch.int32, device=dev))
+
+    off, ln, sc, kd = _const(("noise", table, str(dev)), make_tables)
     kc, ep = _key(key, n, dev)
     _check(nat.lib().dk_dr_sensor_noise(_dtype_code(buf), n, buf.shape[1], _ptr(buf), len(specs),
                                         _ptr(off), _ptr(ln), _ptr(sc), _ptr(kd),
