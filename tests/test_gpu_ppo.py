@@ -108,3 +108,24 @@ def test_normalizer_large_vs_oracle(P):
     assert gc == c
     np.testing.assert_allclose(gm, m, rtol=1e-12, atol=1e-14)
     np.testing.assert_allclose(gv, v, rtol=1e-12)
+
+
+@pytest.mark.parametrize("dt", ["float32", "float64"])
+@pytest.mark.parametrize("T,N", [(77, 36), (1, 4), (64, 100), (33, 8)])
+def test_gae_ragged_vs_oracle(P, dt, T, N):
+    """GAE on ragged shapes (T not a multiple of the kernel's 16-step register
+    chunks, partial 128-world blocks, frequent terminations), both dtypes;
+    bit-exact against the oracle."""
+    from oracle import ppo as orc
+
+    npdt = np.float32 if dt == "float32" else np.float64
+    tdt = torch.float32 if dt == "float32" else torch.float64
+    rng = np.random.default_rng(T * 1000 + N)
+    r = rng.normal(0, 1, (T, N)).astype(npdt)
+    v = rng.normal(0, 1, (T, N)).astype(npdt)
+    d = (rng.uniform(size=(T, N)) < 0.05).astype(npdt)
+    b = rng.normal(0, 1, N).astype(npdt)
+    adv, ret = P.compute_gae_batch(_t(r, tdt), _t(v, tdt), _t(b, tdt), _t(d, tdt), 0.99, 0.95)
+    ra, rr = orc.gae(r, v, b, d, 0.99, 0.95)
+    np.testing.assert_array_equal(adv.cpu().numpy(), ra.astype(npdt))
+    np.testing.assert_array_equal(ret.cpu().numpy(), rr.astype(npdt))
