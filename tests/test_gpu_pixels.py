@@ -229,3 +229,27 @@ def test_pixel_env_sharding_invariance(PX):
             assert torch.equal(tp[m], f["terminal_pixels"][m])
     for e in (full, *halves):
         e.check()
+
+
+@pytest.mark.parametrize("shape,levels", [((40, 64, 64, 3), 3), ((33, 64, 64, 3), 0),
+                                          ((5, 7, 9, 3), 2), ((3, 64, 64, 3), 1)])
+def test_pixel_normalize_float32_stacks_vs_oracle(PX, shape, levels):
+    """The float32 3-channel path on rendered-like stacks (`levels` gray levels,
+    long runs, constant channels) and on fully random values (levels 0: a run
+    boundary at every pixel), ragged sizes; bit-exact against the oracle."""
+    from oracle import ppo as orc
+
+    rng = np.random.default_rng(sum(shape) + levels)
+    if levels == 0:
+        x = rng.uniform(0, 1, shape).astype(np.float32)
+    else:
+        lv = rng.uniform(0, 1, levels).astype(np.float32)
+        idx = (rng.uniform(size=shape) < 0.2).astype(np.int64) * rng.integers(0, levels, shape)
+        x = lv[idx]
+    want = orc.pixel_normalize(x)
+    t = torch.as_tensor(x, device="cuda")
+    y = PX.pixel_normalize(t, channels_first=False, out_dtype=torch.float64)
+    np.testing.assert_array_equal(y.cpu().numpy(), want)
+    pol = PX.pixel_normalize(t)
+    np.testing.assert_array_equal(pol.cpu().numpy(),
+                                  np.ascontiguousarray(np.moveaxis(want, -1, 1)).astype(np.float32))

@@ -9,7 +9,16 @@ import torch  # noqa: E402
 from paper_2502_08844_b200 import pixels
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 8192
-x = torch.rand(n, 64, 64, 3, device="cuda")
+if len(sys.argv) > 2 and sys.argv[2] == "env":  # rendered stacks from the pixel env
+    import paper_2502_08844_b200 as dk
+
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance-pixels", visual_randomization=True), n)
+    env.reset(seed=0)
+    for _ in range(3):
+        o = env.step(torch.rand(n, 1, device="cuda") * 2 - 1)
+    x = o["pixels"].clone()
+else:
+    x = torch.rand(n, 64, 64, 3, device="cuda")
 for _ in range(3):
     pixels.pixel_normalize(x)
 torch.cuda.synchronize()
