@@ -12,6 +12,21 @@
 #pragma once
 #include "envmath.cuh"
 
+// Unroll factors of the runtime-sized joint / foot loops (development hooks;
+// unset = the compiler's choice).
+#define DK_PRAGMA_(x) _Pragma(#x)
+#define DK_UNROLL_(n) DK_PRAGMA_(unroll n)
+#ifdef DK_TAIL_UNROLL_J
+#define DK_UNROLL_J DK_UNROLL_(DK_TAIL_UNROLL_J)
+#else
+#define DK_UNROLL_J
+#endif
+#ifdef DK_TAIL_UNROLL_F
+#define DK_UNROLL_F DK_UNROLL_(DK_TAIL_UNROLL_F)
+#else
+#define DK_UNROLL_F
+#endif
+
 namespace dk {
 
 template <typename T>
@@ -123,6 +138,7 @@ loco_tail_kernel(LocoFrames<T> f, const T *__restrict__ prev_action, const T *__
         const T *fpa = f.pact + (int64_t)nj * r;
         const int o_jp = 9, o_jv = 9 + nj, o_pa = 9 + 2 * nj, o_cmd = 9 + 3 * nj;
         const int o_ph = o_cmd + 3, o_con = S, o_tau = S + nf, o_pert = S + nf + nj;
+        DK_UNROLL_J
         for (int j = 0; j < nj; ++j) {
             const T qj = __ldg(q + j), vj = __ldg(qd + j), tj = __ldg(tau + j);
             tt = tt + tj * tj;
@@ -149,6 +165,7 @@ loco_tail_kernel(LocoFrames<T> f, const T *__restrict__ prev_action, const T *__
         const T *phase = f.phase + (int64_t)nf * r;
         const uint8_t *td = f.touchdown + (int64_t)nf * r, *con = f.contact + (int64_t)nf * r;
         const T span = c.airtime_max - c.airtime_min;
+        DK_UNROLL_F
         for (int k = 0; k < nf; ++k) {
             T gain = (__ldg(air + k) - c.airtime_min) * (td[k] ? T(1) : T(0));
             gain = gain < T(0) ? T(0) : (gain > span ? span : gain);  // np.clip
