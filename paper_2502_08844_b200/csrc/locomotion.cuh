@@ -342,12 +342,35 @@ __device__ __forceinline__ void philox_seek(Philox4x64 &r, uint64_t seed, uint64
     r.block();
     r.pos = (int)(q & 3);
 }
-__device__ __forceinline__ uint64_t philox_word(uint64_t seed, uint64_t env, uint32_t episode,
-                                                uint64_t step, uint64_t q) {
-    Philox4x64 r;
-    philox_seek(r, seed, env, episode, step, q);
-    return r.buf[q & 3];
-}
+// The warp's block cache: lane l holds block base + l of the world's stream,
+// i.e. words [4 base, 4 base + 128), so one Philox block per lane serves four
+// 32-word rounds of draws instead of one.
+struct WarpPhiloxCache {
+    uint64_t w0, w1, w2, w3;
+    uint64_t base;  // block index of lane 0's block (warp-uniform)
+    bool valid;
+
+    __device__ __forceinline__ void fill(uint64_t seed, uint64_t env, uint32_t episode,
+                                         uint64_t step, uint64_t b0, int lane) {
+        Philox4x64 r;
+        philox_seek(r, seed, env, episode, step, (b0 + (uint64_t)lane) << 2);
+        w0 = r.buf[0]; w1 = r.buf[1]; w2 = r.buf[2]; w3 = r.buf[3];
+        base = b0;
+        valid = true;
+    }
+    // word q (per lane) of the stream, q in [pos, pos + 32) for a warp-uniform pos;
+    // every lane of the warp must call it.
+    __device__ __forceinline__ uint64_t word(uint64_t seed, uint64_t env, uint32_t episode,
+                                             uint64_t step, uint64_t pos, uint64_t q, int lane) {
+        if (!valid || (pos >> 2) < base || ((pos + 31) >> 2) >= base + 32)
+            fill(seed, env, episode, step, pos >> 2, lane);
+        const int src = (int)((q >> 2) - base);
+        const uint64_t a = __shfl_sync(0xffffffffu, w0, src), b = __shfl_sync(0xffffffffu, w1, src);
+        const uint64_t c = __shfl_sync(0xffffffffu, w2, src), d = __shfl_sync(0xffffffffu, w3, src);
+        const int j = (int)(q & 3);
+        return j == 0 ? a : j == 1 ? b : j == 2 ? c : d;
+    }
+};
 
 template <typename T>
 __global__ void __launch_bounds__(128) sensor_noise_warp_kernel(
@@ -360,6 +383,8 @@ __global__ void __launch_bounds__(128) sensor_noise_warp_kernel(
     const uint32_t ep = episode ? episode[i] : 0u;
     T *row = obs + i * dim;
     uint64_t pos = 0;  // next unread word of the world's stream
+    WarpPhiloxCache cache;
+    cache.valid = false;
     for (int s = 0; s < nspec; ++s) {
         const double sc = scale[s];
         if (sc == 0.0) continue;
@@ -369,8 +394,9 @@ __global__ void __launch_bounds__(128) sensor_noise_warp_kernel(
             const double range = __dsub_rn(sc, -sc);
             for (int k0 = 0; k0 < L; k0 += 32) {
                 const int k = k0 + lane;
+                const uint64_t w = cache.word(seed, env, ep, step, pos + (uint64_t)k0,
+                                              pos + (uint64_t)k, lane);
                 if (k < L) {
-                    const uint64_t w = philox_word(seed, env, ep, step, pos + (uint64_t)k);
                     const double u = __dmul_rn((double)(w >> 11), 1.0 / 9007199254740992.0);
                     x[k] = (T)__dadd_rn((double)x[k], __dadd_rn(-sc, __dmul_rn(range, u)));
                 }
@@ -384,8 +410,8 @@ __global__ void __launch_bounds__(128) sensor_noise_warp_kernel(
             const bool act = k < L;
             bool fast = false;
             double z = 0.0;
+            uint64_t r = cache.word(seed, env, ep, step, pos, pos + (uint64_t)lane, lane);
             if (act) {
-                uint64_t r = philox_word(seed, env, ep, step, pos + (uint64_t)lane);
                 const int idx = (int)(r & 0xff);
                 r >>= 8;
                 const uint64_t rabs = (r >> 1) & 0x000fffffffffffffULL;
