@@ -127,8 +127,17 @@ int dk_pixels_normalize(int in_dtype, int out_dtype, int64_t n, int h, int w, in
             if (e != cudaSuccess) return cuda_rc(e, "pixel_normalize attribute");
             if (dev < 64) __atomic_fetch_or(&attr_set, 1ull << dev, __ATOMIC_RELAXED);
         }
-        dk::pixnorm_stats3_kernel<<<(unsigned)((n + 31) / 32), 96, dk::pixnorm::SMEM, st>>>(
-            n, hw, (const float *)x, stats);
+        // samples per CTA: spread the batch over every SM's two CTA slots (the
+        // stage reads are bound per SM), at most one warp of samples
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        int64_t spc = (n + 2 * (int64_t)sms - 1) / (2 * (int64_t)sms);
+#ifdef DK_PIXNORM_SPC
+        spc = DK_PIXNORM_SPC;
+#endif
+        spc = spc < 1 ? 1 : (spc > 32 ? 32 : spc);
+        dk::pixnorm_stats3_kernel<<<(unsigned)((n + spc - 1) / spc), 96, dk::pixnorm::SMEM, st>>>(
+            n, hw, (int)spc, (const float *)x, stats);
         const dim3 g((unsigned)((hw / 4 + 255) / 256), (unsigned)(n < 65535 ? n : 65535));
         const float *xf = (const float *)x;
         if (out_dtype == DK_F64) {

@@ -511,14 +511,14 @@ __device__ __forceinline__ void pixnorm_chan(const float4 *row, double &a, doubl
 
 // Staging: all 96 threads copy the stage with 16-byte cp.async (each sample's
 // 768-byte run coalesced), NS - 1 stages in flight, two CTA barriers per stage.
-__global__ void __launch_bounds__(96) pixnorm_stats3_kernel(int64_t n, int hw,
+__global__ void __launch_bounds__(96) pixnorm_stats3_kernel(int64_t n, int hw, int spc,
                                                              const float *__restrict__ x,
                                                              double *__restrict__ stats) {
     using namespace pixnorm;
     extern __shared__ __align__(128) unsigned char sm[];
     const int tid = threadIdx.x, lane = tid & 31, c = tid >> 5;
-    const int64_t s0 = (int64_t)blockIdx.x * 32;
-    const int ns = (int)(n - s0 < 32 ? n - s0 : 32);
+    const int64_t s0 = (int64_t)blockIdx.x * spc;  // spc <= 32 samples per CTA
+    const int ns = (int)(n - s0 < spc ? n - s0 : spc);
     const int tiles = hw / PN, total = 2 * tiles;
     const unsigned char *base = reinterpret_cast<const unsigned char *>(x + s0 * (int64_t)hw * 3);
     const int64_t sample_bytes = (int64_t)hw * 12;
