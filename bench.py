@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tail", action="store_true", help="skip the Go1-shape step-tail line")
+    ap.add_argument("--no-f64", action="store_true", help="skip the precision-matched f64 leg")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the drop-in BatchEnv.step and world-count sweep lines")
     return ap.parse_args()
@@ -95,11 +96,24 @@ class ClockSampler:
 
             pynvml.nvmlInit()
             self._nv = pynvml
-            self._h = pynvml.nvmlDeviceGetHandleByIndex(device_index)
+            self._h = self._handle(pynvml, device_index)
             self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
         except Exception as e:  # pragma: no cover - no NVML
             self._nv = None
             self.error = str(e)
+
+    @staticmethod
+    def _handle(nv, device_index):
+        """NVML handle of the CUDA device by PCI bus id (NVML's enumeration
+        ignores CUDA_VISIBLE_DEVICES, so an index could name another GPU)."""
+        try:
+            import torch
+
+            p = torch.cuda.get_device_properties(device_index)
+            bus = f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+            return nv.nvmlDeviceGetHandleByPciBusId(bus.encode())
+        except Exception:
+            return nv.nvmlDeviceGetHandleByIndex(device_index)
 
     def _run(self):
         nv = self._nv
@@ -113,6 +127,12 @@ class ClockSampler:
             except Exception:
                 pass
             time.sleep(self._period)
+
+    def start(self):
+        return self.__enter__()
+
+    def stop(self):
+        self.__exit__(None, None, None)
 
     def __enter__(self):
         if self._nv is not None:
@@ -249,22 +269,68 @@ def run_reference(args, rank):
                                    f"({cpu_model()}); oracle/oracle.c, the bit-exact C "
                                    "restatement of deskrl BatchEnv.step"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        # what was actually timed: rank 0 alone, num_envs worlds on the host
+        # cores, whatever N the job was launched with
+        "timed_worlds": args.num_envs, "timed_ranks": 1,
     }
     print(json.dumps(line), flush=True)
 
 
-def run_b200(args, rank, world, local_rank, dist):
+class DeviceGate:
+    """dk_stream_gate: the stream waits on a pinned host flag, so the timed
+    region (events + launches) is fully enqueued before the device starts it
+    and host submission latency stays outside the events."""
+
+    def __init__(self):
+        import torch
+
+        from paper_2502_08844_b200 import _native
+
+        self._lib = _native.lib()
+        self.flag = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+
+    def close(self, stream):
+        self.flag[0] = 0
+        # ~5e6 polls (seconds) as a safety valve: the device never hangs on it
+        rc = self._lib.dk_stream_gate(self.flag.data_ptr(), 5_000_000, stream.cuda_stream)
+        if rc != 0:
+            raise RuntimeError("dk_stream_gate failed")
+
+    def open(self):
+        self.flag[0] = 1
+
+
+_GATE = None
+
+
+def gated_region(fn, stream, dev):
+    """Enqueue gate, start event, fn()'s launches, end event; release; return ms."""
+    import torch
+
+    global _GATE
+    if _GATE is None:
+        _GATE = DeviceGate()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _GATE.close(stream)
+    t0.record(stream)
+    fn()
+    t1.record(stream)
+    _GATE.open()
+    torch.cuda.synchronize(dev)
+    return t0.elapsed_time(t1)
+
+
+def measure_rollout(args, dtype, dev, rank, world, dist, local_rank):
+    """The headline measurement for one real type: W warm-up steps, L2 flush,
+    then exactly K steps of every world as fused rollout launches, behind a
+    device gate, timed with CUDA events on the launching stream, max over ranks."""
     import torch
 
     import paper_2502_08844_b200 as dk
-    from paper_2502_08844_b200 import _native
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
     n = args.num_envs
     cfg = dk.EnvConfig(task=args.task)
-    env = dk.DeviceBatchEnv(cfg, n, dtype=args.dtype, device=local_rank,
-                            env_index_offset=rank * n)
+    env = dk.DeviceBatchEnv(cfg, n, dtype=dtype, device=local_rank, env_index_offset=rank * n)
     A, O, I, NS = env.action_dim, env.obs_dim, len(env.info_keys), env.spec.state_dim
     tdt = env.dtype
     esz = 8 if tdt == torch.float64 else 4
@@ -294,28 +360,27 @@ def run_b200(args, rank, world, local_rank, dist):
     flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
     flush.zero_()  # evict L2 before the timed region
     torch.cuda.synchronize(dev)
+    del flush
 
     nlaunch = (args.steps + U - 1) // U
-    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = env.kernel_launches
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
-    with ClockSampler(local_rank) as clocks:
-        t_start.record(stream)
+
+    def region():
         left = args.steps
         for L in range(nlaunch):
             k = min(U, left)
             launch(j + L, k)  # back to back: events between launches cost 8% (measured)
             left -= k
-        t_end.record(stream)
-        torch.cuda.synchronize(dev)
+
+    elapsed_ms = gated_region(region, stream, dev)
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
     env.check()
     gpu_launches = env.kernel_launches - launches0
-    elapsed_ms = t_start.elapsed_time(t_end)
     if dist is not None:
         t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -328,10 +393,50 @@ def run_b200(args, rank, world, local_rank, dist):
     bpw = bytes_per_world_step(A, O, I, esz)
     alg_bytes_launch = n * U * bpw + n * state_io_bytes(NS, esz) + n * (U // 1000) * O * esz
     # average launch duration over the timed region (device events around the
-    # whole region / launches: includes the inter-launch gaps, so the achieved
-    # bandwidth below is a lower bound for the kernel itself)
+    # whole gated region / launches: includes any inter-launch gaps, so the
+    # achieved bandwidth is a lower bound for the kernel itself)
     avg_launch_s = elapsed_ms / 1e3 * U / args.steps
     achieved = alg_bytes_launch / avg_launch_s / 1e9
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": achieved / peak, "peak_source": peak_src,
+            "traffic": ncu_traffic(args.task, dtype, n, U),
+            "kernel": "rollout_kernel", "alg_bytes_per_launch": alg_bytes_launch,
+            "bytes_per_world_step": bpw, "avg_launch_ms": avg_launch_s * 1e3}
+    return {"env": env, "value": value, "elapsed_ms": elapsed_ms, "gpu_launches": gpu_launches,
+            "roofline": roof, "dims": (A, O, I, esz), "ms_per_step": elapsed_ms / args.steps}
+
+
+def emit_extra(name, obj):
+    """Secondary results go on their own short lines BEFORE the headline line
+    (no top-level "metric" key), so the headline stays the last line."""
+    print(json.dumps({"extra": name, "result": obj}), flush=True)
+
+
+def run_b200(args, rank, world, local_rank, dist):
+    import torch
+
+    from paper_2502_08844_b200 import _native
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n = args.num_envs
+    # NVML clocks: sampled from before the warm-up until after the f64 leg (the
+    # gated headline region itself is only microseconds long at --steps 20)
+    clocks = ClockSampler(local_rank).start()
+    head = measure_rollout(args, args.dtype, dev, rank, world, dist, local_rank)
+    other = "float64" if args.dtype == "float32" else "float32"
+    f_other = None
+    if not args.no_f64:
+        r = measure_rollout(args, other, dev, rank, world, dist, local_rank)
+        r["env"].close()
+        f_other = {"dtype": "f64" if other == "float64" else "f32", "value": r["value"],
+                   "ms_per_step": r["ms_per_step"], "gpu_launches": r["gpu_launches"],
+                   "roofline": {k: r["roofline"][k] for k in
+                                ("achieved", "peak", "frac", "bytes_per_world_step",
+                                 "avg_launch_ms", "traffic")}}
+    clocks.stop()
+    env = head["env"]
+    A, O, I, esz = head["dims"]
 
     # end-to-end through the C ABI with pinned host buffers (H2D actions,
     # D2H every output), chunked and pipelined inside dk_env_rollout_host
@@ -339,19 +444,16 @@ def run_b200(args, rank, world, local_rank, dist):
     if args.e2e_steps > 0:
         e2e = measure_e2e(env, args, dev, dist, A, O, I, esz, world)
 
-    tail = None
+    extras = {}
+    if rank == 0 and not args.no_extra:
+        extras["loco_small"] = bench_loco_small(args, dev)
+        extras["e2e_dropin_step"] = bench_dropin_step(args, dev)
+        extras["sweep"] = bench_sweep(args, dev)
+        extras["all_tasks"] = bench_tasks(args, dev)
+        extras["ppo_rollout"] = bench_ppo_rollout(args, dev)
+        extras["pixels"] = bench_pixels(args, dev)
     if not args.no_tail:
-        tail = bench_go1_tail(args, dev, rank)
-    loco_small = None
-    if rank == 0 and not args.no_extra:
-        loco_small = bench_loco_small(args, dev)
-    dropin = sweep = ppo_rollout = pixels = tasks = None
-    if rank == 0 and not args.no_extra:
-        dropin = bench_dropin_step(args, dev)
-        sweep = bench_sweep(args, dev)
-        tasks = bench_tasks(args, dev)
-        ppo_rollout = bench_ppo_rollout(args, dev)
-        pixels = bench_pixels(args, dev)
+        extras["go1_tail"] = bench_go1_tail(args, dev, rank)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -365,30 +467,23 @@ def run_b200(args, rank, world, local_rank, dist):
             cpu = {"value": None, "error": str(e)}
 
     if rank == 0:
+        for k, v in extras.items():
+            emit_extra(k, v)
         line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps,
+            "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if esz == 4 else "f64",
             "data": "synthetic U(-1,1) actions pre-generated in HBM",
             "config": headline_config(args, world),
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "peak_source": peak_src,
-                         "traffic": ncu_traffic(args.task, args.dtype, n, U),
-                         "kernel": "rollout_kernel", "alg_bytes_per_launch": alg_bytes_launch,
-                         "bytes_per_world_step": bpw, "avg_launch_ms": avg_launch_s * 1e3},
+            "roofline": head["roofline"],
             "cpu_baseline": cpu,
             "e2e": e2e,
-            "gpu_launches": gpu_launches,
-            "go1_tail": tail,
-            "loco_small": loco_small,
-            "e2e_dropin_step": dropin,
-            "sweep": sweep,
-            "ppo_rollout": ppo_rollout,
-            "pixels": pixels,
-            "all_tasks": tasks,
+            "gpu_launches": head["gpu_launches"],
+            "f64" if other == "float64" else "f32": f_other,
             "clocks": clocks.summary(),
-            "library": _native.LIB_PATH,
+            "library": os.path.relpath(_native.LIB_PATH, ROOT),
+            "extra_lines": sorted(extras),
         }
         print(json.dumps(line), flush=True)
     env.close()

@@ -360,6 +360,116 @@ int dk_pixels_normalize(int in_dtype, int out_dtype, int64_t n, int h, int w, in
                         const void *x, int channels_first, double *stats, void *out,
                         void *stream);
 
+/* ------------------------------------------------------------------------
+ * Articulated contact physics: SURVEY.md §8a rows G1-G4 (north_star
+ * subsystems 2-5).  The reference has NO such code (SPEC.md:8 puts the
+ * MJX/MuJoCo contact solver out of scope; PAPER.md:580 fixes feet-only
+ * collision for the joystick tasks), so parity is against the repo's own
+ * independent fp64 oracle (oracle/physics.c) and is labelled UNPINNED.
+ *
+ * The model is a Go1-shaped quadruped: a floating trunk (free joint: 7 qpos,
+ * 6 qvel; linear velocity in the world frame, angular velocity in the trunk
+ * frame, MuJoCo's convention) and DK_PHYS_LIMBS serial limbs of DK_PHYS_LJ
+ * hinges (hip abduction, hip, knee), bodies aligned with their parent at q=0.
+ * qpos = [trunk pos 3, trunk quat (w,x,y,z) 4, joints 12];
+ * qvel = [trunk lin vel (world) 3, trunk ang vel (trunk frame) 3, joints 12].
+ * Geoms (ids): 0 floor plane z=0, 1 trunk box, 2+2l thigh capsule of limb l
+ * (body 1 origin -> body 2 origin), 3+2l foot sphere of limb l.  Contacts are
+ * listed in geom order (box corners in corner order, capsule ends, foot).
+ * Dynamics per step (timestep h): FK, composite-rigid-body mass matrix + armature + h*damping
+ * (implicit joint damping), recursive Newton-Euler bias, position actuators
+ * tau = clip(kp (ctrl - q) - kd qd, +-limit), soft constraints (MuJoCo-style:
+ * solref (timeconst, dampratio), constant impedance solimp) for pyramidal
+ * friction cones (4 edges per contact) and joint limits, a primal Newton
+ * solver with exact line search, semi-implicit Euler (velocity first,
+ * quaternion exponential map).  DESIGN.md §3 "Go1 physics" has the details.
+ * ------------------------------------------------------------------------ */
+#define DK_PHYS_LIMBS 4
+#define DK_PHYS_LJ 3
+#define DK_PHYS_NQ 19
+#define DK_PHYS_NV 18
+#define DK_PHYS_NU 12
+#define DK_PHYS_NBODY 13
+#define DK_PHYS_MAXCON 16 /* 4 box corners + 4 x (2 capsule ends + 1 foot) */
+#define DK_PHYS_NSENSOR 46 /* framequat 4, gyro 3, velocimeter 3, jointpos 12, jointvel 12, foot pos 12 */
+
+typedef struct dk_phys_model {
+    double timestep;            /* physics step h (s) */
+    double gravity[3];
+    double friction;            /* pyramidal cone coefficient mu */
+    double solref[2];           /* timeconst, dampratio */
+    double solimp;              /* constant impedance in (0, 1) */
+    double base_mass;
+    double base_ipos[3];        /* trunk com in the trunk frame */
+    double base_inertia[3];     /* principal inertia (trunk frame axes) */
+    double base_box[3];         /* trunk box half sizes */
+    double body_pos[4][3][3];   /* body origin in its parent's frame */
+    double jnt_axis[4][3][3];   /* hinge axis (unit) in the body frame */
+    double body_mass[4][3];
+    double body_ipos[4][3][3];  /* com in the body frame */
+    double body_inertia[4][3][3];
+    double jnt_range[4][3][2];
+    double dof_damping[4][3];
+    double dof_armature[4][3];
+    double torque_limit[4][3];
+    double kp, kd;              /* position actuators */
+    double foot_pos[4][3];      /* foot sphere centre in the last body's frame */
+    double foot_radius;
+    double thigh_radius;        /* capsule radius */
+    int32_t iterations;         /* max Newton iterations */
+    int32_t ls_iterations;      /* max line-search iterations */
+    int32_t collide_box;        /* trunk box vs floor (0 = feet-only) */
+    int32_t collide_thigh;      /* thigh capsules vs floor */
+} dk_phys_model;
+
+typedef struct dk_phys dk_phys;
+
+/* Outputs of the LAST physics step of a dk_phys_step call (every pointer
+ * nullable; device buffers in the handle's dtype unless int32). */
+typedef struct dk_phys_diag {
+    void *qacc;              /* [N, NV] constrained acceleration */
+    void *qfrc_bias;         /* [N, NV] Coriolis/centrifugal + gravity */
+    void *qfrc_constraint;   /* [N, NV] */
+    void *act_force;         /* [N, NU] actuator torques */
+    int32_t *ncon;           /* [N] */
+    int32_t *contact_geom;   /* [N, MAXCON, 2] (0 = floor, geom id) */
+    void *contact_dist;      /* [N, MAXCON] signed distance (< 0: penetration) */
+    void *contact_pos;       /* [N, MAXCON, 3] world */
+    void *contact_force;     /* [N, MAXCON, 3] normal, tangent x, tangent y */
+    int32_t *solver_iter;    /* [N] Newton iterations used */
+    void *sensordata;        /* [N, NSENSOR] of the post-step state */
+} dk_phys_diag;
+
+/* Go1-shaped defaults (Menagerie unitree_go1-like masses and offsets,
+ * Playground Go1 joystick solver/actuator settings: h = 0.004, kp 35, kd 0.5). */
+int dk_phys_default_model(dk_phys_model *model);
+int dk_phys_create(const dk_phys_model *model, int dtype, int64_t num_worlds, int device,
+                   dk_phys **out);
+int dk_phys_destroy(dk_phys *phys);
+/* device buffers, row-major [N, NQ] / [N, NV], handle dtype */
+int dk_phys_set_state(dk_phys *phys, const void *qpos, const void *qvel, void *stream);
+int dk_phys_get_state(dk_phys *phys, void *qpos, void *qvel, void *stream);
+/* num_steps physics steps of every world with ctrl [N, NU] (joint position
+ * targets) held; diag (nullable) receives the last step's outputs. */
+int dk_phys_step(dk_phys *phys, int64_t num_steps, const void *ctrl, const dk_phys_diag *diag,
+                 void *stream);
+/* G1 inspection at the current state: M (mass matrix incl. armature, without
+ * the implicit-damping term) [N, NV, NV], qfrc_bias [N, NV], body positions
+ * xpos [N, NBODY, 3] and com positions xipos [N, NBODY, 3] (all nullable). */
+int dk_phys_inspect(dk_phys *phys, void *mass_matrix, void *qfrc_bias, void *xpos, void *xipos,
+                    void *stream);
+/* Synchronising check of the sticky "matrix not positive definite" flag a
+ * step sets for a non-finite state / control (DK_ERR_INVALID_INPUT). */
+int dk_phys_check(dk_phys *phys);
+int64_t dk_phys_kernel_launches(const dk_phys *phys);
+
+/* Benchmark/timing helper (no reference counterpart): enqueue on `stream` a
+ * one-thread kernel that waits until *host_flag (pinned host memory) becomes
+ * non-zero, or max_spins polls have elapsed (0 = no limit).  Lets a caller
+ * queue a timed region behind it and release it once the whole region is
+ * submitted. */
+int dk_stream_gate(const int32_t *host_flag, int64_t max_spins, void *stream);
+
 int dk_abi_version(void);
 const char *dk_last_error(void);
 

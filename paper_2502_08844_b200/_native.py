@@ -85,6 +85,16 @@ _i64 = ctypes.c_int64
 
 _SIGS = {
     "dk_abi_version": (ctypes.c_int, []),
+    "dk_stream_gate": (ctypes.c_int, [_vp, _i64, _vp]),
+    "dk_phys_default_model": (ctypes.c_int, [_vp]),
+    "dk_phys_create": (ctypes.c_int, [_vp, ctypes.c_int, _i64, ctypes.c_int, ctypes.POINTER(_vp)]),
+    "dk_phys_destroy": (ctypes.c_int, [_vp]),
+    "dk_phys_set_state": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "dk_phys_get_state": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
+    "dk_phys_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp]),
+    "dk_phys_inspect": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
+    "dk_phys_check": (ctypes.c_int, [_vp]),
+    "dk_phys_kernel_launches": (ctypes.c_int64, [_vp]),
     "dk_last_error": (ctypes.c_char_p, []),
     "dk_task_id": (ctypes.c_int, [ctypes.c_char_p]),
     "dk_task_dims": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),

@@ -38,6 +38,9 @@ UNITS = {
     "capi_loco.cu": [],
     "capi_ppo.cu": ["--fmad=false"],
     "capi_pixels.cu": ["--fmad=false"],
+    "physics_f32.cu": [],
+    "physics_f64.cu": ["--fmad=false"],
+    "capi_phys.cu": [],
 }
 
 
@@ -65,13 +68,18 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     nvcc = _nvcc()
     os.makedirs(OBJDIR, exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for unit, extra in UNITS.items():
         obj = os.path.join(OBJDIR, unit.replace(".cu", ".o"))
-        cmd = [nvcc, *ARCH, *COMMON, *extra, "-Xptxas", "-v" if verbose else "-O3", "-c",
-               os.path.join(CSRC, unit), "-o", obj]
-        subprocess.run(cmd, check=True)
+        cmds.append([nvcc, *ARCH, *COMMON, *extra, "-Xptxas", "-v" if verbose else "-O3", "-c",
+                     os.path.join(CSRC, unit), "-o", obj])
         objs.append(obj)
+    # translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 1)) as ex:
+        for r in list(ex.map(lambda c: subprocess.run(c, check=True), cmds)):
+            pass
     tmp = LIB + ".tmp"
     subprocess.run([nvcc, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", tmp, *objs], check=True)
     os.replace(tmp, LIB)

@@ -631,3 +631,27 @@ int dk_env_set_state(dk_env *e, const double *state, const double *target, const
 int64_t dk_env_kernel_launches(const dk_env *e) { return e ? e->launches : 0; }
 
 }  // extern "C"
+
+namespace {
+// One thread spins on a word of pinned (UVA-mapped) host memory until the host
+// stores a non-zero value: work queued behind it on the stream is submitted
+// while the device waits, so a timed region bracketed by events after the
+// gate measures the device, not host submission.  The gate never triggers
+// programmatic dependents early: a PDL launch behind it starts only after it
+// completes.
+__global__ void stream_gate_kernel(const volatile int32_t *flag, int64_t max_spins) {
+    for (int64_t i = 0; *flag == 0; ++i) {
+        if (max_spins > 0 && i >= max_spins) break;  // safety valve: never hang the device
+        __nanosleep(256);
+    }
+}
+}  // namespace
+
+extern "C" int dk_stream_gate(const int32_t *host_flag, int64_t max_spins, void *stream) {
+    if (!host_flag) return fail(DK_ERR_INVALID_INPUT, "dk_stream_gate: null flag");
+    int32_t *dflag = nullptr;
+    DK_CUDA(cudaHostGetDevicePointer((void **)&dflag, (void *)host_flag, 0));
+    stream_gate_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(dflag, max_spins);
+    DK_CUDA(cudaGetLastError());
+    return DK_OK;
+}

@@ -25,6 +25,12 @@
 
 namespace dk {
 
+#ifdef DK_F32_ORDER
+constexpr bool kRefOrder = true;  // f32 in the reference's operation order (A/B build)
+#else
+constexpr bool kRefOrder = false;
+#endif
+
 // DynamicsParams (dynamics.py:40-60) in the kernel's real type.
 template <typename T>
 struct Params {
@@ -128,7 +134,7 @@ struct Cartpole {
         const T r1 = force + mp * l * w.thd * w.thd * w.s;
         const T r2 = mp * g * l * w.s;
         const T det = m11 * m22 - m12 * m12;
-        if constexpr (std::is_same<T, float>::value) {
+        if constexpr (std::is_same<T, float>::value && !kRefOrder) {
             // f32 (tolerance-checked, not bit-exact): one reciprocal, and the
             // angle update folded as th + dt*thd + dt^2*thdd so that only one
             // FFMA follows the reciprocal on the th -> sincos -> th chain.
@@ -194,7 +200,7 @@ template <typename T>
 __device__ __forceinline__ void twolink_refresh(TwoLinkW<T> &w) {
     RealOps<T>::sincos_(w.t1, &w.s1, &w.c1);
     RealOps<T>::sincos_(w.t2, &w.s2, &w.c2);
-    if constexpr (std::is_same<T, float>::value) {
+    if constexpr (std::is_same<T, float>::value && !kRefOrder) {
         // f32 (tolerance-checked): the sum angle by the addition formulas,
         // four FMA-pipe ops instead of a third sincos (error <= ~2 ulp)
         w.s12 = fmaf(w.s1, w.c2, w.c1 * w.s2);
@@ -221,7 +227,7 @@ __device__ __forceinline__ void twolink_advance(TwoLinkW<T> &w, T tau1, T tau2, 
     const T rhs1 = tau1 - cor1 - g1 - p.link_damping * d1;
     const T rhs2 = tau2 - cor2 - g2 - p.link_damping * d2;
     const T det = m11 * m22 - m12 * m12;
-    if constexpr (std::is_same<T, float>::value) {
+    if constexpr (std::is_same<T, float>::value && !kRefOrder) {
         // f32 (tolerance-checked): one reciprocal; angles folded as
         // t + dt d + dt^2 a so one FFMA follows the reciprocal (as cartpole)
         const float rdet = RealOps<float>::div_(1.0f, det);

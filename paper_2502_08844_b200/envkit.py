@@ -280,6 +280,7 @@ class _Infos(Sequence):
         self._mask = term_mask
         self._term = term_obs
         self._term_pixels = term_pixels
+        self._built = {}  # index -> dict: persistent like the reference's list of dicts
 
     def __len__(self):
         return self._info.shape[0]
@@ -291,7 +292,10 @@ class _Infos(Sequence):
             i += len(self)
         if not 0 <= i < len(self):
             raise IndexError(i)
-        d = {k: float(self._info[i, j]) for j, k in enumerate(self._keys)}
+        d = self._built.get(i)
+        if d is not None:
+            return d
+        d = self._built[i] = {k: float(self._info[i, j]) for j, k in enumerate(self._keys)}
         if self._mask is not None and self._mask[i]:
             t = np.array(self._term[i], dtype=np.float64)
             d["terminal_observation"] = {"state": t, "privileged_state": t.copy()}
@@ -314,7 +318,7 @@ class _EnvView:
         self.config = owner.config
 
     def _row(self):
-        s, t, steps, ep, nr = self._owner._h.get_state()
+        s, t, steps, ep, nr = self._owner._state_snapshot()
         return s[self._i], t[self._i], steps[self._i], ep[self._i], nr[self._i]
 
     @property
@@ -375,6 +379,7 @@ class BatchEnv:
         self.dtype = np.dtype(self._h.np_dtype)
         self._alloc_host_buffers()
         self._envs = None
+        self._version, self._snap = 0, None
         self._pix = None
         if spec.pixels:  # rendered on the device from the state observations
             import torch
@@ -397,6 +402,14 @@ class BatchEnv:
         self._b_mask = _pinned((n,), np.uint8)
         self._b_info = _pinned((n, i), dt)
 
+    def _state_snapshot(self):
+        """One device->host copy of every world's state per env version
+        (invalidated by reset / step), shared by all ``envs[i]`` views, so
+        walking ``envs`` is O(N), not O(N^2)."""
+        if self._snap is None or self._snap[0] != self._version:
+            self._snap = (self._version, self._h.get_state())
+        return self._snap[1]
+
     @property
     def envs(self):
         if self._envs is None:
@@ -409,6 +422,7 @@ class BatchEnv:
             if self._envs is not None:
                 for e in self._envs:
                     e.config = self.config
+        self._version += 1
         _check(self._h._lib.dk_env_reset_host(self._h.h, int(seed is not None),
                                               0 if seed is None else int(seed) & (2**64 - 1),
                                               self._b_obs.ctypes.data))
@@ -430,6 +444,7 @@ class BatchEnv:
             # device-side check
             a = np.where(np.isfinite(a), np.clip(a, -1.0, 1.0), a)
         np.copyto(self._b_act, a, casting="unsafe")
+        self._version += 1
         _check(self._h._lib.dk_env_step_host(
             self._h.h, self._b_act.ctypes.data, int(bool(autoreset)), self._b_obs.ctypes.data,
             self._b_rew.ctypes.data, self._b_done.ctypes.data, self._b_trunc.ctypes.data,

@@ -40,6 +40,7 @@ class DeviceRolloutBatch:
     bootstrap: object
     raw_policy_obs: object = None  # [T*N, O] raw observations of the phase (normaliser input)
     raw_value_obs: object = None
+    nan_flag: object = None  # device bool: the policy produced a NaN mean in this phase
 
 
 _LOG_2 = 0.6931471805599453
@@ -175,6 +176,9 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
     T, N = int(cfg.unroll_length), env.num_envs
     if noise is not None and tuple(noise.shape[:2]) != (T, N):
         raise ConfigError("noise must be [unroll_length, num_envs, action_dim]")
+    # ppo.policy_forward's NaN check (ppo.py:208), as a device flag read once
+    # per phase instead of one host sync per step
+    nan_flag = torch.zeros((), dtype=torch.bool, device=env.device)
     out = env._outputs((), False)  # reused step buffers (stream-ordered)
     f32 = torch.float32
     p_obs, v_obs, acts, pres, lps, rews, dns, vals = [], [], [], [], [], [], [], []
@@ -202,6 +206,7 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             if value_normalizer is not None:
                 raw_v.append(val_in.clone())
             mean, log_std = policy(pol_t)
+            nan_flag |= torch.isnan(mean).any()
             eps = noise[t].to(mean.dtype) if noise is not None else torch.randn(
                 mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
             pre_tanh = mean + torch.exp(log_std) * eps
@@ -237,10 +242,22 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
                                torch.stack(dns), torch.stack(vals), bootstrap)
     batch.raw_policy_obs = torch.cat(raw_p, 0) if raw_p else None
     batch.raw_value_obs = torch.cat(raw_v, 0) if raw_v else None
+    batch.nan_flag = nan_flag
+    if not torch.cuda.is_current_stream_capturing():
+        _check_phase(env, batch)
     # fold the phase's raw observations into the statistics afterwards (ppo.py:370-377)
     if update_normalizers:
         _update(batch, policy_normalizer, value_normalizer)
     return batch, obs, raw_reward_sum / T
+
+
+def _check_phase(env, batch):
+    """One host sync per phase: the policy's NaN flag (ppo.py:208 raises
+    RuntimeError('policy produced NaN mean')) and the env's sticky device
+    error word (a rejected step leaves its worlds untouched)."""
+    if bool(batch.nan_flag):
+        raise RuntimeError("policy produced NaN mean")
+    env.check()
 
 
 def evaluate_device(policy, env, cfg, episodes: int | None = None, max_steps: int | None = None,
@@ -320,6 +337,12 @@ class RolloutGraph:
             env, policy, value, cfg, obs, policy_normalizer, value_normalizer)
         self.obs_in = obs["state"].clone()
         self.last = batch
+        # the capture warm-up really steps the env: snapshot the worlds (state,
+        # counters, episode) and the sampling generator, and restore both
+        # afterwards so the first replay continues exactly where the eager
+        # phase stopped
+        snap = env.state()
+        gen_state = torch.cuda.get_rng_state(env.device)
         side = torch.cuda.Stream(device=env.device)
         side.wait_stream(torch.cuda.current_stream(env.device))
         with torch.cuda.stream(side):  # capture warm-up on a side stream
@@ -328,6 +351,10 @@ class RolloutGraph:
                                    policy_normalizer, value_normalizer,
                                    update_normalizers=False)
         torch.cuda.current_stream(env.device).wait_stream(side)
+        torch.cuda.synchronize(env.device)
+        env.set_state(state=snap[0], target=snap[1], steps=snap[2], episode=snap[3],
+                      needs_reset=snap[4])
+        torch.cuda.set_rng_state(gen_state, env.device)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.batch, self.obs_out, self.reward_out = collect_rollout_device(
@@ -341,6 +368,7 @@ class RolloutGraph:
         if obs is not None and obs["state"].data_ptr() != self.obs_in.data_ptr():
             self.obs_in.copy_(obs["state"])
         self.graph.replay()
+        _check_phase(self.env, self.batch)
         _update(self.batch, self.pn, self.vn)
         self.obs_in.copy_(self.obs_out["state"])
         return self.batch, {"state": self.obs_in, "privileged_state": self.obs_in}, \

@@ -105,6 +105,73 @@ def test_rollout_graph_replay():
     env.check()
 
 
+def test_rollout_graph_first_replay_continues_eager_phase():
+    """Building a RolloutGraph must not advance the env: its first replay starts
+    from exactly the worlds (state, counters) and observation where the eager
+    set-up phase stopped -- the same inputs as a second eager phase -- and the
+    episode counters after it equal two eager phases'."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+
+    N, T = 256, 6
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = T, 10.0, 0.995
+        policy_obs_key = value_obs_key = "state"
+
+    def setup():
+        torch.manual_seed(0)
+        policy, value = R.make_policy(5, 1, (32, 32)).cuda(), R.make_value(5, (32,)).cuda()
+        env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance", episode_length=4), N)
+        obs = env.reset(seed=1)
+        return env, policy, value, obs, P.DeviceRunningNormalizer(5), P.DeviceRunningNormalizer(5)
+
+    env_a, pa, va, obs_a, pna, vna = setup()
+    rg = R.RolloutGraph(env_a, pa, va, Cfg, obs_a, pna, vna)
+    env_b, pb, vb, obs_b, pnb, vnb = setup()
+    _, obs_b, _ = R.collect_rollout_device(env_b, pb, vb, Cfg, obs_b, pnb, vnb)
+    sa, sb = env_a.state(), env_b.state()
+    for x, y in zip(sa, sb):  # construction left the env exactly after phase 1
+        np.testing.assert_array_equal(x, y)
+    batch_a, _, _ = rg.run()
+    batch_b, _, _ = R.collect_rollout_device(env_b, pb, vb, Cfg, obs_b, pnb, vnb)
+    torch.testing.assert_close(batch_a.policy_obs[0], batch_b.policy_obs[0], rtol=0, atol=0)
+    torch.testing.assert_close(batch_a.value_obs[0], batch_b.value_obs[0], rtol=0, atol=0)
+    sa, sb = env_a.state(), env_b.state()
+    np.testing.assert_array_equal(sa[2], sb[2])  # steps
+    np.testing.assert_array_equal(sa[3], sb[3])  # episode
+    np.testing.assert_array_equal(batch_a.dones.cpu().numpy(), batch_b.dones.cpu().numpy())
+    env_a.close()
+    env_b.close()
+
+
+def test_rollout_nan_policy_raises():
+    """ppo.policy_forward raises RuntimeError('policy produced NaN mean')
+    (ppo.py:208); the device rollout checks the flag once per phase."""
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import rollout as R
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = 3, 10.0, 0.995
+        policy_obs_key = value_obs_key = "state"
+
+    torch.manual_seed(0)
+    policy, value = R.make_policy(5, 1, (32,)).cuda(), R.make_value(5, (32,)).cuda()
+    with torch.no_grad():
+        for prm in policy.parameters():  # NaN weights -> NaN mean
+            prm.fill_(float("nan"))
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance"), 64)
+    obs = env.reset(seed=0)
+    with pytest.raises(RuntimeError, match="policy produced NaN mean"):
+        R.collect_rollout_device(env, policy, value, Cfg, obs)
+    env.close()
+
+
 def test_pixel_policy_rollout_matches_reference():
     """collect_rollout_device with the reference's CNNPolicy on pixel_normalize'd
     cartpole pixel stacks (tests/golden/rollout_pixels_golden.npz): the policy

@@ -27,6 +27,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "parity.json"))
     ap.add_argument("--n", type=int, default=8192)
+    ap.add_argument("--dtypes", default="float64,float32")
+    ap.add_argument("--tag", default=os.environ.get("DK_LIB_PATH", "product"))
     args = ap.parse_args()
     import torch
 
@@ -42,7 +44,7 @@ def main():
             ref = OracleBatchEnv(task, n, episode_length=1000, wide_init=wide)
             ref.reset(seed=5)
             r_obs, r_rew, _, r_tr, _, r_mask, r_info = ref.rollout(acts)
-            for dtype in ("float64", "float32"):
+            for dtype in args.dtypes.split(","):
                 env = dk.DeviceBatchEnv(dk.EnvConfig(task=task, wide_init=wide), n, dtype=dtype)
                 env.reset(seed=5)
                 out = env.rollout(torch.as_tensor(acts, device="cuda", dtype=env.dtype),
@@ -62,12 +64,18 @@ def main():
                         rec[f"obs@{h}/floor{fl:g}"] = float(eo.max())
                         rec[f"rew@{h}/floor{fl:g}"] = float(er.max())
                     rec[f"obs_bitexact_frac@{h}"] = float((obs[:h] == r_obs[:h]).mean())
+                    # per observation component, absolute error and rel @ floor 1e-3
+                    d = np.abs(obs[:h] - r_obs[:h])
+                    rec[f"obs_abs_per_comp@{h}"] = [float(x) for x in d.max(axis=(0, 1))]
+                    rec[f"obs_rel_per_comp@{h}/floor0.001"] = [
+                        float(x) for x in (d / np.maximum(np.abs(r_obs[:h]), 1e-3)).max(axis=(0, 1))]
                 rec["reward_mean_gpu"] = float(rew.mean())
                 rec["reward_mean_ref"] = float(r_rew.mean())
                 report[key] = rec
                 env.close()
                 print(key, {k: f"{v:.2e}" if isinstance(v, float) else v for k, v in rec.items()
-                            if "floor0.1" in k or "exact" in k}, flush=True)
+                            if "floor0.001" in k or "exact" in k}, flush=True)
+    report["_tag"] = os.path.basename(args.tag)
     os.makedirs(os.path.dirname(args.out), exist_ok=True)
     with open(args.out, "w") as f:
         json.dump(report, f, indent=1)
