@@ -91,6 +91,124 @@ __device__ __forceinline__ T rexp(T x) { return RealOps<T>::exp_(x); }
 template <typename T>
 __device__ __forceinline__ void rsincos(T x, T *s, T *c) { RealOps<T>::sincos_(x, s, c); }
 
+// One frame row of the step tail, as pointers to that row's fields (global
+// memory in loco_tail_kernel, shared memory in the fused Go1 env kernel).
+template <typename T>
+struct LocoRowIn {
+    const T *q, *lin, *ang, *cmd, *fcmd, *pa, *fpa, *nom, *def, *jpos, *jvel, *jtau, *act;
+    const T *air, *fh, *fhd, *fvel, *phase;
+    const uint8_t *td, *con;
+    bool done;
+    const T *pert;  // [3] or null
+};
+
+template <bool GLOBAL, typename T>
+__device__ __forceinline__ T ldv(const T *p) {
+    if constexpr (GLOBAL) return __ldg(p);
+    else return *p;
+}
+
+// rewards.total_reward (16 terms in TERM_REGISTRY order, rewards.py:97-211) and
+// the clean observation row of envkit.build_locomotion_observation
+// (envkit.py:147-193) in the privileged layout [S | contacts, torques, pert].
+// Returns the unclipped total; t[16] receives the terms; ok = unit quaternion.
+template <bool GLOBAL, typename T>
+__device__ __forceinline__ T loco_row(const LocoRowIn<T> &f, const RewardCfg<T> &c, int nj, int nf,
+                                      T *row, T *t, bool &ok) {
+    const int S = 9 + 3 * nj + 3 + 2 * nf;
+    // lin / ang velocity tracking (rewards.py:97-104): from the FRAME's command
+    const T e0 = f.fcmd[0] - f.lin[0], e1 = f.fcmd[1] - f.lin[1];
+    t[0] = rexp(-(e0 * e0 + e1 * e1) / c.sigma_lin);
+    const T ea = f.fcmd[2] - f.ang[2];
+    t[1] = rexp(-(ea * ea) / c.sigma_ang);
+    // projected gravity -> orientation term + obs
+    T g[3];
+    ok = project_gravity(f.q, g);
+    if (!ok) g[0] = g[1] = g[2] = T(NAN);  // InvalidInputError (mathcore.py:46-47)
+    t[6] = g[0] * g[0] + g[1] * g[1];
+    int o = 0;
+    row[o++] = g[0]; row[o++] = g[1]; row[o++] = g[2];
+    for (int k = 0; k < 3; ++k) row[o++] = f.lin[k];
+    for (int k = 0; k < 3; ++k) row[o++] = f.ang[k];
+    // joints: terms 7-11, 13 (gated) + obs joint_pos / joint_vel / prev_action / torque
+    T tt = 0, jp = 0, ar = 0, en = 0, pose = 0, vv = 0;
+    const int o_jp = 9, o_jv = 9 + nj, o_pa = 9 + 2 * nj, o_cmd = 9 + 3 * nj;
+    const int o_ph = o_cmd + 3, o_con = S, o_tau = S + nf, o_pert = S + nf + nj;
+    DK_UNROLL_J
+    for (int j = 0; j < nj; ++j) {
+        const T qj = ldv<GLOBAL>(f.jpos + j), vj = ldv<GLOBAL>(f.jvel + j);
+        const T tj = ldv<GLOBAL>(f.jtau + j);
+        tt = tt + tj * tj;
+        const T d1 = qj - ldv<GLOBAL>(f.nom + j);
+        jp = jp + d1 * d1;
+        const T d2 = ldv<GLOBAL>(f.act + j) - ldv<GLOBAL>(f.fpa + j);
+        ar = ar + d2 * d2;
+        en = en + fabs(vj * tj);
+        const T d3 = qj - ldv<GLOBAL>(f.def + j);
+        pose = pose + d3 * d3;
+        vv = vv + vj * vj;
+        row[o_jp + j] = qj;
+        row[o_jv + j] = vj;
+        row[o_pa + j] = ldv<GLOBAL>(f.pa + j);
+        row[o_tau + j] = tj;
+    }
+    t[7] = tt; t[8] = jp; t[9] = ar; t[10] = en;
+    t[11] = rexp(-pose);
+    for (int k = 0; k < 3; ++k) row[o_cmd + k] = f.cmd[k];
+    // feet: terms 2-5 + obs phase cos/sin and contact flags
+    T air_s = 0, clr = 0, ph = 0, slip = 0;
+    const T span = c.airtime_max - c.airtime_min;
+    DK_UNROLL_F
+    for (int k = 0; k < nf; ++k) {
+        T gain = (ldv<GLOBAL>(f.air + k) - c.airtime_min) * (f.td[k] ? T(1) : T(0));
+        gain = gain < T(0) ? T(0) : (gain > span ? span : gain);  // np.clip
+        air_s = air_s + gain;
+        const T hk = ldv<GLOBAL>(f.fh + k), err_h = hk - ldv<GLOBAL>(f.fhd + k);
+        const T vx = ldv<GLOBAL>(f.fvel + 2 * k), vy = ldv<GLOBAL>(f.fvel + 2 * k + 1);
+        const T sp = RealOps<T>::sqrt_(vx * vx + vy * vy);
+        clr = clr + err_h * err_h * RealOps<T>::sqrt_(sp);
+        T sn, cs;
+        rsincos(ldv<GLOBAL>(f.phase + k), &sn, &cs);
+        const T tgt = c.swing_height * (sn > T(0) ? sn : T(0));  // swing_height_profile
+        const T dz = hk - tgt;
+        ph = ph + dz * dz;
+        const T m = f.con[k] ? T(1) : T(0);
+        const T cx = vx * m, cy = vy * m;
+        slip = slip + (cx * cx + cy * cy);
+        row[o_ph + 2 * k] = cs;
+        row[o_ph + 2 * k + 1] = sn;
+        row[o_con + k] = m;
+    }
+    t[2] = air_s; t[3] = clr; t[4] = rexp(-ph / c.sigma_phase); t[5] = slip;
+    t[12] = f.done ? T(1) : T(0);
+    const T cn = RealOps<T>::sqrt_(f.fcmd[0] * f.fcmd[0] + f.fcmd[1] * f.fcmd[1]);
+    t[13] = !c.gated ? cn : (cn > T(0.1) ? T(0) : RealOps<T>::sqrt_(vv));
+    t[14] = f.lin[2] * f.lin[2];
+    t[15] = f.ang[0] * f.ang[0] + f.ang[1] * f.ang[1];
+    T u = T(0);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) u = u + c.w[k] * t[k];  // sum(weighted) in registry order
+    for (int k = 0; k < 3; ++k) row[o_pert + k] = f.pert ? f.pert[k] : T(0);
+    return u;
+}
+
+// uniform sensor noise per group, drawn in the reference's order from
+// stream_rng(seed, env, episode, step) (envkit.py:41-49, 176-180)
+template <typename T>
+__device__ __forceinline__ void loco_row_noise(T *row, int nj, uint64_t seed, uint64_t env,
+                                               uint32_t episode, uint64_t step,
+                                               const double *noise) {
+    Philox4x64 rng;
+    rng.init(seed, env, episode, step);
+    const int start[5] = {0, 3, 6, 9, 9 + nj}, len[5] = {3, 3, 3, nj, nj};
+    for (int gi = 0; gi < 5; ++gi) {
+        const double s = noise[gi];
+        if (s > 0)
+            for (int e = 0; e < len[gi]; ++e)
+                row[start[gi] + e] = row[start[gi] + e] + (T)rng.uniform(-s, s);
+    }
+}
+
 template <typename T>
 __global__ void __launch_bounds__(128)
 loco_tail_kernel(LocoFrames<T> f, const T *__restrict__ prev_action, const T *__restrict__ command,
@@ -109,99 +227,39 @@ loco_tail_kernel(LocoFrames<T> f, const T *__restrict__ prev_action, const T *__
     const bool live = r < rows;
 
     if (live) {
-        const T *lin = f.lin + 3 * r, *ang = f.ang + 3 * r;
-        const T *cmd = (command ? command : f.cmd) + 3 * r;
-        const T *pa = (prev_action ? prev_action : f.pact) + (int64_t)nj * r;
-        const T *nom = f.nom + f.nom_stride * r, *def = f.def + f.def_stride * r;
+        LocoRowIn<T> in;
+        in.q = f.q + 4 * r;
+        in.lin = f.lin + 3 * r;
+        in.ang = f.ang + 3 * r;
+        in.cmd = (command ? command : f.cmd) + 3 * r;
+        in.fcmd = f.cmd + 3 * r;
+        in.pa = (prev_action ? prev_action : f.pact) + (int64_t)nj * r;
+        in.fpa = f.pact + (int64_t)nj * r;
+        in.nom = f.nom + f.nom_stride * r;
+        in.def = f.def + f.def_stride * r;
+        in.jpos = f.jpos + (int64_t)nj * r;
+        in.jvel = f.jvel + (int64_t)nj * r;
+        in.jtau = f.jtau + (int64_t)nj * r;
+        in.act = f.act + (int64_t)nj * r;
+        in.air = f.air + (int64_t)nf * r;
+        in.fh = f.fh + (int64_t)nf * r;
+        in.fhd = f.fhd + (int64_t)nf * r;
+        in.fvel = f.fvel + (int64_t)2 * nf * r;
+        in.phase = f.phase + (int64_t)nf * r;
+        in.td = f.touchdown + (int64_t)nf * r;
+        in.con = f.contact + (int64_t)nf * r;
+        in.done = f.done[r] != 0;
+        in.pert = pert ? pert + 3 * r : nullptr;
         T t[16];
-        // lin / ang velocity tracking (rewards.py:97-104): from the FRAME's command
-        const T *fcmd = f.cmd + 3 * r;
-        const T e0 = fcmd[0] - lin[0], e1 = fcmd[1] - lin[1];
-        t[0] = rexp(-(e0 * e0 + e1 * e1) / c.sigma_lin);
-        const T ea = fcmd[2] - ang[2];
-        t[1] = rexp(-(ea * ea) / c.sigma_ang);
-        // projected gravity -> orientation term + obs
-        T g[3];
-        if (!project_gravity(f.q + 4 * r, g)) {
-            atomicMin(err, (unsigned long long)r);  // InvalidInputError (mathcore.py:46-47)
-            g[0] = g[1] = g[2] = T(NAN);
-        }
-        t[6] = g[0] * g[0] + g[1] * g[1];
-        int o = 0;
-        row[o++] = g[0]; row[o++] = g[1]; row[o++] = g[2];
-        for (int k = 0; k < 3; ++k) row[o++] = lin[k];
-        for (int k = 0; k < 3; ++k) row[o++] = ang[k];
-        // joints: terms 7-11, 13 (gated) + obs joint_pos / joint_vel / prev_action / torque
-        T tt = 0, jp = 0, ar = 0, en = 0, pose = 0, vv = 0;
-        const T *q = f.jpos + (int64_t)nj * r, *qd = f.jvel + (int64_t)nj * r;
-        const T *tau = f.jtau + (int64_t)nj * r, *act = f.act + (int64_t)nj * r;
-        const T *fpa = f.pact + (int64_t)nj * r;
-        const int o_jp = 9, o_jv = 9 + nj, o_pa = 9 + 2 * nj, o_cmd = 9 + 3 * nj;
-        const int o_ph = o_cmd + 3, o_con = S, o_tau = S + nf, o_pert = S + nf + nj;
-        DK_UNROLL_J
-        for (int j = 0; j < nj; ++j) {
-            const T qj = __ldg(q + j), vj = __ldg(qd + j), tj = __ldg(tau + j);
-            tt = tt + tj * tj;
-            const T d1 = qj - __ldg(nom + j);
-            jp = jp + d1 * d1;
-            const T d2 = __ldg(act + j) - __ldg(fpa + j);
-            ar = ar + d2 * d2;
-            en = en + fabs(vj * tj);
-            const T d3 = qj - __ldg(def + j);
-            pose = pose + d3 * d3;
-            vv = vv + vj * vj;
-            row[o_jp + j] = qj;
-            row[o_jv + j] = vj;
-            row[o_pa + j] = __ldg(pa + j);
-            row[o_tau + j] = tj;
-        }
-        t[7] = tt; t[8] = jp; t[9] = ar; t[10] = en;
-        t[11] = rexp(-pose);
-        for (int k = 0; k < 3; ++k) row[o_cmd + k] = cmd[k];
-        // feet: terms 2-5 + obs phase cos/sin and contact flags
-        T air_s = 0, clr = 0, ph = 0, slip = 0;
-        const T *air = f.air + (int64_t)nf * r, *fh = f.fh + (int64_t)nf * r;
-        const T *fhd = f.fhd + (int64_t)nf * r, *fv = f.fvel + (int64_t)2 * nf * r;
-        const T *phase = f.phase + (int64_t)nf * r;
-        const uint8_t *td = f.touchdown + (int64_t)nf * r, *con = f.contact + (int64_t)nf * r;
-        const T span = c.airtime_max - c.airtime_min;
-        DK_UNROLL_F
-        for (int k = 0; k < nf; ++k) {
-            T gain = (__ldg(air + k) - c.airtime_min) * (td[k] ? T(1) : T(0));
-            gain = gain < T(0) ? T(0) : (gain > span ? span : gain);  // np.clip
-            air_s = air_s + gain;
-            const T hk = __ldg(fh + k), err_h = hk - __ldg(fhd + k);
-            const T vx = __ldg(fv + 2 * k), vy = __ldg(fv + 2 * k + 1);
-            const T sp = RealOps<T>::sqrt_(vx * vx + vy * vy);
-            clr = clr + err_h * err_h * RealOps<T>::sqrt_(sp);
-            T sn, cs;
-            rsincos(__ldg(phase + k), &sn, &cs);
-            const T tgt = c.swing_height * (sn > T(0) ? sn : T(0));  // swing_height_profile
-            const T dz = hk - tgt;
-            ph = ph + dz * dz;
-            const T m = con[k] ? T(1) : T(0);
-            const T cx = vx * m, cy = vy * m;
-            slip = slip + (cx * cx + cy * cy);
-            row[o_ph + 2 * k] = cs;
-            row[o_ph + 2 * k + 1] = sn;
-            row[o_con + k] = m;
-        }
-        t[2] = air_s; t[3] = clr; t[4] = rexp(-ph / c.sigma_phase); t[5] = slip;
-        t[12] = f.done[r] ? T(1) : T(0);
-        const T cn = RealOps<T>::sqrt_(fcmd[0] * fcmd[0] + fcmd[1] * fcmd[1]);
-        t[13] = !c.gated ? cn : (cn > T(0.1) ? T(0) : RealOps<T>::sqrt_(vv));
-        t[14] = lin[2] * lin[2];
-        t[15] = ang[0] * ang[0] + ang[1] * ang[1];
-        T u = T(0);
-#pragma unroll
-        for (int k = 0; k < 16; ++k) u = u + c.w[k] * t[k];  // sum(weighted) in registry order
+        bool ok;
+        const T u = loco_row<true>(in, c, nj, nf, row, t, ok);
+        if (!ok) atomicMin(err, (unsigned long long)r);
         out.unclipped[r] = u;
-        out.total[r] = T(0) > u ? T(0) : u;                  // max(unclipped, 0.0)
+        out.total[r] = T(0) > u ? T(0) : u;  // max(unclipped, 0.0)
         if (out.terms) {
 #pragma unroll
             for (int k = 0; k < 16; ++k) out.terms[16 * r + k] = t[k];
         }
-        for (int k = 0; k < 3; ++k) row[o_pert + k] = pert ? pert[3 * r + k] : T(0);
     }
     __syncwarp();
     const int64_t nrow = rows - r0 < 32 ? rows - r0 : 32;
@@ -212,19 +270,9 @@ loco_tail_kernel(LocoFrames<T> f, const T *__restrict__ prev_action, const T *__
         }
     }
     if (live && a.has_noise) {
-        // uniform noise per group, drawn in the reference's order from
-        // stream_rng(seed, env, episode, step) (envkit.py:41-49, 176-180)
         const int64_t k = r / a.N, i = r - k * a.N;
-        Philox4x64 rng;
-        rng.init(a.seed, (uint64_t)(a.env0 + i), a.episode ? a.episode[i] : 0u,
-                 a.step0 + (uint64_t)k);
-        const int start[5] = {0, 3, 6, 9, 9 + nj}, len[5] = {3, 3, 3, nj, nj};
-        for (int gi = 0; gi < 5; ++gi) {
-            const double s = a.noise[gi];
-            if (s > 0)
-                for (int e = 0; e < len[gi]; ++e)
-                    row[start[gi] + e] = row[start[gi] + e] + (T)rng.uniform(-s, s);
-        }
+        loco_row_noise(row, nj, a.seed, (uint64_t)(a.env0 + i), a.episode ? a.episode[i] : 0u,
+                       a.step0 + (uint64_t)k, a.noise);
     }
     __syncwarp();
     if (out.state) {

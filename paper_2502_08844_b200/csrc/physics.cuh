@@ -425,12 +425,13 @@ struct Lane {
     T ctrl[3];
 };
 
-// rows in shared memory: field f of row r of lane t at rows[(r * RF + f) * THREADS + t]
+// rows in shared memory: field f of row r of lane t at rows[(r * RF + f) * nt + t]
+// (nt = threads of the CTA: 128, or fewer when many collision geoms need more rows)
 template <typename T>
 struct Rows {
     T *base;
-    int t;
-    __device__ __forceinline__ T &at(int r, int f) const { return base[(r * RF + f) * THREADS + t]; }
+    int t, nt;
+    __device__ __forceinline__ T &at(int r, int f) const { return base[(r * RF + f) * nt + t]; }
 };
 
 enum { F_JB = 0, F_JL = 6, F_AREF = 9, F_D = 10, F_X = 11, F_Y = 12 };
@@ -1151,12 +1152,12 @@ __global__ void __launch_bounds__(THREADS) phys_kernel(PhysConst<T> pc, PhysArgs
     {   // stage the model in shared memory
         const uint32_t *src = reinterpret_cast<const uint32_t *>(&pc);
         uint32_t *dst = reinterpret_cast<uint32_t *>(smem_raw);
-        for (int i = threadIdx.x; i < (int)(sizeof(PhysConst<T>) / 4); i += THREADS) dst[i] = src[i];
+        for (int i = threadIdx.x; i < (int)(sizeof(PhysConst<T>) / 4); i += blockDim.x) dst[i] = src[i];
     }
     __syncthreads();
     const int tid = threadIdx.x;
     const int lane_limb = tid & 3;
-    const int64_t w = (int64_t)blockIdx.x * WPC + (tid >> 2);
+    const int64_t w = (int64_t)blockIdx.x * (blockDim.x >> 2) + (tid >> 2);
     if (w >= a.n) return;  // whole quads exit together
     const int64_t n = a.n;
     Lane<T> L;
@@ -1171,7 +1172,7 @@ __global__ void __launch_bounds__(THREADS) phys_kernel(PhysConst<T> pc, PhysArgs
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) L.quat[i] = a.qpos[(3 + i) * n + w];
-    Rows<T> rows{rowbuf, tid};
+    Rows<T> rows{rowbuf, tid, (int)blockDim.x};
     if (ins.on()) {
         phys_step(P, L, rows, lane_limb, static_cast<const PhysArgs<T> *>(nullptr), w, &ins);
         return;
@@ -1209,15 +1210,19 @@ namespace dk {
 namespace phys {
 
 template <typename T>
-size_t phys_smem_bytes(const PhysConst<T> &pc) {
+size_t phys_smem_bytes(const PhysConst<T> &pc, int threads) {
     return ((sizeof(PhysConst<T>) + 15) & ~size_t(15)) +
-           (size_t)pc.rows_per_lane * RF * THREADS * sizeof(T);
+           (size_t)pc.rows_per_lane * RF * threads * sizeof(T);
 }
 
 template <typename T>
 cudaError_t launch_phys(const PhysConst<T> &pc, const PhysArgs<T> &a, const PhysInspect<T> &ins,
                         cudaStream_t st) {
-    const size_t smem = phys_smem_bytes(pc);
+    // 128 threads (32 worlds) per CTA unless the constraint rows of that many
+    // lanes would not fit two CTAs' worth of shared memory on an SM
+    int threads = THREADS;
+    while (threads > 32 && phys_smem_bytes(pc, threads) > 110 * 1024) threads /= 2;
+    const size_t smem = phys_smem_bytes(pc, threads);
     static size_t attr = 0;
     if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(phys_kernel<T>,
@@ -1225,8 +1230,9 @@ cudaError_t launch_phys(const PhysConst<T> &pc, const PhysArgs<T> &a, const Phys
         if (e != cudaSuccess) return e;
         attr = smem;
     }
-    const unsigned grid = (unsigned)((a.n + WPC - 1) / WPC);
-    phys_kernel<T><<<grid, THREADS, smem, st>>>(pc, a, ins);
+    const int wpc = threads / QUAD;
+    const unsigned grid = (unsigned)((a.n + wpc - 1) / wpc);
+    phys_kernel<T><<<grid, threads, smem, st>>>(pc, a, ins);
     return cudaGetLastError();
 }
 

@@ -59,6 +59,22 @@ def envelope(oracle, task, n, seed, acts, mid_reset_step=-1, round_actions=True,
     return np.stack(obs), np.stack(E)
 
 
+def reset_envelope(oracle, task, n, seed, resets=2, **kw):
+    """E_c of the reset observation: the float32-rounded reset state's
+    observation (rounded) against the exact one, per component, over the
+    first `resets` episodes' draws."""
+    env = oracle.OracleBatchEnv(task, n, **kw)
+    params = kw.get("params")
+    E = None
+    for k in range(resets):
+        obs0 = env.reset(seed=seed) if k == 0 else env.reset()
+        E = np.zeros(obs0.shape[1]) if E is None else E
+        for w in range(n):
+            o = oracle.state_obs(task, r32(env.state[w]), r32(env.target[w]), params)
+            E = np.maximum(E, np.abs(r32(o) - obs0[w]))
+    return E
+
+
 def floors(E_k, rtol):
     return np.maximum(1e-3, K_ULP * np.asarray(E_k) / rtol)
 

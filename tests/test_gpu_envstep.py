@@ -81,7 +81,11 @@ def test_golden_trajectories(golden, pkg, oracle, dtype):
             np.testing.assert_allclose(o_ref, g("obs"), rtol=1e-12, atol=1e-12)  # oracle pinned
             floor_k = lambda k: fe.floors(E[k], fe.RTOL_1 if k == 0 else fe.RTOL_H)  # noqa: E731
             tol_k = lambda k: fe.RTOL_1 if k == 0 else fe.RTOL_H  # noqa: E731
-            floor0, tol0 = 1e-3, 1e-6  # reset states: float32 rounding of the f64 draw
+            # reset states: the float32 rounding of the f64 draw
+            floor0 = fe.floors(fe.reset_envelope(oracle, task, n, int(g("meta_seed")),
+                                                 dt=None if dt < 0 else dt, params=params, **kw),
+                               fe.RTOL_1)
+            tol0 = fe.RTOL_1
             tol_r = lambda k: 1e-4 if k == 0 else 1e-3  # noqa: E731  (reward, info terms)
         obs0 = env.reset(seed=int(g("meta_seed")))
         assert _close(obs0["state"], g("obs0"), 0, floor0) < tol0
@@ -89,7 +93,7 @@ def test_golden_trajectories(golden, pkg, oracle, dtype):
             fl, tol = floor_k(k), tol_k(k)
             if k == int(g("mid_reset_step")):
                 o = env.reset()
-                assert _close(o["state"], g("obs_mid_reset"), 0, floor0) < max(tol0, 1e-6)
+                assert _close(o["state"], g("obs_mid_reset"), 0, floor0) < max(tol0, 1e-12)
             obs, rew, done, trunc, infos = env.step(acts[k])
             assert obs["state"].dtype == np.float64 and obs["state"].shape == g("obs")[k].shape
             np.testing.assert_array_equal(obs["state"], obs["privileged_state"])

@@ -149,3 +149,15 @@ def test_joint_limit_pushes_back(model):
     m = pm.go1_model(kp=0.0, kd=0.0)
     out = op.step(m.to_c(), qpos, np.zeros((1, pm.NV)), qpos[:, 7:])
     assert out["qfrc_constraint"][0, 6 + 2] < 0  # pushes towards the range
+
+
+def test_library_default_model_equals_python_model():
+    """dk_phys_default_model (C ABI, no GPU needed) == physmodel.go1_model()."""
+    import ctypes
+
+    from paper_2502_08844_b200 import physics
+
+    c = physics.default_model_c()
+    py = pm.go1_model().to_c()
+    assert bytes(c) == bytes(py)
+    assert ctypes.sizeof(c) == 2016  # sizeof(dk_phys_model) in C

@@ -82,6 +82,12 @@ def main():
                 a, b = np.asarray(a, np.float64)[same], np.asarray(b, np.float64)[same]
                 r[f"step1/{k}/abs"] = float(np.abs(a - b).max()) if a.size else 0.0
                 r[f"step1/{k}/rel@1e-3"] = rel(a, b, 1e-3)
+            # normwise per world: ||d||_inf / max(||ref||_inf, 1)
+            for k, a, b in (("qpos", qp, one_r["qpos"]), ("qvel", qv, one_r["qvel"]),
+                            ("qacc", o["qacc"], one_r["qacc"])):
+                nw = np.abs(a - b).max(1) / np.maximum(np.abs(b).max(1), 1.0)
+                r[f"step1/{k}/normwise_max"] = float(nw.max())
+                r[f"step1/{k}/normwise_p99"] = float(np.percentile(nw, 99))
             # 100 steps (ctrl held), from the same state
             sim.set_state(cast(q32), cast(v32))
             qp_r, qv_r = q32.copy(), v32.copy()
@@ -94,12 +100,34 @@ def main():
                 ncon_eq.append(float((o100["ncon"].cpu().numpy() == ref["ncon"]).mean()))
                 if s in (0, 9, 99):
                     qp, qv = (x.double().cpu().numpy() for x in sim.state())
+                    for k, a, b in (("qpos", qp, qp_r), ("qvel", qv, qv_r)):
+                        nw = np.abs(a - b).max(1) / np.maximum(np.abs(b).max(1), 1.0)
+                        r[f"h{s + 1}/{k}/normwise_p50"] = float(np.percentile(nw, 50))
+                        r[f"h{s + 1}/{k}/normwise_p99"] = float(np.percentile(nw, 99))
+                        r[f"h{s + 1}/{k}/normwise_max"] = float(nw.max())
+                        r[f"h{s + 1}/{k}/frac_over_1e-3"] = float((nw > 1e-3).mean())
                     r[f"h{s + 1}/qpos/abs"] = float(np.abs(qp - qp_r).max())
                     r[f"h{s + 1}/qvel/abs"] = float(np.abs(qv - qv_r).max())
                     r[f"h{s + 1}/qpos/rel@1e-3"] = rel(qp, qp_r, 1e-3)
                     r[f"h{s + 1}/qvel/rel@1e-3"] = rel(qv, qv_r, 1e-3)
                     r[f"h{s + 1}/qvel/p99_abs"] = float(np.percentile(np.abs(qv - qv_r).max(1), 99))
             sim.check()
+            if dtype == "float32":
+                # the float64 oracle's own sensitivity: state rounded to float32
+                # after every step (storage alone), against the exact oracle
+                qe, ve, qx, vx = q32.copy(), v32.copy(), q32.copy(), v32.copy()
+                for s in range(100):
+                    e = op.step(mc, qe, ve, c32, 1)
+                    qe = e["qpos"].astype(np.float32).astype(np.float64)
+                    ve = e["qvel"].astype(np.float32).astype(np.float64)
+                    x = op.step(mc, qx, vx, c32, 1)
+                    qx, vx = x["qpos"], x["qvel"]
+                    if s in (0, 9, 99):
+                        for k, a, b in (("qpos", qe, qx), ("qvel", ve, vx)):
+                            nw = np.abs(a - b).max(1) / np.maximum(np.abs(b).max(1), 1.0)
+                            r[f"envelope_h{s + 1}/{k}/normwise_p99"] = float(np.percentile(nw, 99))
+                            r[f"envelope_h{s + 1}/{k}/normwise_max"] = float(nw.max())
+                            r[f"envelope_h{s + 1}/{k}/frac_over_1e-3"] = float((nw > 1e-3).mean())
             r["h100/ncon_equal_frac_min"] = float(min(ncon_eq))
             r["h100/ncon_equal_frac_mean"] = float(np.mean(ncon_eq))
             rep[key] = r
