@@ -463,6 +463,58 @@ int dk_phys_inspect(dk_phys *phys, void *mass_matrix, void *qfrc_bias, void *xpo
 int dk_phys_check(dk_phys *phys);
 int64_t dk_phys_kernel_launches(const dk_phys *phys);
 
+/* ------------------------------------------------------------------------
+ * Go1 joystick environment (north_star subsystem 6): the physics step above
+ * with the locomotion tail (rows B1-B7) fused into the same kernel --
+ * action -> PD targets (envkit.action_to_target, absolute), ctrl_dt/timestep
+ * physics steps, foot kinematics, airtime / touchdown / advance_phase,
+ * rewards.total_reward, build_locomotion_observation with Philox sensor
+ * noise, termination (trunk upside down or below term_height), truncation,
+ * Philox-keyed auto-reset.  No reference counterpart: UNPINNED.
+ * Observations: state [N, 56], privileged_state [N, 75] (Go1 shape of
+ * build_locomotion_observation); reward f[N]; done / trunc u8[N].
+ * ------------------------------------------------------------------------ */
+typedef struct dk_go1_config {
+    int64_t episode_length;      /* control steps per episode */
+    double ctrl_dt;              /* control period (s); physics steps = ctrl_dt / timestep */
+    double action_scale;         /* PD target = q_default + action_scale * clip(a, -1, 1) */
+    double gait_freq;            /* advance_phase frequency (Hz) */
+    double term_height;          /* terminate below this trunk height (m) */
+    double cmd_lo[3], cmd_hi[3]; /* joystick command ranges (vx, vy, yaw rate) */
+    double joint_noise;          /* reset joint offsets U(-x, x) */
+    double yaw_range;            /* reset heading U(-x, x) */
+    double obs_noise[5];         /* ObservationNoise: gravity, lin_vel, ang_vel, joint_pos, joint_vel */
+    uint64_t seed;
+    dk_reward_config reward;
+} dk_go1_config;
+
+typedef struct dk_go1_env dk_go1_env;
+
+int dk_go1_default_config(dk_go1_config *cfg);
+int dk_go1_create(const dk_phys_model *model, const dk_go1_config *cfg, int dtype,
+                  int64_t num_worlds, int64_t env_index_offset, int device, dk_go1_env **out);
+int dk_go1_destroy(dk_go1_env *env);
+/* reset every world (episode 0; has_seed: replace the config seed); obs [N,56],
+ * priv [N,75] (nullable) device buffers */
+int dk_go1_reset(dk_go1_env *env, int has_seed, uint64_t seed, void *obs, void *priv,
+                 void *stream);
+/* K control steps; actions [K,N,12]; obs [K,N,56]; priv [K,N,75] | NULL; reward [K,N];
+ * done / trunc u8 [K,N]; terms [K,N,16] | NULL; terminal_obs [K,N,56] | NULL;
+ * terminal_mask u8 [K,N] | NULL (device buffers, handle dtype) */
+int dk_go1_step(dk_go1_env *env, int64_t num_steps, const void *actions, void *obs, void *priv,
+                void *reward, uint8_t *done, uint8_t *trunc, void *terms, void *terminal_obs,
+                uint8_t *terminal_mask, void *stream);
+/* state as row-major device buffers (each nullable): qpos [N,19], qvel [N,18],
+ * command [N,3], phase [N,4], airtime [N,4], last_contact u8 [N,4],
+ * prev_action [N,12], steps i32 [N], episode u32 [N] */
+int dk_go1_get_state(dk_go1_env *env, void *qpos, void *qvel, void *command, void *phase,
+                     void *airtime, uint8_t *last_contact, void *prev_action, int32_t *steps,
+                     uint32_t *episode, void *stream);
+/* synchronising error check: non-finite actions (DK_ERR_INVALID_INPUT, with
+ * the first step / world), non-positive-definite physics matrices */
+int dk_go1_check(dk_go1_env *env, int64_t *step_index, int64_t *env_index);
+int64_t dk_go1_kernel_launches(const dk_go1_env *env);
+
 /* Benchmark/timing helper (no reference counterpart): enqueue on `stream` a
  * one-thread kernel that waits until *host_flag (pinned host memory) becomes
  * non-zero, or max_spins polls have elapsed (0 = no limit).  Lets a caller

@@ -788,3 +788,27 @@ void orc_phys_energy(const dk_phys_model *m, int64_t n, const double *qpos, cons
             for (int i = 0; i < 6; ++i) momentum6[w * 6 + i] = P[i];
     }
 }
+
+/* foot sphere centres [n][4][3] and their world velocities J(q) qvel [n][4][3] */
+void orc_phys_foot_kin(const dk_phys_model *m, int64_t n, const double *qpos, const double *qvel,
+                       double *pos, double *vel) {
+    tree_t t;
+    build_tree(m, &t);
+    for (int64_t w = 0; w < n; ++w) {
+        kin_t k;
+        fk(&t, qpos + w * NQ, &k);
+        for (int l = 0; l < 4; ++l) {
+            const int b2 = 3 + 3 * l;
+            double off[3], f[3], J[3][NV];
+            mat_vec3(k.xR[b2], m->foot_pos[l], off);
+            for (int i = 0; i < 3; ++i) f[i] = k.xpos[b2][i] + off[i];
+            point_jac(&t, &k, b2, f, J);
+            for (int i = 0; i < 3; ++i) {
+                double s = 0.0;
+                for (int d = 0; d < NV; ++d) s += J[i][d] * qvel[w * NV + d];
+                pos[(w * 4 + l) * 3 + i] = f[i];
+                vel[(w * 4 + l) * 3 + i] = s;
+            }
+        }
+    }
+}

@@ -33,6 +33,8 @@ def lib():
         L.orc_phys_inspect.argtypes = [_P, ctypes.c_int64] + [_P] * 6
         L.orc_phys_inverse.restype = None
         L.orc_phys_inverse.argtypes = [_P, ctypes.c_int64] + [_P] * 4
+        L.orc_phys_foot_kin.restype = None
+        L.orc_phys_foot_kin.argtypes = [_P, ctypes.c_int64] + [_P] * 4
         L.orc_phys_energy.restype = None
         L.orc_phys_energy.argtypes = [_P, ctypes.c_int64] + [_P] * 5
         _bound = True
@@ -84,6 +86,16 @@ def inverse(model_c, qpos, qvel, qacc):
     lib().orc_phys_inverse(ctypes.byref(model_c), n, qpos.ctypes.data, qvel.ctypes.data,
                            qacc.ctypes.data, qfrc.ctypes.data)
     return qfrc
+
+
+def foot_kin(model_c, qpos, qvel):
+    """foot sphere centres [N,4,3] and their world velocities [N,4,3]"""
+    qpos, qvel = _c(qpos), _c(qvel)
+    n = qpos.shape[0]
+    pos, vel = np.zeros((n, 4, 3)), np.zeros((n, 4, 3))
+    lib().orc_phys_foot_kin(ctypes.byref(model_c), n, qpos.ctypes.data, qvel.ctypes.data,
+                            pos.ctypes.data, vel.ctypes.data)
+    return pos, vel
 
 
 def energy(model_c, qpos, qvel):

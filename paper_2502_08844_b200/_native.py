@@ -95,6 +95,16 @@ _SIGS = {
     "dk_phys_inspect": (ctypes.c_int, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "dk_phys_check": (ctypes.c_int, [_vp]),
     "dk_phys_kernel_launches": (ctypes.c_int64, [_vp]),
+    "dk_go1_default_config": (ctypes.c_int, [_vp]),
+    "dk_go1_create": (ctypes.c_int, [_vp, _vp, ctypes.c_int, _i64, _i64, ctypes.c_int,
+                                     ctypes.POINTER(_vp)]),
+    "dk_go1_destroy": (ctypes.c_int, [_vp]),
+    "dk_go1_reset": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_uint64, _vp, _vp, _vp]),
+    "dk_go1_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _u8p, _u8p, _vp, _vp, _u8p,
+                                   _vp]),
+    "dk_go1_get_state": (ctypes.c_int, [_vp] + [_vp] * 9 + [_vp]),
+    "dk_go1_check": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
+    "dk_go1_kernel_launches": (ctypes.c_int64, [_vp]),
     "dk_last_error": (ctypes.c_char_p, []),
     "dk_task_id": (ctypes.c_int, [ctypes.c_char_p]),
     "dk_task_dims": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),

@@ -41,6 +41,9 @@ UNITS = {
     "physics_f32.cu": [],
     "physics_f64.cu": ["--fmad=false"],
     "capi_phys.cu": [],
+    "go1env_f32.cu": [],
+    "go1env_f64.cu": ["--fmad=false"],
+    "capi_go1.cu": [],
 }
 
 

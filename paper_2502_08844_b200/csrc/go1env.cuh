@@ -1,0 +1,485 @@
+// go1env.cuh -- the Go1 joystick environment step, fused (north_star
+// subsystem 6: reward, observation, termination, auto-reset and domain
+// randomisation in the step kernel's tail, one HBM round trip per control step).
+//
+// One launch advances every world K control steps.  Per control step and
+// world (one lane quad, lane = limb, as in physics.cuh):
+//   action -> PD targets      envkit.action_to_target, absolute mode (envkit.py:111-131)
+//   `substeps` physics steps  physics.cuh phys_step (PD torque clip = envkit.pd_torque)
+//   foot kinematics           foot height / velocity, contact = sphere below the floor
+//   gait bookkeeping          airtime, touchdown, advance_phase (mathcore.py:143-171),
+//                             swing_height_profile (rewards.py:92-94)
+//   reward                    rewards.total_reward, 16 terms (rewards.py:97-211)
+//   observation               envkit.build_locomotion_observation with Philox-keyed
+//                             uniform sensor noise (envkit.py:147-193; randomization
+//                             B7 sensor noise)
+//   termination / truncation  upside-down trunk or trunk below term_height; episode_length
+//   auto-reset                Philox-keyed reset draw (stream_rng(seed, env, episode, 0),
+//                             envkit.py:41-49), terminal observation kept
+// The frame of the reward/observation row is assembled in shared memory by the
+// four lanes, lane 0 evaluates loco_row (locomotion.cuh, the same code as the
+// standalone tail kernel), and the CTA stores its 32 worlds' contiguous output
+// rows cooperatively.  The reference has no Go1 env: the physics is
+// checked against oracle/physics.c, the tail against oracle/locomotion.c, and
+// the glue against oracle/go1env.py (tests/test_gpu_go1env.py) -- UNPINNED.
+#pragma once
+#include "locomotion.cuh"
+#include "physics.cuh"
+
+namespace dk {
+namespace go1 {
+
+using phys::Lane;
+using phys::PhysConst;
+using phys::Rows;
+
+constexpr int NJ = 12, NF = 4;
+constexpr int S = 9 + 3 * NJ + 3 + 2 * NF;  // 56: state slot
+constexpr int P = S + NF + NJ + 3;          // 75: privileged slot
+constexpr int FR = 112;                     // frame scratch per world (T)
+
+template <typename T>
+struct EnvConst {
+    int substeps;
+    int has_noise;
+    int64_t episode_length;
+    uint64_t seed;
+    int64_t env0;
+    T ctrl_dt, action_scale, gait_freq, term_height, home_height;
+    T q_default[NJ];
+    T phase0[NF];
+    double cmd_lo[3], cmd_hi[3], joint_noise, yaw_range;
+    double noise[5];
+    RewardCfg<T> rc;
+};
+
+template <typename T>
+struct EnvState {  // structure of arrays, [field][n]
+    T *qpos, *qvel, *cmd, *phase, *air, *prev_action;
+    uint8_t *last_contact;
+    int32_t *steps;
+    uint32_t *episode;
+};
+
+template <typename T>
+struct EnvIO {
+    int64_t n, K;
+    int reset_all;          // 1: reset every world (episode = 0) and write its obs (K ignored)
+    const T *actions;       // [K][n][12]
+    T *obs, *priv;          // [K][n][56] / [K][n][75] (priv nullable)
+    T *reward;              // [K][n]
+    uint8_t *done, *trunc;  // [K][n]
+    T *terms;               // [K][n][16] nullable
+    T *terminal_obs;        // [K][n][56] nullable (rows of auto-reset worlds)
+    uint8_t *terminal_mask; // [K][n] nullable
+    unsigned long long *err;  // first (step * n + world) with a non-finite action
+    int32_t *bad;             // set when a physics factorisation broke down
+};
+
+// frame scratch offsets (T units)
+enum {
+    O_Q = 0, O_LIN = 4, O_ANG = 7, O_CMD = 10, O_JPOS = 13, O_JVEL = 25, O_JTAU = 37,
+    O_ACT = 49, O_FPA = 61, O_AIR = 73, O_FH = 77, O_FHD = 81, O_FVEL = 85, O_PHASE = 93,
+    O_FLAGS = 97  // 8 bytes: touchdown[4], contact[4] (as raw bytes)
+};
+
+// foot position and world velocity of the lane's limb (point on the last body)
+template <typename T>
+__device__ __forceinline__ void foot_kin(const PhysConst<T> &P, const Lane<T> &L, int l, T *fpos,
+                                         T *fvel) {
+    const auto &lm = P.limb[l];
+    T R0[9];
+    phys::quat2mat(L.quat, R0);
+    T w[3];
+    phys::mat_vec3(R0, L.wb, w);
+    T vel[6] = {w[0], w[1], w[2], L.vlin[0], L.vlin[1], L.vlin[2]};
+    T Rp[9], pp[3];
+#pragma unroll
+    for (int i = 0; i < 9; ++i) Rp[i] = R0[i];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) pp[i] = L.pos[i];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        T off[3], a[3], Rq[9], Rj[9], rel[3], lin[3];
+        phys::mat_vec3(Rp, lm.body_pos[j], off);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) pp[i] = pp[i] + off[i];
+        phys::mat_vec3(Rp, lm.axis[j], a);
+        phys::axis_rot(lm.axis[j], L.q[j], Rq);
+        phys::mat_mul3(Rp, Rq, Rj);
+#pragma unroll
+        for (int i = 0; i < 9; ++i) Rp[i] = Rj[i];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) rel[i] = L.pos[i] - pp[i];
+        phys::cross3(a, rel, lin);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            vel[i] = vel[i] + a[i] * L.qd[j];
+            vel[3 + i] = vel[3 + i] + lin[i] * L.qd[j];
+        }
+    }
+    T foff[3];
+    phys::mat_vec3(Rp, lm.foot_pos, foff);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) fpos[i] = pp[i] + foff[i];
+    T r[3], wr[3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i) r[i] = fpos[i] - L.pos[i];
+    phys::cross3(vel, r, wr);
+#pragma unroll
+    for (int i = 0; i < 3; ++i) fvel[i] = vel[3 + i] + wr[i];
+}
+
+// per-world reset draw from stream_rng(seed, env, episode, 0): yaw, then the
+// 12 joint offsets, then the 3 command components (Generator.uniform order)
+template <typename T>
+__device__ void reset_world(const PhysConst<T> &P, const EnvConst<T> &E, Lane<T> &L, int l,
+                            uint64_t env, uint32_t episode, T *cmd, T &phase, T &air,
+                            T *prev_action) {
+    Philox4x64 rng;
+    rng.init(E.seed, env, episode, 0);
+    const double yaw = rng.uniform(-E.yaw_range, E.yaw_range);
+    double jn[NJ];
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) jn[j] = rng.uniform(-E.joint_noise, E.joint_noise);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) cmd[k] = (T)rng.uniform(E.cmd_lo[k], E.cmd_hi[k]);
+    double sh, ch;
+    sincos(0.5 * yaw, &sh, &ch);
+    L.pos[0] = T(0);
+    L.pos[1] = T(0);
+    L.pos[2] = E.home_height;
+    L.quat[0] = (T)ch;
+    L.quat[1] = T(0);
+    L.quat[2] = T(0);
+    L.quat[3] = (T)sh;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+        L.vlin[i] = T(0);
+        L.wb[i] = T(0);
+        L.qd[i] = T(0);
+        L.q[i] = (T)((double)E.q_default[3 * l + i] + jn[3 * l + i]);
+        prev_action[i] = T(0);
+    }
+    phase = E.phase0[l];
+    air = T(0);
+    (void)P;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(phys::THREADS)
+go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const size_t pc_b = (sizeof(PhysConst<T>) + 15) & ~size_t(15);
+    const size_t ec_b = (sizeof(EnvConst<T>) + 15) & ~size_t(15);
+    PhysConst<T> &Pc = *reinterpret_cast<PhysConst<T> *>(smem_raw);
+    EnvConst<T> &E = *reinterpret_cast<EnvConst<T> *>(smem_raw + pc_b);
+    const int nt = blockDim.x, wpc = nt >> 2;
+    T *rowbuf = reinterpret_cast<T *>(smem_raw + pc_b + ec_b);
+    T *frames = rowbuf + (size_t)pc.rows_per_lane * phys::RF * nt;  // [wpc][FR]
+    T *tile = frames + (size_t)wpc * FR;                             // [wpc][P]
+    {
+        const uint32_t *s1 = reinterpret_cast<const uint32_t *>(&pc);
+        uint32_t *d1 = reinterpret_cast<uint32_t *>(smem_raw);
+        for (int i = threadIdx.x; i < (int)(sizeof(PhysConst<T>) / 4); i += nt) d1[i] = s1[i];
+        const uint32_t *s2 = reinterpret_cast<const uint32_t *>(&ec);
+        uint32_t *d2 = reinterpret_cast<uint32_t *>(smem_raw + pc_b);
+        for (int i = threadIdx.x; i < (int)(sizeof(EnvConst<T>) / 4); i += nt) d2[i] = s2[i];
+    }
+    __syncthreads();
+    const int tid = threadIdx.x, l = tid & 3, wl = tid >> 2;
+    const int64_t n = io.n;
+    const int64_t w0 = (int64_t)blockIdx.x * wpc;
+    const int64_t w = w0 + wl;
+    const bool live = w < n;
+    const int nlive = (int)(n - w0 < wpc ? n - w0 : wpc);
+    T *fr = frames + (size_t)wl * FR;
+    T *row = tile + (size_t)wl * P;
+    uint8_t *flags = reinterpret_cast<uint8_t *>(fr + O_FLAGS);
+    Rows<T> rows{rowbuf, tid, nt};
+    const uint64_t env = (uint64_t)(E.env0 + w);
+
+    // ---- load the world
+    Lane<T> L;
+    T cmd[3] = {T(0), T(0), T(0)}, phase = T(0), air = T(0), prev[3] = {T(0), T(0), T(0)};
+    uint8_t lastc = 1;
+    int32_t steps = 0;
+    uint32_t episode = 0;
+    if (live) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            L.pos[i] = st.qpos[i * n + w];
+            L.vlin[i] = st.qvel[i * n + w];
+            L.wb[i] = st.qvel[(3 + i) * n + w];
+            L.q[i] = st.qpos[(7 + 3 * l + i) * n + w];
+            L.qd[i] = st.qvel[(6 + 3 * l + i) * n + w];
+            cmd[i] = st.cmd[i * n + w];
+            prev[i] = st.prev_action[(3 * l + i) * n + w];
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) L.quat[i] = st.qpos[(3 + i) * n + w];
+        phase = st.phase[l * n + w];
+        air = st.air[l * n + w];
+        lastc = st.last_contact[l * n + w];
+        steps = st.steps[w];
+        episode = st.episode[w];
+    }
+
+    // evaluate the reward / observation row of the current state into `row`
+    // (lane 0 of the quad), with the frame fields already in `fr`
+    auto build_row = [&](bool done, uint32_t ep, int32_t stp, T *reward, T *terms16) {
+        (void)ep;
+        (void)stp;
+        if (l == 0) {
+            LocoRowIn<T> in;
+            in.q = fr + O_Q;
+            in.lin = fr + O_LIN;
+            in.ang = fr + O_ANG;
+            in.cmd = fr + O_CMD;
+            in.fcmd = fr + O_CMD;
+            in.pa = fr + O_ACT;   // observation: the action just applied
+            in.fpa = fr + O_FPA;  // reward action rate: against the previous action
+            in.nom = E.q_default;
+            in.def = E.q_default;
+            in.jpos = fr + O_JPOS;
+            in.jvel = fr + O_JVEL;
+            in.jtau = fr + O_JTAU;
+            in.act = fr + O_ACT;
+            in.air = fr + O_AIR;
+            in.fh = fr + O_FH;
+            in.fhd = fr + O_FHD;
+            in.fvel = fr + O_FVEL;
+            in.phase = fr + O_PHASE;
+            in.td = flags;
+            in.con = flags + 4;
+            in.done = done;
+            in.pert = nullptr;
+            T t[16];
+            bool ok;
+            const T u = loco_row<false>(in, E.rc, NJ, NF, row, t, ok);
+            if (reward) *reward = T(0) > u ? T(0) : u;
+            if (terms16)
+#pragma unroll
+                for (int k = 0; k < 16; ++k) terms16[k] = t[k];
+        }
+    };
+    // lane-parallel part of the frame for the current state
+    auto fill_frame = [&](const T *act3, const T *act_force3, bool reset_frame) {
+        T fpos[3], fvel[3];
+        foot_kin(Pc, L, l, fpos, fvel);
+        const bool contact = fpos[2] - Pc.foot_radius < T(0);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            fr[O_JPOS + 3 * l + j] = L.q[j];
+            fr[O_JVEL + 3 * l + j] = L.qd[j];
+            fr[O_JTAU + 3 * l + j] = act_force3[j];
+            fr[O_ACT + 3 * l + j] = act3[j];
+            fr[O_FPA + 3 * l + j] = prev[j];
+        }
+        if (!reset_frame) {
+            air = air + E.ctrl_dt;
+            phase = wrap_angle_dev(phase + T(6.283185307179586) * E.gait_freq * E.ctrl_dt);
+        }
+        const bool td = reset_frame ? false : (contact && !lastc);
+        fr[O_AIR + l] = air;
+        fr[O_FH + l] = fpos[2] - Pc.foot_radius;
+        T sn, cs;
+        RealOps<T>::sincos_(phase, &sn, &cs);
+        fr[O_FHD + l] = E.rc.swing_height * (sn > T(0) ? sn : T(0));
+        fr[O_FVEL + 2 * l] = fvel[0];
+        fr[O_FVEL + 2 * l + 1] = fvel[1];
+        fr[O_PHASE + l] = phase;
+        flags[l] = td ? 1 : 0;
+        flags[4 + l] = contact ? 1 : 0;
+        if (l == 0) {
+            T R0[9], vl[3];
+            phys::quat2mat(L.quat, R0);
+            phys::mat_tvec3(R0, L.vlin, vl);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) fr[O_Q + i] = L.quat[i];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                fr[O_LIN + i] = vl[i];
+                fr[O_ANG + i] = L.wb[i];
+                fr[O_CMD + i] = cmd[i];
+            }
+        }
+        return contact;
+    };
+    // cooperative, coalesced store of the CTA's rows [nlive][cols] (tile pitch P)
+    auto store_rows = [&](T *dst, int cols) {
+        for (int e = tid; e < nlive * cols; e += nt) {
+            const int r = e / cols, c = e - r * cols;
+            dst[(w0 + r) * cols + c] = tile[r * P + c];
+        }
+    };
+    const unsigned qm = phys::quad_mask();
+
+    // observation noise key: stream_rng(seed, env, episode, steps + 1) -- step 0
+    // of an episode's stream belongs to its reset draw
+    auto add_noise = [&]() {
+        if (l == 0 && E.has_noise)
+            loco_row_noise(row, NJ, E.seed, env, episode, (uint64_t)steps + 1, E.noise);
+    };
+    auto do_reset = [&]() {
+        reset_world(Pc, E, L, l, env, episode, cmd, phase, air, prev);
+        const T zero3[3] = {T(0), T(0), T(0)};
+        const bool c = fill_frame(zero3, zero3, true);
+        lastc = c ? 1 : 0;
+        __syncwarp(qm);
+        build_row(false, episode, steps, nullptr, nullptr);
+        __syncwarp(qm);
+    };
+
+    if (io.reset_all) {
+        if (live) {
+            episode = 0;
+            steps = 0;
+            do_reset();
+        }
+        __syncthreads();
+        if (io.priv) store_rows(io.priv, P);
+        __syncthreads();
+        if (live) add_noise();
+        __syncthreads();
+        store_rows(io.obs, S);
+    }
+
+    for (int64_t k = 0; k < (io.reset_all ? 0 : io.K); ++k) {
+        T a[3] = {T(0), T(0), T(0)}, tau[3] = {T(0), T(0), T(0)};
+        bool done = false, trunc = false;
+        T rw = T(0);
+        T t16[16];
+        if (live) {
+            // action -> clipped [-1, 1] -> absolute joint targets
+            bool finite = true;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                T v = io.actions[(k * n + w) * NJ + 3 * l + j];
+                finite &= isfinite(v);
+                v = isfinite(v) ? (v < T(-1) ? T(-1) : (v > T(1) ? T(1) : v)) : T(0);
+                a[j] = v;
+                L.ctrl[j] = E.q_default[3 * l + j] + E.action_scale * v;
+            }
+            if (!phys::qall(finite) && l == 0 && io.err)
+                atomicMin(io.err, (unsigned long long)(k * n + w));
+            bool okp = true;
+            for (int s = 0; s < E.substeps; ++s)
+                okp &= phys::phys_step(Pc, L, rows, l,
+                                       static_cast<const phys::PhysArgs<T> *>(nullptr), w,
+                                       static_cast<const phys::PhysInspect<T> *>(nullptr),
+                                       s + 1 == E.substeps ? tau : nullptr);
+            if (!okp && l == 0 && io.bad) *io.bad = 1;
+            const bool c = fill_frame(a, tau, false);
+            // termination: trunk upside down (its z axis points down) or below term_height
+            T R0[9];
+            phys::quat2mat(L.quat, R0);
+            done = R0[8] < T(0) || L.pos[2] < E.term_height;
+            steps += 1;
+            trunc = steps >= E.episode_length;
+            __syncwarp(qm);
+            build_row(done, episode, steps, &rw, t16);
+            __syncwarp(qm);
+            // post-reward bookkeeping (the frame used the pre-step values)
+            air = c ? T(0) : air;
+            lastc = c ? 1 : 0;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) prev[j] = a[j];
+            if (l == 0) {
+                io.reward[k * n + w] = rw;
+                io.done[k * n + w] = done ? 1 : 0;
+                io.trunc[k * n + w] = trunc ? 1 : 0;
+                if (io.terms)
+#pragma unroll
+                    for (int q = 0; q < 16; ++q) io.terms[(k * n + w) * 16 + q] = t16[q];
+                if (io.terminal_mask) io.terminal_mask[k * n + w] = (done || trunc) ? 1 : 0;
+            }
+            // auto-reset: emit the terminal observation, start the next episode
+            if (done || trunc) {
+                add_noise();
+                __syncwarp(qm);
+                if (io.terminal_obs)
+                    for (int c2 = l; c2 < S; c2 += 4) io.terminal_obs[(k * n + w) * S + c2] = row[c2];
+                __syncwarp(qm);
+                episode += 1;
+                steps = 0;
+                do_reset();
+            }
+        }
+        __syncthreads();
+        if (io.priv) store_rows(io.priv + k * n * P, P);
+        __syncthreads();
+        if (live) add_noise();
+        __syncthreads();
+        store_rows(io.obs + k * n * S, S);
+        __syncthreads();
+    }
+
+    // ---- store the world
+    if (live) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            if (l == 0) {
+                st.qpos[i * n + w] = L.pos[i];
+                st.qvel[i * n + w] = L.vlin[i];
+                st.qvel[(3 + i) * n + w] = L.wb[i];
+                st.cmd[i * n + w] = cmd[i];
+            }
+            st.qpos[(7 + 3 * l + i) * n + w] = L.q[i];
+            st.qvel[(6 + 3 * l + i) * n + w] = L.qd[i];
+            st.prev_action[(3 * l + i) * n + w] = prev[i];
+        }
+        if (l == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) st.qpos[(3 + i) * n + w] = L.quat[i];
+            st.steps[w] = steps;
+            st.episode[w] = episode;
+        }
+        st.phase[l * n + w] = phase;
+        st.air[l * n + w] = air;
+        st.last_contact[l * n + w] = lastc;
+    }
+}
+
+}  // namespace go1
+}  // namespace dk
+
+namespace dk {
+namespace go1 {
+
+template <typename T>
+size_t env_smem_bytes(const PhysConst<T> &pc, int threads) {
+    return ((sizeof(PhysConst<T>) + 15) & ~size_t(15)) + ((sizeof(EnvConst<T>) + 15) & ~size_t(15)) +
+           (size_t)pc.rows_per_lane * phys::RF * threads * sizeof(T) +
+           (size_t)(threads / 4) * (FR + P) * sizeof(T);
+}
+
+template <typename T>
+cudaError_t launch_env(const PhysConst<T> &pc, const EnvConst<T> &ec, const EnvState<T> &st,
+                       const EnvIO<T> &io, cudaStream_t s) {
+    int threads = phys::THREADS;
+    while (threads > 32 && env_smem_bytes(pc, threads) > 110 * 1024) threads /= 2;
+    const size_t smem = env_smem_bytes(pc, threads);
+    static size_t attr = 0;
+    if (smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(go1_env_kernel<T>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    const int wpc = threads / 4;
+    const unsigned grid = (unsigned)((io.n + wpc - 1) / wpc);
+    go1_env_kernel<T><<<grid, threads, smem, s>>>(pc, ec, st, io);
+    return cudaGetLastError();
+}
+
+#define DK_GO1_DECLARE(T)                                                                     \
+    extern template cudaError_t launch_env<T>(const PhysConst<T> &, const EnvConst<T> &,     \
+                                              const EnvState<T> &, const EnvIO<T> &,         \
+                                              cudaStream_t);
+#define DK_GO1_INSTANTIATE(T)                                                                 \
+    template cudaError_t launch_env<T>(const PhysConst<T> &, const EnvConst<T> &,            \
+                                       const EnvState<T> &, const EnvIO<T> &, cudaStream_t);
+
+}  // namespace go1
+}  // namespace dk

@@ -448,7 +448,8 @@ struct PhysInspect {
 // With ins->on(), stops after the mass matrix and bias and writes them instead.
 template <typename T>
 __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int lane_limb,
-                          const PhysArgs<T> *dg, int64_t w, const PhysInspect<T> *ins = nullptr) {
+                          const PhysArgs<T> *dg, int64_t w, const PhysInspect<T> *ins = nullptr,
+                          T *act_out = nullptr) {
     const LimbConst<T> &lm = P.limb[lane_limb];
     const T h = P.h;
     // ---------------- trunk FK and velocity (redundant in the quad)
@@ -694,6 +695,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
         const T lim = lm.tlim[j];
         tau = tau < -lim ? -lim : (tau > lim ? lim : tau);
         act[j] = tau;
+        if (act_out) act_out[j] = tau;
         qf_l[j] = (tau - lm.damping[j] * L.qd[j]) - bias_l[j];
     }
 #pragma unroll

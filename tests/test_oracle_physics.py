@@ -161,3 +161,14 @@ def test_library_default_model_equals_python_model():
     py = pm.go1_model().to_c()
     assert bytes(c) == bytes(py)
     assert ctypes.sizeof(c) == 2016  # sizeof(dk_phys_model) in C
+
+
+def test_library_default_go1_config_equals_python_config():
+    import ctypes
+
+    from paper_2502_08844_b200 import _native as nat
+    from paper_2502_08844_b200.go1env import Go1Config, Go1ConfigC
+
+    c = Go1ConfigC()
+    assert nat.lib().dk_go1_default_config(ctypes.byref(c)) == 0
+    assert bytes(c) == bytes(Go1Config().to_c())
