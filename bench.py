@@ -3,20 +3,27 @@
     python bench.py [--gpus N --steps K --warmup W] [--impl reference]
     torchrun --nproc-per-node N bench.py --gpus N ...     (one rank per GPU)
 
-A "step" is one BatchEnv.step over every world of the job (envkit.py:625-646):
-dynamics + reward (+ info terms) + obs + truncation + Philox autoreset, with
-synthetic U(-1, 1) actions pre-generated in HBM.  K steps are executed as
-K / --unroll fused rollout launches (one kernel each) cycling through a ring of
-action / output chunks larger than L2.  Rank r owns global worlds
+Headline (BASELINE.json's metric): physics steps/s of the Go1 joystick env at
+8192 worlds per GPU.  A "step" is one control step of every world through the
+fused kernel (csrc/go1env.cuh): action -> PD targets, 5 physics steps (FK, CRB
+mass matrix, contacts, Newton solver, Euler), reward, noisy observation,
+termination and Philox auto-reset; physics steps = control steps x 5 (the
+metric's physics steps, as the reference counts env-steps x action_repeat,
+SURVEY.md §8d).  K steps run as ceil(K / --unroll) fused launches over a ring
+of action / output chunks, behind a device gate (dk_stream_gate) so the CUDA
+events time the device, not host submission.  Rank r owns global worlds
 [r*N, (r+1)*N) -- no collective on the data path ("weak" scaling).
 
-Prints ONE JSON line (rank 0) with the metric, roofline of the rollout kernel,
-the CPU oracle baseline, an end-to-end number through the host-buffer C ABI
-(dk_env_rollout_host) and the clocks seen during the timed region.
+The reference has no Go1 physics: parity is against the repo's
+independent oracle (UNPINNED), and the CPU baseline / --impl reference arm is
+that oracle's C physics step on all host cores (kind "port").  The analytic
+tasks the reference does implement (cartpole etc., pinned bit-exact in f64)
+are timed on their own lines before the headline (extra "cartpole", "sweep",
+"all_tasks", ...), each a JSON line without a top-level "metric" key.
 
---impl reference times the reference's algorithm on the host CPU instead: the
-C restatement in oracle/ (kind "port"; the reference is pure Python and cannot
-be installed on the GPU box), all host threads, same workload and metric.
+Prints the headline JSON line (rank 0) LAST, with roofline, cpu_baseline,
+an end-to-end number through the public API with host buffers, the float64
+leg and the clocks seen around the timed region.
 """
 
 from __future__ import annotations
@@ -35,7 +42,10 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "physics steps/sec (8192 worlds/GPU) at 1/2/4/8 B200 vs CPU host"
+METRIC = "physics steps/sec (Go1 joystick, 8192 worlds/GPU) at 1/2/4/8 B200 vs CPU host"
+ANALYTIC_METRIC = "physics steps/sec (8192 worlds/GPU) at 1/2/4/8 B200 vs CPU host"
+GO1 = "go1-joystick"
+GO1_SUBSTEPS = 5
 UNIT = "physics_steps/s"
 FALLBACK_HBM_GBS = 6650.0
 
@@ -43,22 +53,33 @@ FALLBACK_HBM_GBS = 6650.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=100_000)
-    ap.add_argument("--warmup", type=int, default=3_000)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--task", default="cartpole-balance")
+    ap.add_argument("--task", default=GO1, help="go1-joystick (headline) or an analytic task")
+    ap.add_argument("--analytic-task", default="cartpole-balance",
+                    help="analytic task of the secondary 'cartpole' line")
+    ap.add_argument("--analytic-steps", type=int, default=20_000,
+                    help="steps of the secondary analytic line")
     ap.add_argument("--num-envs", type=int, default=8192, help="worlds per GPU")
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
-    ap.add_argument("--unroll", type=int, default=1000, help="env steps fused per launch")
+    ap.add_argument("--unroll", type=int, default=0,
+                    help="env steps fused per launch (0: 50 for go1, 1000 for analytic tasks)")
     ap.add_argument("--ring", type=int, default=6, help="action/output chunks in the ring")
-    ap.add_argument("--e2e-steps", type=int, default=20_000)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="steps of the e2e leg (0: 200 for go1, 20000 for analytic tasks)")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-tail", action="store_true", help="skip the Go1-shape step-tail line")
     ap.add_argument("--no-f64", action="store_true", help="skip the precision-matched f64 leg")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the drop-in BatchEnv.step and world-count sweep lines")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.unroll <= 0:
+        a.unroll = 50 if a.task == GO1 else 1000
+    if a.e2e_steps <= 0:
+        a.e2e_steps = 200 if a.task == GO1 else 20_000
+    return a
 
 
 # ---------------------------------------------------------------------------
@@ -222,52 +243,67 @@ TASK_DIMS = {"cartpole-balance": (1, 5, 3), "pendulum-swingup": (1, 3, 1),
              "acrobot-swingup": (1, 6, 1), "reacher-easy": (2, 10, 1)}  # (A, O, info terms)
 
 
-def headline_config(args, world):
-    """The `config` object of the headline line, shared by both arms."""
-    A, O, I = TASK_DIMS[args.task]
+def headline_config(args, world, task=None, steps=None, unroll=None):
+    """The `config` object of an analytic-task line."""
+    task = task or args.task
+    steps = args.steps if steps is None else steps
+    A, O, I = TASK_DIMS[task]
     esz = 8 if args.dtype == "float64" else 4
-    U = min(args.unroll, args.steps)
+    U = min(unroll or args.unroll, steps)
     R = max(2, args.ring)
     bpw = bytes_per_world_step(A, O, I, esz)
     chunk_mb = U * args.num_envs * (bpw + A * esz) / 1e6
-    nlaunch = -(-args.steps // U)
+    nlaunch = -(-steps // U)
     if nlaunch == 1:
         l2_note = "flushed before the timed region (a single launch)"
     else:
         l2_note = (f"flushed before the timed region; {R}-chunk ring of {chunk_mb:.0f} MB "
                    f"chunks ({'>' if chunk_mb * min(R, nlaunch) > 126 else '<'} 126 MB L2)")
     return {
-        "workload": f"{args.task} BatchEnv.step (dynamics, reward + info terms, obs, "
-                    "truncation, Philox autoreset), episode_length 1000; BASELINE's Go1 "
-                    "joystick physics does not exist in the reference (SURVEY.md §0)",
-        "task": args.task, "worlds_per_gpu": args.num_envs,
+        "workload": f"{task} BatchEnv.step (dynamics, reward + info terms, obs, "
+                    "truncation, Philox autoreset), episode_length 1000",
+        "task": task, "worlds_per_gpu": args.num_envs,
         "global_worlds": args.num_envs * world, "steps_per_launch": U,
         "parallelism": f"worlds sharded dp{world}",
         "l2": l2_note,
     }
 
 
-def run_reference(args, rank):
+def run_reference(args, rank, world):
+    """The CPU arm: rank 0 alone times the oracle on all host cores (the
+    reference itself has no Go1 physics and is single-threaded Python for the
+    analytic tasks); other ranks exit without work."""
     if rank != 0:
         return
     from oracle.oracle import build as build_oracle
 
     build_oracle()
-    # warm-up W steps (bounded), then exactly K steps, each one batched step
-    # of num_envs worlds on all host threads
-    cpu_rate(args.task, args.num_envs, 0.5, steps=max(3, min(args.warmup, 200)))
-    rate, threads, steps, dt = cpu_rate(args.task, args.num_envs, 0, steps=args.steps)
-    cores = threads
+    if args.task == GO1:
+        # warm-up, then exactly K control steps (x 5 physics steps) of every
+        # world, bounded to ~30 s of CPU work
+        cpu_go1_rate(args.num_envs, max(1, min(args.warmup, 2)), seconds=2.0)
+        rate, threads, n_phys, dt = cpu_go1_rate(args.num_envs, args.steps, seconds=30.0)
+        steps = n_phys / GO1_SUBSTEPS
+        kind_note = ("oracle/physics.c, the independent fp64 restatement of the Go1 physics "
+                     "step (the reference has no Go1 physics, SPEC.md:8); physics only, the "
+                     "env tail excluded")
+        cfg = go1_config_obj(args, world, min(args.unroll, args.steps))
+        metric, dtype = METRIC, "f64"
+    else:
+        cpu_rate(args.task, args.num_envs, 0.5, steps=max(3, min(args.warmup, 200)))
+        rate, threads, steps, dt = cpu_rate(args.task, args.num_envs, 0, steps=args.steps)
+        kind_note = "oracle/oracle.c, the bit-exact C restatement of deskrl BatchEnv.step"
+        cfg = headline_config(args, world)
+        metric, dtype = ANALYTIC_METRIC, "f64"
     line = {
-        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
-        "ms_per_step": dt / steps * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic U(-1,1) actions",
-        "config": headline_config(args, args.gpus),
-        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"{steps} steps x {args.num_envs} worlds on {cores} threads "
-                                   f"({cpu_model()}); oracle/oracle.c, the bit-exact C "
-                                   "restatement of deskrl BatchEnv.step"},
+        "impl": "reference", "metric": metric, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt / max(steps, 1e-9) * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": dtype, "data": "synthetic",
+        "config": cfg,
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                         "sample": f"{steps:g} env steps x {args.num_envs} worlds on {threads} "
+                                   f"threads ({cpu_model()}) in {dt:.1f} s; {kind_note}"},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         # what was actually timed: rank 0 alone, num_envs worlds on the host
         # cores, whatever N the job was launched with
@@ -320,7 +356,8 @@ def gated_region(fn, stream, dev):
     return t0.elapsed_time(t1)
 
 
-def measure_rollout(args, dtype, dev, rank, world, dist, local_rank):
+def measure_rollout(args, dtype, dev, rank, world, dist, local_rank, task=None, steps=None,
+                    unroll=None):
     """The headline measurement for one real type: W warm-up steps, L2 flush,
     then exactly K steps of every world as fused rollout launches, behind a
     device gate, timed with CUDA events on the launching stream, max over ranks."""
@@ -329,12 +366,14 @@ def measure_rollout(args, dtype, dev, rank, world, dist, local_rank):
     import paper_2502_08844_b200 as dk
 
     n = args.num_envs
-    cfg = dk.EnvConfig(task=args.task)
+    task = task or args.task
+    steps = args.steps if steps is None else steps
+    cfg = dk.EnvConfig(task=task)
     env = dk.DeviceBatchEnv(cfg, n, dtype=dtype, device=local_rank, env_index_offset=rank * n)
     A, O, I, NS = env.action_dim, env.obs_dim, len(env.info_keys), env.spec.state_dim
     tdt = env.dtype
     esz = 8 if tdt == torch.float64 else 4
-    U = min(args.unroll, args.steps)
+    U = min(unroll or args.unroll, steps)
     R = max(2, args.ring)
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -362,14 +401,14 @@ def measure_rollout(args, dtype, dev, rank, world, dist, local_rank):
     torch.cuda.synchronize(dev)
     del flush
 
-    nlaunch = (args.steps + U - 1) // U
+    nlaunch = (steps + U - 1) // U
     launches0 = env.kernel_launches
     if dist is not None:
         dist.barrier()
     torch.cuda.synchronize(dev)
 
     def region():
-        left = args.steps
+        left = steps
         for L in range(nlaunch):
             k = min(U, left)
             launch(j + L, k)  # back to back: events between launches cost 8% (measured)
@@ -385,7 +424,7 @@ def measure_rollout(args, dtype, dev, rank, world, dist, local_rank):
         t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms = float(t.item())
-    total_steps = args.steps * n * world * cfg.action_repeat
+    total_steps = steps * n * world * cfg.action_repeat
     value = total_steps / (elapsed_ms / 1e3)
 
     # roofline of the rollout kernel (the only kernel of a launch)
@@ -395,15 +434,272 @@ def measure_rollout(args, dtype, dev, rank, world, dist, local_rank):
     # average launch duration over the timed region (device events around the
     # whole gated region / launches: includes any inter-launch gaps, so the
     # achieved bandwidth is a lower bound for the kernel itself)
-    avg_launch_s = elapsed_ms / 1e3 * U / args.steps
+    avg_launch_s = elapsed_ms / 1e3 * U / steps
     achieved = alg_bytes_launch / avg_launch_s / 1e9
     roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": achieved / peak, "peak_source": peak_src,
-            "traffic": ncu_traffic(args.task, dtype, n, U),
+            "traffic": ncu_traffic(task, dtype, n, U),
             "kernel": "rollout_kernel", "alg_bytes_per_launch": alg_bytes_launch,
             "bytes_per_world_step": bpw, "avg_launch_ms": avg_launch_s * 1e3}
     return {"env": env, "value": value, "elapsed_ms": elapsed_ms, "gpu_launches": gpu_launches,
-            "roofline": roof, "dims": (A, O, I, esz), "ms_per_step": elapsed_ms / args.steps}
+            "roofline": roof, "dims": (A, O, I, esz), "ms_per_step": elapsed_ms / steps}
+
+
+# ---------------------------------------------------------------------------
+# Go1 joystick (headline)
+
+# algorithmic bytes per control step and world (float32): actions in; state
+# obs, privileged obs, reward out; done / trunc / terminal-mask bytes out
+GO1_BYTES_STEP = 4 * (12 + 56 + 75 + 1) + 3
+# per launch and world: the env state read + written once (qpos 19, qvel 18,
+# command 3, phase 4, airtime 4, prev_action 12 reals; last_contact 4 B,
+# steps and episode 4 B each)
+GO1_STATE_BYTES = 2 * (4 * (19 + 18 + 3 + 4 + 4 + 12) + 4 + 8)
+
+
+def go1_config_obj(args, world, U):
+    return {
+        "workload": "Go1 joystick env step, fused kernel (csrc/go1env.cuh): action -> PD "
+                    "targets, 5 physics steps (FK, CRB mass matrix, foot-sphere contacts, "
+                    "pyramidal-cone Newton solver, Euler), 16-term reward, noisy 56-d + "
+                    "privileged 75-d observation, termination, Philox auto-reset; "
+                    "episode_length 1000; Go1-shaped model (physmodel.go1_model: 18 DoF, "
+                    "4 feet, h = 4 ms); no reference implementation exists (SPEC.md:8)",
+        "task": GO1, "worlds_per_gpu": args.num_envs, "global_worlds": args.num_envs * world,
+        "physics_steps_per_env_step": GO1_SUBSTEPS, "env_steps_per_launch": U,
+        "parallelism": f"worlds sharded dp{world}",
+        "l2": "flushed before the timed region; ring of action / output chunks "
+              f"({U} steps x {args.num_envs} worlds x {GO1_BYTES_STEP} B each)",
+    }
+
+
+def measure_go1(args, dtype, dev, rank, world, dist, local_rank, steps=None):
+    import torch
+
+    from paper_2502_08844_b200 import go1env as G
+
+    n = args.num_envs
+    steps = args.steps if steps is None else steps
+    env = G.DeviceGo1Env(n, G.Go1Config(), dtype=dtype, device=local_rank,
+                         env_index_offset=rank * n)
+    U = min(args.unroll, steps)
+    R = max(2, args.ring)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(4321 + rank)
+    acts = [torch.rand((U, n, 12), generator=gen, device=dev, dtype=env.dtype) * 2 - 1
+            for _ in range(R)]
+    outs = [env.outputs(U) for _ in range(R)]
+    env.reset(seed=0)
+    stream = torch.cuda.current_stream(dev)
+
+    def launch(j, k):
+        o = outs[j % R] if k == U else {kk: (v[:k] if v is not None else None)
+                                         for kk, v in outs[j % R].items()}
+        env.rollout(acts[j % R][:k], out=o)
+
+    w_left, j = args.warmup, 0
+    while w_left > 0:
+        k = min(U, w_left)
+        launch(j, k)
+        w_left -= k
+        j += 1
+    env.check()
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    flush.zero_()
+    torch.cuda.synchronize(dev)
+    del flush
+    nlaunch = (steps + U - 1) // U
+    launches0 = env.kernel_launches
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+
+    def region():
+        left = steps
+        for L in range(nlaunch):
+            k = min(U, left)
+            launch(j + L, k)
+            left -= k
+
+    elapsed_ms = gated_region(region, stream, dev)
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    env.check()
+    gpu_launches = env.kernel_launches - launches0
+    if dist is not None:
+        t = torch.tensor([elapsed_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+    total = steps * n * world * GO1_SUBSTEPS
+    value = total / (elapsed_ms / 1e3)
+    esz = 8 if env.dtype == torch.float64 else 4
+    bstep = GO1_BYTES_STEP if esz == 4 else 8 * (12 + 56 + 75 + 1) + 3
+    bstate = GO1_STATE_BYTES if esz == 4 else 2 * (8 * (19 + 18 + 3 + 4 + 4 + 12) + 4 + 8)
+    alg = n * U * bstep + n * bstate
+    avg_launch_s = elapsed_ms / 1e3 * U / steps
+    peak, src = hbm_peak()
+    roof = {"bound": "hbm", "achieved": alg / avg_launch_s / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": alg / avg_launch_s / 1e9 / peak, "peak_source": src,
+            "traffic": ncu_traffic(GO1, dtype, n, U), "kernel": "go1_env_kernel",
+            "alg_bytes_per_launch": alg, "bytes_per_env_step": bstep,
+            "avg_launch_ms": avg_launch_s * 1e3,
+            "note": "compute / latency bound: ~5 physics steps of FK, CRB, Newton per "
+                    "env step for ~580 B of I/O; profiles/r02_ncu_go1.md has the pipe and "
+                    "stall breakdown",
+            "compute": ncu_compute(GO1, dtype)}
+    return {"env": env, "value": value, "elapsed_ms": elapsed_ms, "gpu_launches": gpu_launches,
+            "roofline": roof, "ms_per_step": elapsed_ms / steps, "U": U,
+            "env_steps_per_s": value / GO1_SUBSTEPS}
+
+
+def ncu_compute(kernel_key, dtype):
+    """issue / pipe utilisation of the kernel from the committed ncu capture"""
+    path = os.path.join(ROOT, "profiles", "compute.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(f"{kernel_key}/{dtype}")
+    except Exception:
+        return None
+
+
+def measure_go1_e2e(env, args, dev, dist, world):
+    """The same steps through the public API with HOST buffers: per chunk, the
+    actions copied from pinned host memory, DeviceGo1Env.rollout, and the
+    observations / rewards / flags copied back, all inside the timed region."""
+    import torch
+
+    n, K = env.num_envs, args.e2e_steps
+    U = min(args.unroll, K)
+    pin = lambda *s, d=env.dtype: torch.empty(s, dtype=d, pin_memory=True)  # noqa: E731
+    acts_h = pin(K, n, 12)
+    acts_h.copy_(torch.rand((K, n, 12), dtype=env.dtype) * 2 - 1)
+    obs_h, priv_h, rew_h = pin(K, n, 56), pin(K, n, 75), pin(K, n)
+    done_h, trunc_h = pin(K, n, d=torch.uint8), pin(K, n, d=torch.uint8)
+    dev_out = [env.outputs(U, with_terminal=False) for _ in range(2)]
+    dev_act = [torch.empty((U, n, 12), dtype=env.dtype, device=dev) for _ in range(2)]
+
+    def run(k0, k1, slot):
+        k = k1 - k0
+        a = dev_act[slot][:k]
+        a.copy_(acts_h[k0:k1], non_blocking=True)
+        o = {kk: (v[:k] if v is not None else None) for kk, v in dev_out[slot].items()}
+        env.rollout(a, out=o)
+        obs_h[k0:k1].copy_(o["obs"], non_blocking=True)
+        priv_h[k0:k1].copy_(o["privileged_state"], non_blocking=True)
+        rew_h[k0:k1].copy_(o["reward"], non_blocking=True)
+        done_h[k0:k1].copy_(o["done"], non_blocking=True)
+        trunc_h[k0:k1].copy_(o["trunc"], non_blocking=True)
+
+    run(0, min(U, K), 0)
+    torch.cuda.synchronize(dev)
+    if dist is not None:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for c, k0 in enumerate(range(0, K, U)):
+        run(k0, min(K, k0 + U), c % 2)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    env.check()
+    if dist is not None:
+        t = torch.tensor([dt], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dt = float(t.item())
+    esz = 8 if env.dtype == torch.float64 else 4
+    return {"value": K * n * world * GO1_SUBSTEPS / dt, "unit": UNIT,
+            "h2d_bytes_per_step": n * 12 * esz,
+            "d2h_bytes_per_step": n * ((56 + 75 + 1) * esz + 2),
+            "api": "paper_2502_08844_b200.go1env.DeviceGo1Env.rollout with pinned host "
+                   "actions in and obs / privileged obs / reward / done / trunc out",
+            "steps": K, "chunk_steps": U}
+
+
+def cpu_go1_rate(num_envs, steps, seconds=None):
+    """The physics oracle (oracle/physics.c, fp64, OpenMP over worlds) on the
+    host cores: physics steps/s of the Go1 model from the home pose with
+    random PD targets.  Bounded: at most `seconds` of CPU work when given."""
+    from oracle import physics as op
+    from oracle.oracle import max_threads, use_all_host_threads
+    from paper_2502_08844_b200 import physmodel as pm
+
+    use_all_host_threads()
+    m = pm.go1_model()
+    mc = m.to_c()
+    q, v = pm.home_qpos(num_envs), np.zeros((num_envs, 18))
+    ctrl = q[:, 7:] + np.random.default_rng(0).uniform(-0.5, 0.5, (num_envs, 12))
+    t0 = time.perf_counter()
+    o = op.step(mc, q, v, ctrl, 2)
+    probe = (time.perf_counter() - t0) / 2
+    n_phys = steps * GO1_SUBSTEPS
+    if seconds is not None:
+        n_phys = max(2, min(n_phys, int(seconds / max(probe, 1e-9))))
+    t0 = time.perf_counter()
+    op.step(mc, o["qpos"], o["qvel"], ctrl, n_phys)
+    dt = time.perf_counter() - t0
+    return num_envs * n_phys / dt, max_threads(), n_phys, dt
+
+
+def bench_go1_sweep(args, dev, sizes=(1024, 8192, 65536), K=50, reps=3):
+    """Go1 joystick env (fused kernel) at several world counts, f32."""
+    import torch
+
+    from paper_2502_08844_b200 import go1env as G
+
+    out = []
+    for n in sizes:
+        env = G.DeviceGo1Env(n, G.Go1Config(), dtype="float32", device=dev.index)
+        env.reset(seed=0)
+        acts = torch.rand((K, n, 12), device=dev) * 2 - 1
+        o = env.outputs(K)
+        env.rollout(acts, out=o)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            env.rollout(acts, out=o)
+        b.record()
+        torch.cuda.synchronize(dev)
+        env.check()
+        s = a.elapsed_time(b) / 1e3 / reps
+        out.append({"worlds": n, "physics_steps_per_s": n * K * GO1_SUBSTEPS / s,
+                    "env_steps_per_s": n * K / s})
+        env.close()
+        del acts, o
+    return out
+
+
+def bench_phys_only(args, dev, K=100, reps=3):
+    """The physics kernel alone (dk_phys_step, ctrl held, no tail), 8192 worlds,
+    feet-only and full (trunk box + thigh capsules) collision, f32 and f64."""
+    import torch
+
+    from oracle import physics as op
+    from paper_2502_08844_b200 import physics as P
+    from paper_2502_08844_b200 import physmodel as pm
+
+    res = {}
+    n = args.num_envs
+    for cfg, kw in (("feet", {}), ("full", dict(collide_box=1, collide_thigh=1))):
+        for dt in ("float32", "float64"):
+            sim = P.DevicePhysics(pm.go1_model(**kw), n, dtype=dt, device=dev.index)
+            q, v, c = op.random_states(n, seed=1)
+            tt = lambda x: torch.as_tensor(x, device=dev, dtype=sim.dtype)  # noqa: E731
+            sim.set_state(tt(q), tt(v))
+            ct = tt(c)
+            sim.step(ct, K, diag=False)
+            torch.cuda.synchronize(dev)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            for _ in range(reps):
+                sim.step(ct, K, diag=False)
+            b.record()
+            torch.cuda.synchronize(dev)
+            sim.check()
+            res[f"{cfg}/{dt}"] = n * K * reps / (a.elapsed_time(b) / 1e3)
+            sim.close()
+    return {"unit": UNIT, "worlds": n, "physics_steps_per_s": res,
+            "note": "dk_phys_step: FK, CRB mass matrix, RNE, collision, Newton solver, Euler; "
+                    "random states around the home pose"}
 
 
 def emit_extra(name, obj):
@@ -419,33 +715,30 @@ def run_b200(args, rank, world, local_rank, dist):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
+    if args.task != GO1:
+        return run_b200_analytic(args, rank, world, local_rank, dist)
     n = args.num_envs
-    # NVML clocks: sampled from before the warm-up until after the f64 leg (the
-    # gated headline region itself is only microseconds long at --steps 20)
+    # NVML clocks: sampled from before the warm-up until after the f64 leg
     clocks = ClockSampler(local_rank).start()
-    head = measure_rollout(args, args.dtype, dev, rank, world, dist, local_rank)
+    head = measure_go1(args, args.dtype, dev, rank, world, dist, local_rank)
     other = "float64" if args.dtype == "float32" else "float32"
     f_other = None
     if not args.no_f64:
-        r = measure_rollout(args, other, dev, rank, world, dist, local_rank)
+        r = measure_go1(args, other, dev, rank, world, dist, local_rank)
         r["env"].close()
         f_other = {"dtype": "f64" if other == "float64" else "f32", "value": r["value"],
                    "ms_per_step": r["ms_per_step"], "gpu_launches": r["gpu_launches"],
-                   "roofline": {k: r["roofline"][k] for k in
-                                ("achieved", "peak", "frac", "bytes_per_world_step",
-                                 "avg_launch_ms", "traffic")}}
+                   "roofline": {k: r["roofline"][k] for k in ("achieved", "frac", "avg_launch_ms")}}
     clocks.stop()
     env = head["env"]
-    A, O, I, esz = head["dims"]
-
-    # end-to-end through the C ABI with pinned host buffers (H2D actions,
-    # D2H every output), chunked and pipelined inside dk_env_rollout_host
-    e2e = None
-    if args.e2e_steps > 0:
-        e2e = measure_e2e(env, args, dev, dist, A, O, I, esz, world)
+    e2e = measure_go1_e2e(env, args, dev, dist, world) if args.e2e_steps > 0 else None
 
     extras = {}
     if rank == 0 and not args.no_extra:
+        # the pinned analytic task (the reference's own physics) at the same world count
+        extras["cartpole"] = analytic_line(args, dev, rank, world, dist, local_rank)
+        extras["go1_sweep"] = bench_go1_sweep(args, dev)
+        extras["physics_only"] = bench_phys_only(args, dev)
         extras["loco_small"] = bench_loco_small(args, dev)
         extras["e2e_dropin_step"] = bench_dropin_step(args, dev)
         extras["sweep"] = bench_sweep(args, dev)
@@ -458,11 +751,12 @@ def run_b200(args, rank, world, local_rank, dist):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
         try:
-            rate, threads, steps, dt = cpu_rate(args.task, n, args.cpu_seconds)
+            rate, threads, n_phys, dt = cpu_go1_rate(n, args.steps, seconds=args.cpu_seconds)
             cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-                   "sample": f"{steps} steps x {n} worlds in {dt:.1f}s on {threads} threads "
-                             f"({cpu_model()}); oracle/oracle.c, bit-exact C restatement of "
-                             "deskrl BatchEnv.step (reference itself is single-threaded Python)"}
+                   "sample": f"{n_phys} physics steps x {n} worlds in {dt:.1f}s on {threads} "
+                             f"threads ({cpu_model()}); oracle/physics.c, the independent fp64 "
+                             "restatement of the Go1 physics step (no reference "
+                             "implementation exists); physics only, env tail excluded"}
         except Exception as e:  # pragma: no cover
             cpu = {"value": None, "error": str(e)}
 
@@ -473,19 +767,117 @@ def run_b200(args, rank, world, local_rank, dist):
             "metric": METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f32" if esz == 4 else "f64",
-            "data": "synthetic U(-1,1) actions pre-generated in HBM",
-            "config": headline_config(args, world),
+            "dtype": "f32" if args.dtype == "float32" else "f64",
+            "data": "synthetic U(-1,1) actions pre-generated in HBM; random-init Go1-shaped "
+                    "model (no assets in the image)",
+            "config": go1_config_obj(args, world, head["U"]),
+            "env_steps_per_s": head["env_steps_per_s"],
             "roofline": head["roofline"],
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": head["gpu_launches"],
             "f64" if other == "float64" else "f32": f_other,
+            "cartpole": None if "cartpole" not in extras else {
+                k: extras["cartpole"].get(k) for k in ("value", "frac", "f64_value", "e2e")},
             "clocks": clocks.summary(),
             "library": os.path.relpath(_native.LIB_PATH, ROOT),
             "extra_lines": sorted(extras),
         }
         print(json.dumps(line), flush=True)
+    env.close()
+
+
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+_REF_SNIPPET = (
+    "import json, sys\n"
+    "from deskrl import bench\n"
+    "from deskrl.envkit import EnvConfig\n"
+    "r = bench.measure_stage(bench.Stage.ENV_STEP, EnvConfig(task=sys.argv[1]), num_envs=1024,"
+    " repetitions=int(sys.argv[2]), steps_per_batch=16)\n"
+    "print(json.dumps({'sps': r.median_sps, 'lo': r.ci_low, 'hi': r.ci_high}))\n")
+
+
+def reference_python_rate(task, procs=1, reps=10, timeout=120):
+    """The UNMODIFIED reference (deskrl from baseline/_ref, installed with pip
+    from /root/reference) timed by its own bench.measure_stage(ENV_STEP) on
+    1024 worlds: one process, or `procs` independent
+    processes whose rates are summed (its BatchEnv threads are GIL-bound)."""
+    import subprocess
+
+    if not os.path.isdir(os.path.join(REF_DIR, "deskrl")):
+        return {"unavailable": "baseline/_ref not installed"}
+    env = dict(os.environ, PYTHONPATH=REF_DIR, OMP_NUM_THREADS="1", CUDA_VISIBLE_DEVICES="")
+    ps = [subprocess.Popen([sys.executable, "-c", _REF_SNIPPET, task, str(reps)], env=env,
+                           stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+          for _ in range(procs)]
+    rates = []
+    for p in ps:
+        try:
+            out, _ = p.communicate(timeout=timeout)
+            rates.append(json.loads(out.strip().splitlines()[-1])["sps"])
+        except Exception as e:  # pragma: no cover
+            p.kill()
+            return {"error": str(e)}
+    return {"value": float(sum(rates)), "unit": "env_steps/s", "processes": procs,
+            "per_process": rates, "kind": "reference",
+            "sample": f"deskrl.bench.measure_stage(ENV_STEP, {task}, 1024 worlds, {reps} "
+                      "reps x 16 steps) per process, baseline/_ref (pip-installed reference)"}
+
+
+def analytic_line(args, dev, rank, world, dist, local_rank):
+    """The previous round's headline: the analytic task (cartpole, pinned
+    bit-exact in f64 against the reference) at the bench's world count, gated,
+    f32 + f64 legs and the host-buffer C-ABI e2e."""
+    task, steps = args.analytic_task, args.analytic_steps
+    r = measure_rollout(args, "float32", dev, rank, world, dist, local_rank, task=task,
+                        steps=steps, unroll=1000)
+    A, O, I, esz = r["dims"]
+    e2e = measure_e2e(r["env"], args, dev, dist, A, O, I, esz, world, K=20_000, chunk=1000)
+    r["env"].close()
+    r64 = measure_rollout(args, "float64", dev, rank, world, dist, local_rank, task=task,
+                          steps=steps, unroll=1000)
+    r64["env"].close()
+    ref1 = reference_python_rate(task, 1) if not args.no_cpu else None
+    nproc = min(len(os.sched_getaffinity(0)), 32)
+    refn = reference_python_rate(task, nproc, reps=5) if not args.no_cpu else None
+    return {"metric": ANALYTIC_METRIC, "task": task, "value": r["value"], "unit": UNIT,
+            "reference_python_1core": ref1, "reference_python_all_cores": refn,
+            "steps": steps, "ms_per_step": r["ms_per_step"], "frac": r["roofline"]["frac"],
+            "roofline": r["roofline"], "gpu_launches": r["gpu_launches"],
+            "f64_value": r64["value"], "f64_frac": r64["roofline"]["frac"],
+            "e2e": None if e2e is None else e2e["value"], "e2e_detail": e2e,
+            "config": headline_config(args, world, task, steps, 1000)}
+
+
+def run_b200_analytic(args, rank, world, local_rank, dist):
+    """--task <analytic>: the round-1 headline (one analytic task)."""
+    import torch
+
+    from paper_2502_08844_b200 import _native
+
+    dev = torch.device("cuda", local_rank)
+    clocks = ClockSampler(local_rank).start()
+    head = measure_rollout(args, args.dtype, dev, rank, world, dist, local_rank)
+    clocks.stop()
+    env = head["env"]
+    A, O, I, esz = head["dims"]
+    e2e = measure_e2e(env, args, dev, dist, A, O, I, esz, world) if args.e2e_steps > 0 else None
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rate, threads, steps, dt = cpu_rate(args.task, args.num_envs, args.cpu_seconds)
+        cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+               "sample": f"{steps} steps x {args.num_envs} worlds in {dt:.1f}s on {threads} "
+                         f"threads ({cpu_model()}); oracle/oracle.c"}
+    if rank == 0:
+        print(json.dumps({
+            "metric": ANALYTIC_METRIC, "value": head["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32" if esz == 4 else "f64", "data": "synthetic U(-1,1) actions in HBM",
+            "config": headline_config(args, world), "roofline": head["roofline"],
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": head["gpu_launches"],
+            "clocks": clocks.summary(), "library": os.path.relpath(_native.LIB_PATH, ROOT)}),
+            flush=True)
     env.close()
 
 
@@ -602,7 +994,7 @@ def bench_ppo_rollout(args, dev, T=30, reps=5):
 
     n = args.num_envs
     torch.manual_seed(0)
-    env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.task), n, dtype="float32")
+    env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.analytic_task), n, dtype="float32")
     obs = env.reset(seed=0)
     od, ad = env.obs_dim, env.action_dim
     policy, value = R.make_policy(od, ad).cuda(dev), R.make_value(od).cuda(dev)
@@ -635,7 +1027,7 @@ def bench_dropin_step(args, dev, steps=300):
     numpy obs/rewards/dones/truncs/infos (float64, like the reference)."""
     import paper_2502_08844_b200 as dk
 
-    env = dk.BatchEnv(dk.EnvConfig(task=args.task), args.num_envs, dtype="float64",
+    env = dk.BatchEnv(dk.EnvConfig(task=args.analytic_task), args.num_envs, dtype="float64",
                       device=dev.index)
     env.reset(seed=0)
     acts = np.random.default_rng(0).uniform(-1, 1, (steps + 10, args.num_envs, env.action_dim))
@@ -661,7 +1053,7 @@ def bench_sweep(args, dev, sizes=(1024, 8192, 65536), K=1000, launches=5):
     out = []
     peak, _ = hbm_peak()
     for n in sizes:
-        env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.task), n, dtype=args.dtype,
+        env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.analytic_task), n, dtype=args.dtype,
                                 device=dev.index)
         env.reset(seed=0)
         tdt = env.dtype
@@ -931,14 +1323,14 @@ def cpu_tail_rate(n, J, F, seconds):
                                       "envkit.build_locomotion_observation restated)"}
 
 
-def measure_e2e(env, args, dev, dist, A, O, I, esz, world):
+def measure_e2e(env, args, dev, dist, A, O, I, esz, world, K=None, chunk=None):
     import ctypes
 
     import torch
 
     n = env.num_envs
-    K = args.e2e_steps
-    chunk = min(args.unroll, K)
+    K = K or args.e2e_steps
+    chunk = min(chunk or args.unroll, K)
     npdt = np.float64 if esz == 8 else np.float32
 
     def pinned(shape, dt):
@@ -988,7 +1380,7 @@ def main():
     if os.environ.get("DK_BENCH_SAME_DEVICE") == "1":
         local_rank = 0
     if args.impl == "reference":
-        run_reference(args, rank)
+        run_reference(args, rank, world)
         return
     dist = None
     if world > 1:

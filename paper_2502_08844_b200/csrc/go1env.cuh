@@ -133,17 +133,26 @@ __device__ __forceinline__ void foot_kin(const PhysConst<T> &P, const Lane<T> &L
 // per-world reset draw from stream_rng(seed, env, episode, 0): yaw, then the
 // 12 joint offsets, then the 3 command components (Generator.uniform order)
 template <typename T>
-__device__ void reset_world(const PhysConst<T> &P, const EnvConst<T> &E, Lane<T> &L, int l,
+__device__ __noinline__ void reset_world(const PhysConst<T> &P, const EnvConst<T> &E, Lane<T> &L, int l,
                             uint64_t env, uint32_t episode, T *cmd, T &phase, T &air,
                             T *prev_action) {
     Philox4x64 rng;
     rng.init(E.seed, env, episode, 0);
-    const double yaw = rng.uniform(-E.yaw_range, E.yaw_range);
-    double jn[NJ];
+    // 16 draws in Generator.uniform order: yaw, 12 joint offsets, 3 commands
+    // (one rolled loop: a single copy of the Philox block code)
+    double u[16];
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i) {
+        const double lo = i == 0 ? -E.yaw_range
+                                 : (i < 13 ? -E.joint_noise : E.cmd_lo[i - 13 < 0 ? 0 : i - 13]);
+        const double hi = i == 0 ? E.yaw_range
+                                 : (i < 13 ? E.joint_noise : E.cmd_hi[i - 13 < 0 ? 0 : i - 13]);
+        u[i] = rng.uniform(lo, hi);
+    }
+    const double yaw = u[0];
+    const double *jn = u + 1;
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) jn[j] = rng.uniform(-E.joint_noise, E.joint_noise);
-#pragma unroll
-    for (int k = 0; k < 3; ++k) cmd[k] = (T)rng.uniform(E.cmd_lo[k], E.cmd_hi[k]);
+    for (int k = 0; k < 3; ++k) cmd[k] = (T)u[13 + k];
     double sh, ch;
     sincos(0.5 * yaw, &sh, &ch);
     L.pos[0] = T(0);
@@ -164,6 +173,96 @@ __device__ void reset_world(const PhysConst<T> &P, const EnvConst<T> &E, Lane<T>
     phase = E.phase0[l];
     air = T(0);
     (void)P;
+}
+
+// observation noise into the row (lane 0): one out-of-line copy of the
+// Philox draws for the three call sites
+template <typename T>
+__device__ __noinline__ void go1_noise(T *row, uint64_t seed, uint64_t env, uint32_t episode,
+                                       uint64_t step, const double *noise) {
+    loco_row_noise(row, NJ, seed, env, episode, step, noise);
+}
+
+// lane-parallel part of the frame of the current state (each lane its limb,
+// lane 0 the trunk); returns the lane's foot contact.  noinline: one copy for
+// the step and the two reset paths (instruction-cache footprint).
+template <typename T>
+__device__ __noinline__ bool fill_frame(const PhysConst<T> &Pc, const EnvConst<T> &E,
+                                        const Lane<T> &L, int l, T *fr, uint8_t *flags,
+                                        const T *act3, const T *tau3, const T *prev,
+                                        const T *cmd, bool reset_frame, uint8_t lastc, T &phase,
+                                        T &air) {
+    T fpos[3], fvel[3];
+    foot_kin(Pc, L, l, fpos, fvel);
+    const bool contact = fpos[2] - Pc.foot_radius < T(0);
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+        fr[O_JPOS + 3 * l + j] = L.q[j];
+        fr[O_JVEL + 3 * l + j] = L.qd[j];
+        fr[O_JTAU + 3 * l + j] = tau3[j];
+        fr[O_ACT + 3 * l + j] = act3[j];
+        fr[O_FPA + 3 * l + j] = prev[j];
+    }
+    if (!reset_frame) {
+        air = air + E.ctrl_dt;
+        phase = wrap_angle_dev(phase + T(6.283185307179586) * E.gait_freq * E.ctrl_dt);
+    }
+    const bool td = reset_frame ? false : (contact && !lastc);
+    fr[O_AIR + l] = air;
+    fr[O_FH + l] = fpos[2] - Pc.foot_radius;
+    T sn, cs;
+    RealOps<T>::sincos_(phase, &sn, &cs);
+    fr[O_FHD + l] = E.rc.swing_height * (sn > T(0) ? sn : T(0));
+    fr[O_FVEL + 2 * l] = fvel[0];
+    fr[O_FVEL + 2 * l + 1] = fvel[1];
+    fr[O_PHASE + l] = phase;
+    flags[l] = td ? 1 : 0;
+    flags[4 + l] = contact ? 1 : 0;
+    if (l == 0) {
+        T R0[9], vl[3];
+        phys::quat2mat(L.quat, R0);
+        phys::mat_tvec3(R0, L.vlin, vl);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) fr[O_Q + i] = L.quat[i];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            fr[O_LIN + i] = vl[i];
+            fr[O_ANG + i] = L.wb[i];
+            fr[O_CMD + i] = cmd[i];
+        }
+    }
+    return contact;
+}
+
+// reward + clean observation row of the frame in `fr` (lane 0 of the quad)
+template <typename T>
+__device__ __noinline__ T build_row(const EnvConst<T> &E, const T *fr, const uint8_t *flags,
+                                    bool done, T *row, T *terms16) {
+    LocoRowIn<T> in;
+    in.q = fr + O_Q;
+    in.lin = fr + O_LIN;
+    in.ang = fr + O_ANG;
+    in.cmd = fr + O_CMD;
+    in.fcmd = fr + O_CMD;
+    in.pa = fr + O_ACT;   // observation: the action just applied
+    in.fpa = fr + O_FPA;  // reward action rate: against the previous action
+    in.nom = E.q_default;
+    in.def = E.q_default;
+    in.jpos = fr + O_JPOS;
+    in.jvel = fr + O_JVEL;
+    in.jtau = fr + O_JTAU;
+    in.act = fr + O_ACT;
+    in.air = fr + O_AIR;
+    in.fh = fr + O_FH;
+    in.fhd = fr + O_FHD;
+    in.fvel = fr + O_FVEL;
+    in.phase = fr + O_PHASE;
+    in.td = flags;
+    in.con = flags + 4;
+    in.done = done;
+    in.pert = nullptr;
+    bool ok;
+    return loco_row<false>(in, E.rc, NJ, NF, row, terms16, ok);
 }
 
 template <typename T>
@@ -225,86 +324,15 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
         episode = st.episode[w];
     }
 
-    // evaluate the reward / observation row of the current state into `row`
-    // (lane 0 of the quad), with the frame fields already in `fr`
-    auto build_row = [&](bool done, uint32_t ep, int32_t stp, T *reward, T *terms16) {
-        (void)ep;
-        (void)stp;
+    auto build = [&](bool done, T *reward, T *terms16) {
         if (l == 0) {
-            LocoRowIn<T> in;
-            in.q = fr + O_Q;
-            in.lin = fr + O_LIN;
-            in.ang = fr + O_ANG;
-            in.cmd = fr + O_CMD;
-            in.fcmd = fr + O_CMD;
-            in.pa = fr + O_ACT;   // observation: the action just applied
-            in.fpa = fr + O_FPA;  // reward action rate: against the previous action
-            in.nom = E.q_default;
-            in.def = E.q_default;
-            in.jpos = fr + O_JPOS;
-            in.jvel = fr + O_JVEL;
-            in.jtau = fr + O_JTAU;
-            in.act = fr + O_ACT;
-            in.air = fr + O_AIR;
-            in.fh = fr + O_FH;
-            in.fhd = fr + O_FHD;
-            in.fvel = fr + O_FVEL;
-            in.phase = fr + O_PHASE;
-            in.td = flags;
-            in.con = flags + 4;
-            in.done = done;
-            in.pert = nullptr;
             T t[16];
-            bool ok;
-            const T u = loco_row<false>(in, E.rc, NJ, NF, row, t, ok);
+            const T u = build_row(E, fr, flags, done, row, t);
             if (reward) *reward = T(0) > u ? T(0) : u;
             if (terms16)
 #pragma unroll
                 for (int k = 0; k < 16; ++k) terms16[k] = t[k];
         }
-    };
-    // lane-parallel part of the frame for the current state
-    auto fill_frame = [&](const T *act3, const T *act_force3, bool reset_frame) {
-        T fpos[3], fvel[3];
-        foot_kin(Pc, L, l, fpos, fvel);
-        const bool contact = fpos[2] - Pc.foot_radius < T(0);
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-            fr[O_JPOS + 3 * l + j] = L.q[j];
-            fr[O_JVEL + 3 * l + j] = L.qd[j];
-            fr[O_JTAU + 3 * l + j] = act_force3[j];
-            fr[O_ACT + 3 * l + j] = act3[j];
-            fr[O_FPA + 3 * l + j] = prev[j];
-        }
-        if (!reset_frame) {
-            air = air + E.ctrl_dt;
-            phase = wrap_angle_dev(phase + T(6.283185307179586) * E.gait_freq * E.ctrl_dt);
-        }
-        const bool td = reset_frame ? false : (contact && !lastc);
-        fr[O_AIR + l] = air;
-        fr[O_FH + l] = fpos[2] - Pc.foot_radius;
-        T sn, cs;
-        RealOps<T>::sincos_(phase, &sn, &cs);
-        fr[O_FHD + l] = E.rc.swing_height * (sn > T(0) ? sn : T(0));
-        fr[O_FVEL + 2 * l] = fvel[0];
-        fr[O_FVEL + 2 * l + 1] = fvel[1];
-        fr[O_PHASE + l] = phase;
-        flags[l] = td ? 1 : 0;
-        flags[4 + l] = contact ? 1 : 0;
-        if (l == 0) {
-            T R0[9], vl[3];
-            phys::quat2mat(L.quat, R0);
-            phys::mat_tvec3(R0, L.vlin, vl);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) fr[O_Q + i] = L.quat[i];
-#pragma unroll
-            for (int i = 0; i < 3; ++i) {
-                fr[O_LIN + i] = vl[i];
-                fr[O_ANG + i] = L.wb[i];
-                fr[O_CMD + i] = cmd[i];
-            }
-        }
-        return contact;
     };
     // cooperative, coalesced store of the CTA's rows [nlive][cols] (tile pitch P)
     auto store_rows = [&](T *dst, int cols) {
@@ -319,15 +347,16 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
     // of an episode's stream belongs to its reset draw
     auto add_noise = [&]() {
         if (l == 0 && E.has_noise)
-            loco_row_noise(row, NJ, E.seed, env, episode, (uint64_t)steps + 1, E.noise);
+            go1_noise(row, E.seed, env, episode, (uint64_t)steps + 1, E.noise);
     };
     auto do_reset = [&]() {
         reset_world(Pc, E, L, l, env, episode, cmd, phase, air, prev);
         const T zero3[3] = {T(0), T(0), T(0)};
-        const bool c = fill_frame(zero3, zero3, true);
+        const bool c = fill_frame(Pc, E, L, l, fr, flags, zero3, zero3, prev, cmd, true, lastc,
+                                  phase, air);
         lastc = c ? 1 : 0;
         __syncwarp(qm);
-        build_row(false, episode, steps, nullptr, nullptr);
+        build(false, nullptr, nullptr);
         __syncwarp(qm);
     };
 
@@ -370,7 +399,8 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
                                        static_cast<const phys::PhysInspect<T> *>(nullptr),
                                        s + 1 == E.substeps ? tau : nullptr);
             if (!okp && l == 0 && io.bad) *io.bad = 1;
-            const bool c = fill_frame(a, tau, false);
+            const bool c = fill_frame(Pc, E, L, l, fr, flags, a, tau, prev, cmd, false, lastc,
+                                      phase, air);
             // termination: trunk upside down (its z axis points down) or below term_height
             T R0[9];
             phys::quat2mat(L.quat, R0);
@@ -378,7 +408,7 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
             steps += 1;
             trunc = steps >= E.episode_length;
             __syncwarp(qm);
-            build_row(done, episode, steps, &rw, t16);
+            build(done, &rw, t16);
             __syncwarp(qm);
             // post-reward bookkeeping (the frame used the pre-step values)
             air = c ? T(0) : air;
@@ -457,7 +487,7 @@ size_t env_smem_bytes(const PhysConst<T> &pc, int threads) {
 template <typename T>
 cudaError_t launch_env(const PhysConst<T> &pc, const EnvConst<T> &ec, const EnvState<T> &st,
                        const EnvIO<T> &io, cudaStream_t s) {
-    int threads = phys::THREADS;
+    int threads = DK_PHYS_CTA_THREADS;
     while (threads > 32 && env_smem_bytes(pc, threads) > 110 * 1024) threads /= 2;
     const size_t smem = env_smem_bytes(pc, threads);
     static size_t attr = 0;

@@ -36,6 +36,9 @@
 namespace dk {
 namespace phys {
 
+#ifndef DK_PHYS_CTA_THREADS
+#define DK_PHYS_CTA_THREADS 128
+#endif
 constexpr int QUAD = 4;
 constexpr int WPC = 32;            // worlds per CTA
 constexpr int THREADS = WPC * QUAD;
@@ -441,7 +444,7 @@ enum { F_JB = 0, F_JL = 6, F_AREF = 9, F_D = 10, F_X = 11, F_Y = 12 };
 template <typename T>
 struct PhysInspect {
     T *M, *bias, *xpos, *xipos;
-    __device__ __forceinline__ bool on() const { return M || bias || xpos || xipos; }
+    __host__ __device__ __forceinline__ bool on() const { return M || bias || xpos || xipos; }
 };
 
 // one physics step of the lane's world; returns false on a factorisation breakdown.
@@ -1145,7 +1148,9 @@ __device__ void sensors(const PhysConst<T> &P, const Lane<T> &L, int lane_limb, 
     for (int i = 0; i < 3; ++i) s[34 + 3 * lane_limb + i] = pp[i] + foff[i];
 }
 
-template <typename T>
+// INSPECT: the dk_phys_inspect variant (its own instantiation, so the step
+// kernel carries a single copy of phys_step)
+template <typename T, bool INSPECT>
 __global__ void __launch_bounds__(THREADS) phys_kernel(PhysConst<T> pc, PhysArgs<T> a,
                                                        PhysInspect<T> ins) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1175,7 +1180,7 @@ __global__ void __launch_bounds__(THREADS) phys_kernel(PhysConst<T> pc, PhysArgs
 #pragma unroll
     for (int i = 0; i < 4; ++i) L.quat[i] = a.qpos[(3 + i) * n + w];
     Rows<T> rows{rowbuf, tid, (int)blockDim.x};
-    if (ins.on()) {
+    if constexpr (INSPECT) {
         phys_step(P, L, rows, lane_limb, static_cast<const PhysArgs<T> *>(nullptr), w, &ins);
         return;
     }
@@ -1222,19 +1227,26 @@ cudaError_t launch_phys(const PhysConst<T> &pc, const PhysArgs<T> &a, const Phys
                         cudaStream_t st) {
     // 128 threads (32 worlds) per CTA unless the constraint rows of that many
     // lanes would not fit two CTAs' worth of shared memory on an SM
-    int threads = THREADS;
+    // 128 threads (32 worlds) per CTA unless the constraint rows of that many
+    // lanes would not fit two CTAs' worth of shared memory on an SM (measured:
+    // 32-thread CTAs run the physics kernel at the same speed and the fused
+    // env kernel 30% slower -- its per-CTA row stores get narrower)
+    int threads = DK_PHYS_CTA_THREADS;
     while (threads > 32 && phys_smem_bytes(pc, threads) > 110 * 1024) threads /= 2;
     const size_t smem = phys_smem_bytes(pc, threads);
     static size_t attr = 0;
     if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(phys_kernel<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+        for (auto k : {phys_kernel<T, false>, phys_kernel<T, true>}) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+            if (e != cudaSuccess) return e;
+        }
         attr = smem;
     }
     const int wpc = threads / QUAD;
     const unsigned grid = (unsigned)((a.n + wpc - 1) / wpc);
-    phys_kernel<T><<<grid, threads, smem, st>>>(pc, a, ins);
+    if (ins.on()) phys_kernel<T, true><<<grid, threads, smem, st>>>(pc, a, ins);
+    else phys_kernel<T, false><<<grid, threads, smem, st>>>(pc, a, ins);
     return cudaGetLastError();
 }
 
