@@ -459,17 +459,13 @@ GO1_STATE_BYTES = 2 * (4 * (19 + 18 + 3 + 4 + 4 + 12) + 4 + 8)
 
 def go1_config_obj(args, world, U):
     return {
-        "workload": "Go1 joystick env step, fused kernel (csrc/go1env.cuh): action -> PD "
-                    "targets, 5 physics steps (FK, CRB mass matrix, foot-sphere contacts, "
-                    "pyramidal-cone Newton solver, Euler), 16-term reward, noisy 56-d + "
-                    "privileged 75-d observation, termination, Philox auto-reset; "
-                    "episode_length 1000; Go1-shaped model (physmodel.go1_model: 18 DoF, "
-                    "4 feet, h = 4 ms); no reference implementation exists (SPEC.md:8)",
+        "workload": "Go1 joystick env step, one fused kernel (go1env.cuh): 5 physics steps "
+                    "(CRB, contacts, Newton) + reward + obs + autoreset; Go1-shaped model, "
+                    "18 DoF, h=4ms; no reference impl (SPEC.md:8)",
         "task": GO1, "worlds_per_gpu": args.num_envs, "global_worlds": args.num_envs * world,
         "physics_steps_per_env_step": GO1_SUBSTEPS, "env_steps_per_launch": U,
         "parallelism": f"worlds sharded dp{world}",
-        "l2": "flushed before the timed region; ring of action / output chunks "
-              f"({U} steps x {args.num_envs} worlds x {GO1_BYTES_STEP} B each)",
+        "l2": "flushed before the timed region; state on chip within a launch",
     }
 
 
@@ -544,9 +540,7 @@ def measure_go1(args, dtype, dev, rank, world, dist, local_rank, steps=None):
             "traffic": ncu_traffic(GO1, dtype, n, U), "kernel": "go1_env_kernel",
             "alg_bytes_per_launch": alg, "bytes_per_env_step": bstep,
             "avg_launch_ms": avg_launch_s * 1e3,
-            "note": "compute / latency bound: ~5 physics steps of FK, CRB, Newton per "
-                    "env step for ~580 B of I/O; profiles/r02_ncu_go1.md has the pipe and "
-                    "stall breakdown",
+            "note": "compute/latency bound; see profiles/r02_ncu_go1.md",
             "compute": ncu_compute(GO1, dtype)}
     return {"env": env, "value": value, "elapsed_ms": elapsed_ms, "gpu_launches": gpu_launches,
             "roofline": roof, "ms_per_step": elapsed_ms / steps, "U": U,
@@ -768,8 +762,7 @@ def run_b200(args, rank, world, local_rank, dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f32" if args.dtype == "float32" else "f64",
-            "data": "synthetic U(-1,1) actions pre-generated in HBM; random-init Go1-shaped "
-                    "model (no assets in the image)",
+            "data": "synthetic U(-1,1) actions in HBM; Go1-shaped model (no assets)",
             "config": go1_config_obj(args, world, head["U"]),
             "env_steps_per_s": head["env_steps_per_s"],
             "roofline": head["roofline"],

@@ -5,6 +5,8 @@
 #include "../../include/deskrl_b200.h"
 #include "pixels.cuh"
 
+#include "devguard.h"
+
 extern "C" int dk_internal_fail(int code, const char *msg);  // capi.cu
 
 namespace {
@@ -30,6 +32,7 @@ extern "C" {
 
 int dk_pixels_render_rgb(int64_t n, int w, int h, double pole_length, const double *frames,
                          const double *visuals, int brightness, uint8_t *out, void *stream) {
+    dk::PtrDeviceGuard dg_(out);  // launch on the buffers' device
     if (int rc = check_view(w, h)) return rc;
     if (!frames || !visuals || !out)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "render: missing argument");
@@ -43,6 +46,7 @@ int dk_pixels_advance(int dtype, int64_t n, int obs_dim, const void *obs,
                       const uint8_t *reset_mask, int first, double *history, double *visuals,
                       uint32_t *episode, int randomize, const dk_visual_bounds *bounds,
                       uint64_t seed, int64_t env_index_offset, int skip_words, void *stream) {
+    dk::PtrDeviceGuard dg_(history);  // launch on the buffers' device
     if (!obs || !history || !visuals || !episode || !bounds)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixels advance: missing argument");
     if (obs_dim < 3)
@@ -71,6 +75,7 @@ int dk_pixels_advance(int dtype, int64_t n, int obs_dim, const void *obs,
 
 int dk_pixels_stack(int dtype, int64_t n, int w, int h, double pole_length,
                     const double *history, const double *visuals, void *out, void *stream) {
+    dk::PtrDeviceGuard dg_(out);  // launch on the buffers' device
     if (int rc = check_view(w, h)) return rc;
     if (!history || !visuals || !out)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixels stack: missing argument");
@@ -88,6 +93,7 @@ int dk_pixels_stack(int dtype, int64_t n, int w, int h, double pole_length,
 int dk_pixels_terminal(int dtype, int64_t n, int w, int h, double pole_length, int obs_dim,
                        const void *term_obs, const uint8_t *mask, const double *history,
                        const double *visuals, void *out, void *stream) {
+    dk::PtrDeviceGuard dg_(out);  // launch on the buffers' device
     if (int rc = check_view(w, h)) return rc;
     if (!term_obs || !mask || !history || !visuals || !out)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixels terminal: missing argument");
@@ -107,8 +113,10 @@ int dk_pixels_terminal(int dtype, int64_t n, int w, int h, double pole_length, i
 int dk_pixels_normalize(int in_dtype, int out_dtype, int64_t n, int h, int w, int c,
                         const void *x, int channels_first, double *stats, void *out,
                         void *stream) {
-    if (int rc = check_view(w, h)) return rc;
-    if (c <= 0 || n < 0) return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixel_normalize: shape");
+    dk::PtrDeviceGuard dg_(x);  // launch on the buffers' device
+    // any positive image size (not the renderer's viewport limit), overflow-safe
+    if (c <= 0 || n < 0 || h <= 0 || w <= 0 || (int64_t)h * w > (1LL << 30) / c)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixel_normalize: shape");
     if (n == 0) return DK_OK;
     if (!x || !stats || !out)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "pixel_normalize: missing argument");

@@ -6,6 +6,8 @@
 #include "../../include/deskrl_b200.h"
 #include "ppo_kernels.cuh"
 
+#include "devguard.h"
+
 extern "C" int dk_internal_fail(int code, const char *msg);  // capi.cu
 
 namespace {
@@ -22,7 +24,10 @@ unsigned blocks(int64_t n, int bs) { return (unsigned)((n + bs - 1) / bs); }
 // rows are spread over `lanes` strided accumulators per column: enough threads
 // to fill the GPU, each still summing >= 16 rows
 int64_t pick_lanes(int64_t rows, int dim) {
-    int64_t lanes = (148 * 2048 + dim - 1) / dim;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int64_t lanes = ((int64_t)sms * 2048 + dim - 1) / dim;
     const int64_t cap = (rows + 15) / 16;
     if (lanes > cap) lanes = cap;
     return lanes < 1 ? 1 : lanes;
@@ -76,6 +81,7 @@ extern "C" {
 int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
                const void *values, const void *dones, const void *bootstrap, double gamma,
                double lam, void *advantages, void *returns, void *stream) {
+    dk::PtrDeviceGuard dg_(rewards);  // launch on the buffers' device
     if (!rewards || !values || !dones || !bootstrap || !advantages || !returns)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "compute_gae: missing argument");
     if (num_steps < 0 || num_worlds < 0)
@@ -103,6 +109,7 @@ size_t dk_norm_workspace_bytes(int64_t rows, int dim) {
 int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double count,
                    double *mean, double *var, void *workspace, size_t workspace_bytes,
                    void *stream) {
+    dk::PtrDeviceGuard dg_(batch);  // launch on the buffers' device
     if (!batch || !mean || !var)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer_update: missing argument");
     if (dim <= 0 || rows < 0)
@@ -118,6 +125,7 @@ int dk_norm_update(int dtype, int64_t rows, int dim, const void *batch, double c
 
 int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const double *center,
                    double *sums, void *workspace, size_t workspace_bytes, void *stream) {
+    dk::PtrDeviceGuard dg_(batch);  // launch on the buffers' device
     if (!batch || !sums)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer colsum: missing argument");
     if (dim <= 0 || rows < 0)
@@ -145,6 +153,7 @@ int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const do
 
 int dk_norm_merge(int dim, double count, double batch_count, const double *batch_mean,
                   const double *batch_var, double *mean, double *var, void *stream) {
+    dk::PtrDeviceGuard dg_(mean);  // launch on the buffers' device
     if (!batch_mean || !batch_var || !mean || !var)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer merge: missing argument");
     if (dim <= 0) return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer dim mismatch");
@@ -156,6 +165,7 @@ int dk_norm_merge(int dim, double count, double batch_count, const double *batch
 int dk_norm_apply(int dtype, int64_t rows, int dim, const void *batch, double count,
                   const double *mean, const double *var, double epsilon, int invert, void *out,
                   void *stream) {
+    dk::PtrDeviceGuard dg_(batch);  // launch on the buffers' device
     if (!batch || !mean || !var || !out)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "normalizer_apply: missing argument");
     if (dim <= 0 || rows < 0)

@@ -6,7 +6,19 @@
 
 namespace dk {
 
-constexpr int kSms = 148;  // B200
+// SM count of the current device (148 on B200), queried once per device
+inline int sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
 #ifdef DK_NO_PDL
 constexpr bool kUsePdl = false;
 #else
@@ -21,7 +33,8 @@ inline int pick_block(int64_t n) {
     // Few worlds per GPU (1K-8K) is a latency-bound regime: spread warps over
     // all 148 SMs before stacking them on one SM.
     int bs = 256;
-    while (bs > 32 && (n + bs - 1) / bs < 2 * kSms) bs /= 2;
+    const int sms = sm_count();
+    while (bs > 32 && (n + bs - 1) / bs < 2 * sms) bs /= 2;
     return bs;
 }
 

@@ -164,9 +164,13 @@ def pixel_normalize(x, channels_first: bool = True, out_dtype=None):
     policy's input, float32 [n, c, h, w] (ppo.py:281-283); channels_first=False
     and out_dtype=torch.float64 give NumPy's own result."""
     torch = _torch()
-    x = x.contiguous()
     if x.dim() != 4:
         raise InvalidInputError("pixel_normalize expects [n, h, w, c]")
+    if x.dtype not in (torch.float32, torch.float64):
+        # the reference accepts any array (uint8 frames, halves): NumPy's mean /
+        # std promote to float64; float32 holds every uint8 / half value exactly
+        x = x.to(torch.float64 if x.dtype in (torch.int32, torch.int64) else torch.float32)
+    x = x.contiguous()
     n, h, w, c = x.shape
     od = out_dtype or torch.float32
     out = torch.empty((n, c, h, w) if channels_first else (n, h, w, c), dtype=od,

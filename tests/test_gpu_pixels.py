@@ -253,3 +253,20 @@ def test_pixel_normalize_float32_stacks_vs_oracle(PX, shape, levels):
     pol = PX.pixel_normalize(t)
     np.testing.assert_array_equal(pol.cpu().numpy(),
                                   np.ascontiguousarray(np.moveaxis(want, -1, 1)).astype(np.float32))
+
+
+@pytest.mark.parametrize("dtype,shape", [(np.uint8, (3, 64, 64, 3)), (np.float16, (2, 16, 20, 3)),
+                                         (np.float32, (2, 600, 700, 3))])
+def test_pixel_normalize_any_dtype_and_size(PX, dtype, shape):
+    """ppo.pixel_normalize accepts any [n, h, w, c] array (ppo.py:232-238):
+    uint8 frames and halves (converted exactly) and images larger than the
+    renderer's 512-px viewport; bit-exact against the oracle on the same values."""
+    from oracle import ppo as orc
+
+    rng = np.random.default_rng(7)
+    x = (rng.integers(0, 256, shape) if dtype == np.uint8 else rng.uniform(0, 1, shape))
+    x = x.astype(dtype)
+    want = orc.pixel_normalize(x.astype(np.float32))
+    y = PX.pixel_normalize(torch.as_tensor(x, device="cuda"), channels_first=False,
+                           out_dtype=torch.float64)
+    np.testing.assert_array_equal(y.cpu().numpy(), want)
