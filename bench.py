@@ -971,10 +971,12 @@ def bench_pixels(args, dev, steps=50):
 
 def bench_ppo_rollout(args, dev, T=30, reps=5):
     """ppo.collect_rollout on the device (RolloutGraph: the
-    reference's default MLPPolicy 4x128 / MLPValue 5x256 in float32 on cuBLAS,
-    sampling, env step, truncation bootstrap, normalisers) + compute_gae, per
-    phase of T control steps over the bench's worlds.  Reference measured in
-    the build container: 9.7e3 env-steps/s (N=1024, 16 torch threads)."""
+    reference's default MLPPolicy 4x128 / MLPValue 5x256, sampling, env step,
+    truncation bootstrap, normalisers) + compute_gae, per phase of T control
+    steps over the bench's worlds; MLPs on the tensor cores (mlp_tc_kernel,
+    tcgen05 BF16x3) and, for comparison, as torch nn.Linear (cuBLAS float32).
+    Reference measured in the build container: 9.7e3 env-steps/s (N=1024, 16
+    torch threads)."""
     import torch
 
     import paper_2502_08844_b200 as dk
@@ -986,30 +988,35 @@ def bench_ppo_rollout(args, dev, T=30, reps=5):
         policy_obs_key = value_obs_key = "state"
 
     n = args.num_envs
-    torch.manual_seed(0)
-    env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.analytic_task), n, dtype="float32")
-    obs = env.reset(seed=0)
-    od, ad = env.obs_dim, env.action_dim
-    policy, value = R.make_policy(od, ad).cuda(dev), R.make_value(od).cuda(dev)
-    pn, vn = P.DeviceRunningNormalizer(od), P.DeviceRunningNormalizer(od)
-    rg = R.RolloutGraph(env, policy, value, Cfg, obs, pn, vn)
-    for _ in range(2):
-        rg.run()
-    torch.cuda.synchronize(dev)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(reps):
-        batch, _, _ = rg.run()
-        P.compute_gae_batch(batch.rewards, batch.values, batch.bootstrap, batch.dones,
-                            0.995, 0.95)
-    e1.record()
-    torch.cuda.synchronize(dev)
-    env.check()
-    ms = e0.elapsed_time(e1) / reps
-    env.close()
+    res = {}
+    for tc in (True, False):
+        torch.manual_seed(0)
+        env = dk.DeviceBatchEnv(dk.EnvConfig(task=args.analytic_task), n, dtype="float32")
+        obs = env.reset(seed=0)
+        od, ad = env.obs_dim, env.action_dim
+        policy, value = R.make_policy(od, ad).cuda(dev), R.make_value(od).cuda(dev)
+        pn, vn = P.DeviceRunningNormalizer(od), P.DeviceRunningNormalizer(od)
+        rg = R.RolloutGraph(env, policy, value, Cfg, obs, pn, vn, tensor_cores=tc)
+        for _ in range(2):
+            rg.run()
+        torch.cuda.synchronize(dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            batch, _, _ = rg.run()
+            P.compute_gae_batch(batch.rewards, batch.values, batch.bootstrap, batch.dones,
+                                0.995, 0.95)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        env.check()
+        ms = e0.elapsed_time(e1) / reps
+        env.close()
+        res["tensor_cores" if tc else "cublas_fp32"] = {"value": T * n / (ms / 1e3),
+                                                        "ms_per_phase": ms}
     return {"metric": "env-steps/s of on-device PPO rollout collection incl. policy + value "
-                      "inference (float32, CUDA graph)", "value": T * n / (ms / 1e3),
-            "unit": "env_steps/s", "ms_per_phase": ms, "unroll_length": T, "worlds": n,
+                      "inference (CUDA graph)", "value": res["tensor_cores"]["value"],
+            "unit": "env_steps/s", "ms_per_phase": res["tensor_cores"]["ms_per_phase"],
+            "cublas_fp32": res["cublas_fp32"], "unroll_length": T, "worlds": n,
             "reference_cpu": {"value": 9.7e3, "unit": "env_steps/s",
                               "sample": "ppo.collect_rollout, N=1024, T=30, 16 torch threads, "
                                         "build container (not the GPU box)"}}

@@ -515,6 +515,30 @@ int dk_go1_get_state(dk_go1_env *env, void *qpos, void *qvel, void *command, voi
 int dk_go1_check(dk_go1_env *env, int64_t *step_index, int64_t *env_index);
 int64_t dk_go1_kernel_launches(const dk_go1_env *env);
 
+/* ------------------------------------------------------------------------
+ * PPO networks on the tensor cores (ppo.py:109-141
+ * _mlp / MLPPolicy / MLPValue): y = W_out silu(... silu(W_0 x + b_0) ...) + b_out.
+ * Layer 0 (d_in <= 16) and the output layer (n_out <= 4) run in float32 on the
+ * CUDA cores; the n_tc hidden x hidden layers (hidden 128 or 256) on tcgen05
+ * tensor cores with a BF16x3 split and float32 accumulation.  Weights are
+ * float32 torch Linear layouts [out, in]; hidden weights pre-packed by
+ * dk_mlp_pack (bf16 hi / lo, hidden*hidden elements each per layer).
+ * ------------------------------------------------------------------------ */
+typedef struct dk_mlp {
+    int32_t d_in, hidden, n_tc, n_out;
+    const float *w0, *b0;        /* [hidden, d_in], [hidden] */
+    const void *w_hi, *w_lo;     /* packed [n_tc][hidden * hidden] bf16 */
+    const float *b_hidden;       /* [n_tc][hidden] */
+    const float *w_out, *b_out;  /* [n_out, hidden], [n_out] */
+} dk_mlp;
+
+int dk_mlp_pack(const float *w, int n, int k, void *w_hi, void *w_lo, void *stream);
+int dk_mlp_forward(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride, float *y,
+                   int64_t y_stride, void *stream);
+/* developer hook: desc_swap = 1 swaps the descriptors' LBO / SBO (layout check) */
+int dk_mlp_forward_dbg(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride,
+                       float *y, int64_t y_stride, int desc_swap, void *stream);
+
 /* Benchmark/timing helper (no reference counterpart): enqueue on `stream` a
  * one-thread kernel that waits until *host_flag (pinned host memory) becomes
  * non-zero, or max_spins polls have elapsed (0 = no limit).  Lets a caller

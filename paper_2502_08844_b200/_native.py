@@ -105,6 +105,9 @@ _SIGS = {
     "dk_go1_get_state": (ctypes.c_int, [_vp] + [_vp] * 9 + [_vp]),
     "dk_go1_check": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "dk_go1_kernel_launches": (ctypes.c_int64, [_vp]),
+    "dk_mlp_pack": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
+    "dk_mlp_forward": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp]),
+    "dk_mlp_forward_dbg": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, ctypes.c_int, _vp]),
     "dk_last_error": (ctypes.c_char_p, []),
     "dk_task_id": (ctypes.c_int, [ctypes.c_char_p]),
     "dk_task_dims": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),

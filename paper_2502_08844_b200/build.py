@@ -44,6 +44,7 @@ UNITS = {
     "go1env_f32.cu": [],
     "go1env_f64.cu": ["--fmad=false"],
     "capi_go1.cu": [],
+    "capi_mlp.cu": [],
 }
 
 

@@ -1,0 +1,355 @@
+// mlp_tc.cuh -- fused MLP forward on the 5th-generation tensor cores (tcgen05),
+// for the PPO rollout's policy / value networks (
+// reference ppo.py:109-141 _mlp / MLPPolicy / MLPValue: Linear + Swish layers).
+//
+// y = W_out . silu(... silu(W_1 . silu(W_0 x + b_0) + b_1) ...) + b_out for a
+// batch of rows, one CTA per 128-row tile (M = 128), 16 warps: warp w serves
+// TMEM lanes / rows 32 (w % 4) .. 32 (w % 4) + 31 and the column quarter w / 4:
+//   * layer 0 (d_in -> H, d_in small) on the CUDA cores in float32;
+//   * the H x H hidden layers on tcgen05.mma kind::f16 with float32 accumulators in
+//     TMEM, operands split BF16x3: x = x_hi + x_lo (bf16 each), x.w ~ x_hi w_hi +
+//     x_hi w_lo + x_lo w_hi -- ~16 significant bits per product, float32 sums;
+//   * the output layer (H -> n_out, n_out small) on the CUDA cores in float32
+//     straight from the last hidden layer's float32 activations.
+// Activations stay in shared memory between layers (K-major canonical layout,
+// SWIZZLE_NONE: 8-row x 16-byte core matrices, LBO = core-matrix stride along K,
+// SBO = along M); weights are pre-split and pre-packed in the same layout in HBM
+// (pack_weights_kernel) and streamed per 32-column K chunk by 1-D bulk copies
+// (cp.async.bulk, the TMA engine) into a two-stage ring; one thread issues the
+// MMAs and commits them to mbarriers; in the epilogue each warp reads its 32
+// TMEM lanes x its column quarter (tcgen05.ld 32x32b): bias, SiLU, split, store;
+// the output layer's four partial sums per row are added in quarter order.
+#pragma once
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+namespace dk {
+namespace mlp {
+
+constexpr int M = 128;          // rows per CTA (= TMEM lanes)
+constexpr int THREADS = 512;    // 16 warps: warp w -> TMEM lanes 32 (w % 4), column quarter w / 4
+constexpr int KC = 32;          // K columns per chunk
+constexpr int MAXH = 256;
+
+struct MlpArgs {
+    const float *x;        // [rows][x_stride], first d_in columns used
+    int64_t rows, x_stride;
+    int d_in, H, n_tc, n_out;
+    const float *w0, *b0;             // [H][d_in], [H]
+    const __nv_bfloat16 *whi, *wlo;   // packed hidden weights [n_tc][H*H]
+    const float *bh;                  // [n_tc][H]
+    const float *wout, *bout;         // [n_out][H], [n_out]
+    float *y;                         // [rows][y_stride]
+    int64_t y_stride;
+    int desc_swap;                    // debug: swap LBO / SBO
+};
+
+// ------------------------------------------------------------------ PTX glue
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// UMMA shared-memory descriptor (cute::UMMA::SmemDescriptor): start >> 4 at
+// [0,14), LBO >> 4 at [16,30), SBO >> 4 at [32,46), version 1 at [46,48),
+// base offset 0, layout type 0 = SWIZZLE_NONE at [61,64)
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((addr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+
+// UMMA instruction descriptor (cute::UMMA::InstrDescriptor): D f32 (bits 4-5 = 1),
+// A bf16 (bits 7-9 = 1), B bf16 (bits 10-12 = 1), both K-major, N >> 3 at
+// [17,23), M >> 4 at [24,29)
+__host__ __device__ constexpr uint32_t instr_desc_bf16(int m, int n) {
+    return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) |
+           ((uint32_t)(m >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *mbar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(mbar))
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(mbar)), "r"(count)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *mbar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(mbar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *mbar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(smem_u32(mbar)),
+        "r"(parity)
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *mbar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, "
+        "[%3];\n" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(mbar))
+        : "memory");
+}
+
+__device__ __forceinline__ void fence_async_smem() {
+    asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+// 32 consecutive f32 columns of this thread's TMEM lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
+    uint32_t r[32];
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, "
+        "[%32];\n"
+        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+          "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]),
+          "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+          "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]),
+          "=r"(r[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+
+// element (row r, column k) of a K-major canonical operand made of 32-column
+// chunks: chunk k / 32 at chunk_bytes * (k / 32); inside a chunk, core matrix
+// (r / 8, (k % 32) / 8) at (r / 8) * 512 + ((k % 32) / 8) * 128; inside it, row
+// r % 8 at 16 * (r % 8), element k % 8 at 2 * (k % 8)
+__host__ __device__ __forceinline__ uint32_t op_offset(int r, int k, int rows_total) {
+    const uint32_t chunk_bytes = (uint32_t)rows_total * KC * 2;
+    return (uint32_t)(k / KC) * chunk_bytes + (uint32_t)(r / 8) * 512 + (uint32_t)((k % KC) / 8) * 128 +
+           (uint32_t)(r % 8) * 16 + (uint32_t)(k % 8) * 2;
+}
+
+// store 8 consecutive float activations (row r, columns k..k+7) split into bf16 hi / lo
+__device__ __forceinline__ void store_split8(unsigned char *ahi, unsigned char *alo, int r, int k,
+                                             const float *v) {
+    __align__(16) __nv_bfloat16 hi[8], lo[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        hi[i] = __float2bfloat16_rn(v[i]);
+        lo[i] = __float2bfloat16_rn(v[i] - __bfloat162float(hi[i]));
+    }
+    const uint32_t off = op_offset(r, k, M);
+    *reinterpret_cast<uint4 *>(ahi + off) = *reinterpret_cast<const uint4 *>(hi);
+    *reinterpret_cast<uint4 *>(alo + off) = *reinterpret_cast<const uint4 *>(lo);
+}
+
+// fp32 W [N][K] (torch Linear weight: out x in, K contiguous) -> packed bf16 hi / lo
+__global__ void pack_weights_kernel(const float *w, int N, int K, __nv_bfloat16 *hi,
+                                    __nv_bfloat16 *lo) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N * K) return;
+    const int n = i / K, k = i % K;
+    const float v = w[i];
+    const __nv_bfloat16 h = __float2bfloat16_rn(v);
+    const __nv_bfloat16 l = __float2bfloat16_rn(v - __bfloat162float(h));
+    const uint32_t e = op_offset(n, k, N) / 2;
+    hi[e] = h;
+    lo[e] = l;
+}
+
+__global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int H = a.H, din = a.d_in, nout = a.n_out;
+    const uint32_t a_bytes = (uint32_t)M * H * 2;           // one of A_hi / A_lo
+    const uint32_t b_chunk = (uint32_t)H * KC * 2;          // one B chunk (hi or lo)
+    unsigned char *A_hi = smem;
+    unsigned char *A_lo = smem + a_bytes;
+    unsigned char *Bst = smem + 2 * a_bytes;                // [2 stages][hi, lo][b_chunk]
+    uint64_t *bars = reinterpret_cast<uint64_t *>(Bst + 4 * b_chunk);  // full[2], empty[2], done
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5);
+    // the float32 parameters used on the CUDA cores, staged once
+    float *s_w0 = reinterpret_cast<float *>(bars + 6);      // [H][din]
+    float *s_b0 = s_w0 + H * din;                            // [H]
+    float *s_bh = s_b0 + H;                                  // [n_tc][H]
+    float *s_wo = s_bh + a.n_tc * H;                         // [nout][H]
+    float *s_red = s_wo + nout * H;                          // [4 quarters][M][4] partial outputs
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int q = warp & 3, quarter = warp >> 2;            // TMEM lane group, column quarter
+    const int row = 32 * q + lane;
+    const int64_t r_glob = (int64_t)blockIdx.x * M + row;
+    const int HQ = H / 4;                                    // columns per thread (32 or 64)
+
+    for (int i = tid; i < H * din; i += THREADS) s_w0[i] = a.w0[i];
+    for (int i = tid; i < H; i += THREADS) s_b0[i] = a.b0[i];
+    for (int i = tid; i < a.n_tc * H; i += THREADS) s_bh[i] = a.bh[i];
+    for (int i = tid; i < nout * H; i += THREADS) s_wo[i] = a.wout[i];
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(256));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+    }
+    if (tid == 0) {
+        for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    // ---- layer 0 on the CUDA cores (float32): this thread's row, its column quarter
+    {
+        float x[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            x[i] = (i < din && r_glob < a.rows) ? a.x[r_glob * a.x_stride + i] : 0.0f;
+        for (int j0 = quarter * HQ; j0 < (quarter + 1) * HQ; j0 += 8) {
+            float v[8];
+#pragma unroll
+            for (int jj = 0; jj < 8; ++jj) {
+                const int j = j0 + jj;
+                float s = s_b0[j];
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (i < din) s = fmaf(s_w0[j * din + i], x[i], s);
+                v[jj] = r_glob < a.rows ? silu(s) : 0.0f;
+            }
+            store_split8(A_hi, A_lo, row, j0, v);
+        }
+    }
+    fence_async_smem();
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+
+    const uint32_t idesc = instr_desc_bf16(M, H);
+    const int nch = H / KC;
+    const uint32_t lbo = a.desc_swap ? 512u : 128u, sbo = a.desc_swap ? 128u : 512u;
+    float out_acc[4] = {0.f, 0.f, 0.f, 0.f};
+    uint32_t g = 0;  // global chunk counter (stage = g & 1) across layers
+
+    for (int l = 0; l < a.n_tc; ++l) {
+        const __nv_bfloat16 *whi = a.whi + (size_t)l * H * H, *wlo = a.wlo + (size_t)l * H * H;
+        if (tid == 0) {
+            auto load = [&](uint32_t gg, int c) {
+                const int s = gg & 1;
+                if (gg >= 2) mbar_wait(&bars[2 + s], ((gg - 2) >> 1) & 1);  // stage free
+                mbar_expect_tx(&bars[s], 2 * b_chunk);
+                bulk_g2s(Bst + (2 * s) * b_chunk, whi + (size_t)c * H * KC, b_chunk, &bars[s]);
+                bulk_g2s(Bst + (2 * s + 1) * b_chunk, wlo + (size_t)c * H * KC, b_chunk, &bars[s]);
+            };
+            const uint32_t g0 = g;
+            load(g0, 0);
+            for (int c = 0; c < nch; ++c) {
+                const uint32_t gc = g0 + c;
+                const int s = gc & 1;
+                if (c + 1 < nch) load(gc + 1, c + 1);
+                mbar_wait(&bars[s], (gc >> 1) & 1);  // chunk landed
+                tc_fence_after();
+                const uint32_t a_hi = smem_u32(A_hi) + c * (M * KC * 2);
+                const uint32_t a_lo = smem_u32(A_lo) + c * (M * KC * 2);
+                const uint32_t b_hi = smem_u32(Bst + (2 * s) * b_chunk);
+                const uint32_t b_lo = smem_u32(Bst + (2 * s + 1) * b_chunk);
+#pragma unroll
+                for (int ks = 0; ks < KC / 16; ++ks) {
+                    const uint32_t o = ks * 256;  // two core matrices along K
+                    const uint64_t dah = smem_desc(a_hi + o, lbo, sbo);
+                    const uint64_t dal = smem_desc(a_lo + o, lbo, sbo);
+                    const uint64_t dbh = smem_desc(b_hi + o, lbo, sbo);
+                    const uint64_t dbl = smem_desc(b_lo + o, lbo, sbo);
+                    mma_bf16(tmem, dah, dbh, idesc, (c | ks) != 0);
+                    mma_bf16(tmem, dah, dbl, idesc, 1);
+                    mma_bf16(tmem, dal, dbh, idesc, 1);
+                }
+                mma_commit(&bars[2 + s]);  // stage s free once these MMAs complete
+            }
+            mma_commit(&bars[4]);  // the layer's accumulator is final
+        }
+        g += nch;
+        __syncwarp();
+        mbar_wait(&bars[4], l & 1);
+        tc_fence_after();
+        // ---- epilogue (this thread's row and column quarter): bias, SiLU; split
+        // into A for the next layer, or partial output-layer dot products
+        const bool last = l + 1 == a.n_tc;
+        const float *bias = s_bh + (size_t)l * H;
+        for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
+            float v[32];
+            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = silu(v[i] + bias[cc * 32 + i]);
+            if (last) {
+#pragma unroll
+                for (int o = 0; o < 4; ++o) {
+                    if (o < nout) {
+                        const float *wr = s_wo + (size_t)o * H + cc * 32;
+                        float s = out_acc[o];
+#pragma unroll
+                        for (int i = 0; i < 32; ++i) s = fmaf(wr[i], v[i], s);
+                        out_acc[o] = s;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int k8 = 0; k8 < 4; ++k8) store_split8(A_hi, A_lo, row, cc * 32 + k8 * 8, v + 8 * k8);
+            }
+        }
+        fence_async_smem();
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+    }
+    // output layer: the four column quarters' partial sums, in quarter order
+#pragma unroll
+    for (int o = 0; o < 4; ++o) s_red[(quarter * M + row) * 4 + o] = out_acc[o];
+    __syncthreads();
+    if (quarter == 0 && r_glob < a.rows)
+        for (int o = 0; o < nout && o < 4; ++o) {
+            const float s = ((s_red[(0 * M + row) * 4 + o] + s_red[(1 * M + row) * 4 + o]) +
+                             (s_red[(2 * M + row) * 4 + o] + s_red[(3 * M + row) * 4 + o]));
+            a.y[r_glob * a.y_stride + o] = s + a.bout[o];
+        }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+}
+
+inline size_t mlp_smem_bytes(int H, int d_in, int n_tc, int n_out) {
+    return 2 * (size_t)M * H * 2 + 4 * (size_t)H * KC * 2 + 6 * 8 +
+           4 * ((size_t)H * d_in + H + (size_t)n_tc * H + (size_t)n_out * H + 4 * M * 4);
+}
+
+}  // namespace mlp
+}  // namespace dk

@@ -163,7 +163,7 @@ def _route(obs: dict, cfg):
 
 def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer=None,
                            value_normalizer=None, noise=None, generator=None,
-                           update_normalizers: bool = True):
+                           update_normalizers: bool = True, tensor_cores: bool = True):
     """Unroll ``cfg.unroll_length`` control steps across the batch on the GPU.
 
     env: DeviceBatchEnv; policy / value: CUDA ``nn.Module``s with the
@@ -174,6 +174,10 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
     import torch
 
     T, N = int(cfg.unroll_length), env.num_envs
+    if tensor_cores:  # the reference-shaped MLPs on tcgen05 (mlp.py); others unchanged
+        from .mlp import tc_policy, tc_value
+
+        policy, value = tc_policy(policy), tc_value(value)
     if noise is not None and tuple(noise.shape[:2]) != (T, N):
         raise ConfigError("noise must be [unroll_length, num_envs, action_dim]")
     # ppo.policy_forward's NaN check (ppo.py:208), as a device flag read once
@@ -212,7 +216,6 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             pre_tanh = mean + torch.exp(log_std) * eps
             action = torch.tanh(pre_tanh)
             log_prob = tanh_gaussian_log_prob(mean, log_std, pre_tanh)
-            v = value(val_t)
             step = env.step(action.to(env.dtype), autoreset=True, with_info=False, out=out)
             reward = step["reward"].to(torch.float64)
             raw_reward_sum += reward.mean()
@@ -221,7 +224,10 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             boot = step["trunc"] & ~step["done"] & step["terminal_mask"]
             term_in = torch.where(boot[:, None], step["terminal_obs"],
                                   torch.zeros((), dtype=env.dtype, device=env.device))
-            tv = value(prep(value_normalizer, term_in)).to(torch.float64)
+            # the value of the observation and of the terminal observation in one
+            # network call (rows are independent): 2N rows fill twice the SMs
+            vv = value(torch.cat([val_t, prep(value_normalizer, term_in)]))
+            v, tv = vv[:N], vv[N:].to(torch.float64)
             term_val = torch.where(boot, tv, torch.zeros_like(tv))
             p_obs.append(pol_t)
             v_obs.append(val_t)
@@ -325,16 +331,21 @@ class RolloutGraph:
     generator (graph-safe Philox offsets)."""
 
     def __init__(self, env, policy, value, cfg, obs: dict, policy_normalizer=None,
-                 value_normalizer=None):
+                 value_normalizer=None, tensor_cores: bool = True):
         import torch
 
+        if tensor_cores:
+            from .mlp import tc_policy, tc_value
+
+            policy, value = tc_policy(policy), tc_value(value)
         if cfg.policy_obs_key == "pixels":
             raise ConfigError("RolloutGraph: pixel policies run eagerly (collect_rollout_device)")
         self.env, self.policy, self.value, self.cfg = env, policy, value, cfg
         self.pn, self.vn = policy_normalizer, value_normalizer
         # one eager phase: warms up cuBLAS / allocator and fills the statistics
         batch, obs, self.mean_reward = collect_rollout_device(
-            env, policy, value, cfg, obs, policy_normalizer, value_normalizer)
+            env, policy, value, cfg, obs, policy_normalizer, value_normalizer,
+            tensor_cores=False)  # (already wrapped above when requested)
         self.obs_in = obs["state"].clone()
         self.last = batch
         # the capture warm-up really steps the env: snapshot the worlds (state,
@@ -349,7 +360,7 @@ class RolloutGraph:
             collect_rollout_device(env, policy, value, cfg,
                                    {"state": self.obs_in, "privileged_state": self.obs_in},
                                    policy_normalizer, value_normalizer,
-                                   update_normalizers=False)
+                                   update_normalizers=False, tensor_cores=False)
         torch.cuda.current_stream(env.device).wait_stream(side)
         torch.cuda.synchronize(env.device)
         env.set_state(state=snap[0], target=snap[1], steps=snap[2], episode=snap[3],
@@ -359,7 +370,8 @@ class RolloutGraph:
         with torch.cuda.graph(self.graph):
             self.batch, self.obs_out, self.reward_out = collect_rollout_device(
                 env, policy, value, cfg, {"state": self.obs_in, "privileged_state": self.obs_in},
-                policy_normalizer, value_normalizer, update_normalizers=False)
+                policy_normalizer, value_normalizer, update_normalizers=False,
+                tensor_cores=False)
 
     def run(self, obs: dict | None = None):
         """One phase from ``obs`` (default: where the previous phase stopped).

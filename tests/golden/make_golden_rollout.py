@@ -3,6 +3,7 @@ produced by the reference itself on CPU.
 
     python tests/golden/make_golden_rollout.py     (needs /root/reference; CPU)
 
+rollout_golden_default.npz: the same with the default network sizes.
 A 64-world cartpole BatchEnv with episode_length 5 (truncation bootstraps inside
 the 8-step unroll), the reference's MLPPolicy / MLPValue (small hidden sizes),
 observation normalisers, two collect_rollout phases.  Saves the network
@@ -19,7 +20,7 @@ REF = "/root/reference/pkg/src"
 OUT = os.path.dirname(os.path.abspath(__file__))
 
 
-def main():
+def main(policy_hidden=(32, 32), value_hidden=(48, 48), out_name="rollout_golden.npz"):
     sys.path.insert(0, REF)
     import torch
     from deskrl import envkit, ppo
@@ -28,8 +29,8 @@ def main():
     torch.manual_seed(5)
     N, T = 64, 8
     cfg = ppo.PPOConfig(num_envs=N, unroll_length=T, num_minibatches=4, batch_size=128,
-                        policy_hidden=(32, 32),
-                        value_hidden=(48, 48), reward_scaling=10.0, discounting=0.995)
+                        policy_hidden=policy_hidden,
+                        value_hidden=value_hidden, reward_scaling=10.0, discounting=0.995)
     env = envkit.BatchEnv(envkit.EnvConfig(task="cartpole-balance", episode_length=5), N)
     obs = env.reset(seed=3)
     policy = ppo.MLPPolicy(5, 1, cfg.policy_hidden)
@@ -60,10 +61,13 @@ def main():
             data[f"p{phase}/{name}_count"] = np.array(nz.count)
             data[f"p{phase}/{name}_mean"] = nz.mean
             data[f"p{phase}/{name}_var"] = nz.var
-    path = os.path.join(OUT, "rollout_golden.npz")
+    path = os.path.join(OUT, out_name)
     np.savez_compressed(path, **data)
     print(f"wrote {path} ({os.path.getsize(path)} bytes, {len(data)} arrays)")
 
 
 if __name__ == "__main__":
     main()
+    # the reference's default network sizes (PPOConfig: policy 4 x 128, value
+    # 5 x 256): the shapes the tensor-core MLP kernel serves
+    main((128, 128, 128, 128), (256, 256, 256, 256, 256), "rollout_golden_default.npz")

@@ -27,16 +27,27 @@ def _close(a, b, floor=1e-3):
     return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), floor)))
 
 
-def test_collect_rollout_matches_reference(gold):
+@pytest.mark.parametrize("which", ["small", "default"])
+def test_collect_rollout_matches_reference(gold, which):
+    """small: the reference's MLPs with hidden (32, 32) / (48, 48) (torch on the
+    GPU); default: its default sizes 4 x 128 / 5 x 256 (tests/golden/
+    rollout_golden_default.npz), served by the tensor-core MLP kernel."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import paper_2502_08844_b200 as dk
+    from paper_2502_08844_b200 import mlp as TC
     from paper_2502_08844_b200 import ppo as P
     from paper_2502_08844_b200 import rollout as R
+    from tests.conftest import GOLDEN
 
+    if which == "default":
+        gold = np.load(os.path.join(GOLDEN, "rollout_golden_default.npz"))
     N, T = 64, 8
-    policy = R.make_policy(5, 1, (32, 32)).cuda()
-    value = R.make_value(5, (48, 48)).cuda()
+    ph, vh = ((32, 32), (48, 48)) if which == "small" else ((128,) * 4, (256,) * 5)
+    policy = R.make_policy(5, 1, ph).cuda()
+    value = R.make_value(5, vh).cuda()
+    assert TC.supported(policy.trunk) == (which == "default")
+    assert TC.supported(value.trunk) == (which == "default")
     policy.load_state_dict({k[7:]: torch.as_tensor(gold[k]) for k in gold.files
                             if k.startswith("policy/")})
     value.load_state_dict({k[6:]: torch.as_tensor(gold[k]) for k in gold.files
