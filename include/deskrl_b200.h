@@ -285,6 +285,14 @@ int dk_dr_curriculum(int64_t n, int64_t *state, const uint8_t *success, int64_t 
  *
  * compute_gae (ppo.py:80-102): rewards / values / dones [T, N], bootstrap [N]
  * -> advantages, returns (= advantages + values) [T, N]. */
+/* ppo.policy_forward sampling (ppo.py:204-217) + tanh_gaussian_log_prob
+ * (ppo.py:185-192), fused, float32: pre_tanh = mean + exp(log_std) * eps,
+ * action = tanh(pre_tanh), log_prob [n] summed over the action dims;
+ * log_std rows of log_std_stride (0 = one shared row); *nan_flag |= 1 if a mean
+ * is NaN (the reference raises RuntimeError). */
+int dk_ppo_sample(int64_t n, int action_dim, const float *mean, const float *log_std,
+                  int64_t log_std_stride, const float *eps, float *pre_tanh, float *action,
+                  float *log_prob, int *nan_flag, void *stream);
 int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
                const void *values, const void *dones, const void *bootstrap, double gamma,
                double lam, void *advantages, void *returns, void *stream);

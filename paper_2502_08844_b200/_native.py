@@ -165,6 +165,8 @@ _SIGS = {
     "dk_pixels_normalize": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, _i64, ctypes.c_int,
                                            ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp,
                                            _vp, _vp]),
+    "dk_ppo_sample": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _i64, _vp, _vp, _vp, _vp,
+                                     _vp, _vp]),
     "dk_ppo_gae": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_double,
                                   ctypes.c_double, _vp, _vp, _vp]),
     "dk_norm_update": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,

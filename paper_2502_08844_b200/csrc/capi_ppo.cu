@@ -76,7 +76,53 @@ int norm_update(int64_t rows, int dim, const T *batch, double count, double *mea
 
 }  // namespace
 
+
+// tanh-Gaussian sampling + log-prob (ppo.policy_forward / tanh_gaussian_log_prob,
+// ppo.py:185-217) fused: one thread per row; float32 in torch's eager operation
+// order (this translation unit is built with --fmad=false, like the separate
+// elementwise kernels it replaces); the NaN-mean check as a sticky flag.
+__global__ void ppo_sample_kernel(int64_t n, int A, const float *mean, const float *log_std,
+                                  int64_t ls_stride, const float *eps, float *pre, float *act,
+                                  float *lp, int *nan_flag) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const float kHalfLog2Pi = 0.91893853320467274178f;  // 0.5 * log(2 pi) as float32
+    const float kLog2 = 0.69314718055994530942f;
+    float s = 0.0f;
+    bool bad = false;
+    for (int a = 0; a < A; ++a) {
+        const float m = mean[i * A + a], l = log_std[i * ls_stride + a];
+        bad |= isnan(m);
+        const float sd = expf(l);
+        const float u = m + sd * eps[i * A + a];
+        const float z = (u - m) / sd;
+        const float base = ((-0.5f * (z * z)) - l) - kHalfLog2Pi;
+        const float x = -2.0f * u;
+        const float sp = x > 20.0f ? x : log1pf(expf(x));
+        const float corr = 2.0f * ((kLog2 - u) - sp);
+        s = s + (base - corr);
+        pre[i * A + a] = u;
+        act[i * A + a] = tanhf(u);
+    }
+    lp[i] = s;
+    if (bad) atomicOr(nan_flag, 1);
+}
+
 extern "C" {
+
+int dk_ppo_sample(int64_t n, int action_dim, const float *mean, const float *log_std,
+                  int64_t log_std_stride, const float *eps, float *pre_tanh, float *action,
+                  float *log_prob, int *nan_flag, void *stream) {
+    dk::PtrDeviceGuard dg_(mean);
+    if (n < 0 || action_dim < 1 || !mean || !log_std || !eps || !pre_tanh || !action ||
+        !log_prob || !nan_flag)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_sample: bad arguments");
+    if (n == 0) return DK_OK;
+    ppo_sample_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        n, action_dim, mean, log_std, log_std_stride, eps, pre_tanh, action, log_prob, nan_flag);
+    cudaError_t e = cudaGetLastError();
+    return e == cudaSuccess ? DK_OK : dk_internal_fail(DK_ERR_CUDA, cudaGetErrorString(e));
+}
 
 int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
                const void *values, const void *dones, const void *bootstrap, double gamma,

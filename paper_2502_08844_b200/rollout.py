@@ -22,7 +22,7 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
-from .envkit import ConfigError
+from .envkit import ConfigError, _check
 
 
 @dataclass
@@ -154,6 +154,30 @@ def tanh_gaussian_log_prob(mean, log_std, pre_tanh):
     return (base - correction).sum(-1)
 
 
+def _sample(mean, log_std, eps, nan_flag):
+    """policy_forward's sampling + tanh_gaussian_log_prob (ppo.py:204-217): one
+    fused kernel (dk_ppo_sample) for float32 networks, else the torch
+    expressions; NaN means set nan_flag."""
+    import torch
+
+    if (mean.dtype == torch.float32 and eps.dtype == torch.float32 and mean.dim() == 2
+            and log_std.dtype == torch.float32 and log_std.stride(-1) == 1):
+        from . import _native as nat
+
+        m, e = mean.contiguous(), eps.contiguous()
+        n, A = m.shape
+        pre, act = torch.empty_like(m), torch.empty_like(m)
+        lp = torch.empty((n,), dtype=torch.float32, device=m.device)
+        _check(nat.lib().dk_ppo_sample(n, A, m.data_ptr(), log_std.data_ptr(), log_std.stride(0),
+                                       e.data_ptr(), pre.data_ptr(), act.data_ptr(),
+                                       lp.data_ptr(), nan_flag.data_ptr(),
+                                       torch.cuda.current_stream(m.device).cuda_stream))
+        return pre, act, lp
+    nan_flag |= torch.isnan(mean).any().to(nan_flag.dtype)
+    pre_tanh = mean + torch.exp(log_std) * eps
+    return pre_tanh, torch.tanh(pre_tanh), tanh_gaussian_log_prob(mean, log_std, pre_tanh)
+
+
 def _route(obs: dict, cfg):
     for key in (cfg.policy_obs_key, cfg.value_obs_key):
         if key not in obs:
@@ -182,7 +206,7 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
         raise ConfigError("noise must be [unroll_length, num_envs, action_dim]")
     # ppo.policy_forward's NaN check (ppo.py:208), as a device flag read once
     # per phase instead of one host sync per step
-    nan_flag = torch.zeros((), dtype=torch.bool, device=env.device)
+    nan_flag = torch.zeros((), dtype=torch.int32, device=env.device)
     out = env._outputs((), False)  # reused step buffers (stream-ordered)
     f32 = torch.float32
     p_obs, v_obs, acts, pres, lps, rews, dns, vals = [], [], [], [], [], [], [], []
@@ -210,12 +234,9 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             if value_normalizer is not None:
                 raw_v.append(val_in.clone())
             mean, log_std = policy(pol_t)
-            nan_flag |= torch.isnan(mean).any()
             eps = noise[t].to(mean.dtype) if noise is not None else torch.randn(
                 mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
-            pre_tanh = mean + torch.exp(log_std) * eps
-            action = torch.tanh(pre_tanh)
-            log_prob = tanh_gaussian_log_prob(mean, log_std, pre_tanh)
+            pre_tanh, action, log_prob = _sample(mean, log_std, eps, nan_flag)
             step = env.step(action.to(env.dtype), autoreset=True, with_info=False, out=out)
             reward = step["reward"].to(torch.float64)
             raw_reward_sum += reward.mean()
