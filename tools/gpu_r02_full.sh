@@ -12,6 +12,10 @@ timeout 600 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>
 timeout 2400 python -m pytest tests -m gpu -q > $O/pytest.log 2>&1; echo "pytest rc=$?" >> $O/rc.txt
 if [ "${NCU:-1}" = 1 ]; then
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench.csv python3 bench.py --gpus 1 --steps 20 --warmup 5 --no-extra --no-cpu --no-tail > $O/ncu_launches.log 2>&1; echo "ncu launches rc=$?" >> $O/rc.txt
-PROF_K=2 timeout 900 ncu --set full --clock-control none --import-source on -k regex:go1_env_kernel -s 1 -c 1 -o $O/go1_env python tools/prof_go1.py > $O/ncu_go1.log 2>&1; echo "ncu go1 rc=$?" >> $O/rc.txt
+PROF_K=20 timeout 900 ncu --set full --clock-control none --import-source on -k regex:go1_env_kernel -s 1 -c 1 -o $O/go1_env python tools/prof_go1.py > $O/ncu_go1.log 2>&1; echo "ncu go1 rc=$?" >> $O/rc.txt
 PROF_K=2 timeout 900 ncu --set full --clock-control none --import-source on -k regex:phys_kernel -s 1 -c 1 -o $O/phys python tools/prof_go1.py > $O/ncu_phys.log 2>&1; echo "ncu phys rc=$?" >> $O/rc.txt
+fi
+if [ "${NCU:-1}" = 1 ]; then
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:mlp_tc_kernel -s 2 -c 1 -o $O/mlp python tools/mlp_speed.py > $O/ncu_mlp.log 2>&1; echo "ncu mlp rc=$?" >> $O/rc.txt
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_ppo.csv python tools/prof_ppo.py > $O/ncu_ppo.log 2>&1; echo "ncu ppo rc=$?" >> $O/rc.txt
 fi
