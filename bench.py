@@ -460,8 +460,8 @@ GO1_STATE_BYTES = 2 * (4 * (19 + 18 + 3 + 4 + 4 + 12) + 4 + 8)
 def go1_config_obj(args, world, U):
     return {
         "workload": "Go1 joystick env step, one fused kernel (go1env.cuh): 5 physics steps "
-                    "(CRB, contacts, Newton) + reward + obs + autoreset; Go1-shaped model, "
-                    "18 DoF, h=4ms; no reference impl (SPEC.md:8)",
+                    "(CRB, contacts, Newton) + reward + obs + autoreset with per-world DR; "
+                    "Go1-shaped model, 18 DoF, h=4ms; no reference impl (SPEC.md:8)",
         "task": GO1, "worlds_per_gpu": args.num_envs, "global_worlds": args.num_envs * world,
         "physics_steps_per_env_step": GO1_SUBSTEPS, "env_steps_per_launch": U,
         "parallelism": f"worlds sharded dp{world}",

@@ -494,6 +494,11 @@ typedef struct dk_go1_config {
     double obs_noise[5];         /* ObservationNoise: gravity, lin_vel, ang_vel, joint_pos, joint_vel */
     uint64_t seed;
     dk_reward_config reward;
+    /* domain randomisation drawn per world at every reset (randomization.py:156-181
+     * additive / multiplicative kinds): foot friction U(lo, hi), trunk payload
+     * U(lo, hi) kg added to the trunk mass, PD stiffness scale U(lo, hi) x kp;
+     * lo == hi fixes the value */
+    double dr_friction[2], dr_payload[2], dr_kp_scale[2];
 } dk_go1_config;
 
 typedef struct dk_go1_env dk_go1_env;
@@ -521,6 +526,8 @@ int dk_go1_get_state(dk_go1_env *env, void *qpos, void *qvel, void *command, voi
 /* synchronising error check: non-finite actions (DK_ERR_INVALID_INPUT, with
  * the first step / world), non-positive-definite physics matrices */
 int dk_go1_check(dk_go1_env *env, int64_t *step_index, int64_t *env_index);
+/* the worlds' current physical parameters [N, 3]: friction, trunk mass, kp */
+int dk_go1_get_params(dk_go1_env *env, void *params, void *stream);
 int64_t dk_go1_kernel_launches(const dk_go1_env *env);
 
 /* ------------------------------------------------------------------------

@@ -34,7 +34,8 @@ def default_config():
     return dict(episode_length=1000, ctrl_dt=0.02, action_scale=0.5, gait_freq=1.5,
                 term_height=0.12, cmd_lo=(-1.5, -0.8, -1.2), cmd_hi=(1.5, 0.8, 1.2),
                 joint_noise=0.1, yaw_range=math.pi, obs_noise=(0.05, 0.1, 0.2, 0.01, 1.5),
-                seed=0, reward={})
+                seed=0, reward={}, dr_friction=(0.4, 1.0), dr_payload=(-0.5, 1.5),
+                dr_kp_scale=(0.9, 1.1))
 
 
 def _uniform(words, lo, hi):
@@ -57,16 +58,22 @@ class OracleGo1Env:
         self.cmd, self.phase, self.air = np.zeros((n, 3)), np.zeros((n, 4)), np.zeros((n, 4))
         self.last_contact = np.zeros((n, 4), bool)
         self.prev = np.zeros((n, 12))
+        self.params = np.zeros((n, 3))  # friction, trunk mass, kp (this episode's draw)
         self.steps = np.zeros(n, np.int64)
         self.episode = np.zeros(n, np.int64)
 
     # -- pieces
     def _reset_world(self, i):
         c = self.cfg
-        w = orc.stream_raw(c["seed"], self.env0 + i, int(self.episode[i]), 0, 16)
+        w = orc.stream_raw(c["seed"], self.env0 + i, int(self.episode[i]), 0, 19)
         yaw = _uniform(w[0:1], -c["yaw_range"], c["yaw_range"])[0]
         jn = _uniform(w[1:13], -c["joint_noise"], c["joint_noise"])
         cmd = [_uniform(w[13 + k:14 + k], c["cmd_lo"][k], c["cmd_hi"][k])[0] for k in range(3)]
+        # randomize_params kinds (randomization.py:156-181): friction replaced,
+        # payload added to the trunk mass, kp scaled
+        dr = [_uniform(w[16 + k:17 + k], *c[f])[0]
+              for k, f in enumerate(("dr_friction", "dr_payload", "dr_kp_scale"))]
+        self.params[i] = (dr[0], self.model.base_mass + dr[1], self.model.kp * dr[2])
         q = np.zeros(19)
         q[2] = HOME_HEIGHT
         q[3], q[6] = math.cos(0.5 * yaw), math.sin(0.5 * yaw)
@@ -136,8 +143,14 @@ class OracleGo1Env:
                "terminal_obs": np.zeros((n, 56)), "terminal_mask": np.zeros(n, bool)}
         a = np.clip(np.nan_to_num(np.asarray(actions, np.float64), nan=0.0), -1.0, 1.0)
         ctrl = HOME + c["action_scale"] * a
-        ph = op.step(self.mc, self.qpos, self.qvel, ctrl, self.substeps)
-        self.qpos, self.qvel = ph["qpos"], ph["qvel"]
+        # physics per world with the world's own randomised model
+        ph = {"act_force": np.zeros((n, 12))}
+        for i in range(n):
+            m = self.model.to_c()
+            m.friction, m.base_mass, m.kp = self.params[i]
+            r = op.step(m, self.qpos[i:i + 1], self.qvel[i:i + 1], ctrl[i:i + 1], self.substeps)
+            self.qpos[i], self.qvel[i] = r["qpos"][0], r["qvel"][0]
+            ph["act_force"][i] = r["act_force"][0]
         for i in range(n):
             fr, contact, R = self._frame(i, a[i], ph["act_force"][i], False)
             done = bool(R[2, 2] < 0 or self.qpos[i, 2] < c["term_height"])

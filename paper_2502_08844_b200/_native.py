@@ -105,6 +105,7 @@ _SIGS = {
     "dk_go1_get_state": (ctypes.c_int, [_vp] + [_vp] * 9 + [_vp]),
     "dk_go1_check": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "dk_go1_kernel_launches": (ctypes.c_int64, [_vp]),
+    "dk_go1_get_params": (ctypes.c_int, [_vp, _vp, _vp]),
     "dk_mlp_pack": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "dk_mlp_forward": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "dk_mlp_forward_dbg": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, ctypes.c_int, _vp]),

@@ -28,7 +28,7 @@ struct dk_go1_env {
     int dtype = DK_F32, device = 0;
     int64_t n = 0, env0 = 0;
     void *qpos = nullptr, *qvel = nullptr, *cmd = nullptr, *phase = nullptr, *air = nullptr,
-         *prev = nullptr;
+         *prev = nullptr, *dr = nullptr;
     uint8_t *lastc = nullptr;
     int32_t *steps = nullptr;
     uint32_t *episode = nullptr;
@@ -133,6 +133,11 @@ dk::go1::EnvConst<T> env_const(const dk_go1_env *e) {
     }
     c.joint_noise = g.joint_noise;
     c.yaw_range = g.yaw_range;
+    for (int k = 0; k < 2; ++k) {
+        (k == 0 ? c.dr_lo : c.dr_hi)[0] = g.dr_friction[k];
+        (k == 0 ? c.dr_lo : c.dr_hi)[1] = g.dr_payload[k];
+        (k == 0 ? c.dr_lo : c.dr_hi)[2] = g.dr_kp_scale[k];
+    }
     c.has_noise = 0;
     for (int k = 0; k < 5; ++k) {
         c.noise[k] = g.obs_noise[k];
@@ -163,6 +168,7 @@ int launch(dk_go1_env *e, dk::go1::EnvIO<T> io, cudaStream_t st) {
     s.phase = (T *)e->phase;
     s.air = (T *)e->air;
     s.prev_action = (T *)e->prev;
+    s.dr = (T *)e->dr;
     s.last_contact = e->lastc;
     s.steps = e->steps;
     s.episode = e->episode;
@@ -201,6 +207,12 @@ int dk_go1_default_config(dk_go1_config *c) {
     const double nz[5] = {0.05, 0.1, 0.2, 0.01, 1.5};  // ObservationNoise defaults
     for (int k = 0; k < 5; ++k) c->obs_noise[k] = nz[k];
     c->seed = 0;
+    c->dr_friction[0] = 0.4;  // Playground-like Go1 randomisation ranges
+    c->dr_friction[1] = 1.0;
+    c->dr_payload[0] = -0.5;
+    c->dr_payload[1] = 1.5;
+    c->dr_kp_scale[0] = 0.9;
+    c->dr_kp_scale[1] = 1.1;
     dk_reward_config &r = c->reward;  // RewardTermConfig defaults (rewards.py:51-75)
     r.w_lin_vel = 1.0; r.sigma_lin_vel = 0.25; r.w_ang_vel = 0.5; r.sigma_ang_vel = 0.25;
     r.w_airtime = 1.0; r.airtime_min = 0.1; r.airtime_max = 0.5; r.w_clearance = -1.0;
@@ -229,6 +241,11 @@ int dk_go1_create(const dk_phys_model *model, const dk_go1_config *cfg, int dtyp
     for (int k = 0; k < 3; ++k)
         if (!(cfg->cmd_lo[k] <= cfg->cmd_hi[k]))
             return dk_internal_fail(DK_ERR_CONFIG, "command range lower > upper");
+    if (!(cfg->dr_friction[0] <= cfg->dr_friction[1] && cfg->dr_friction[0] >= 0 &&
+          cfg->dr_payload[0] <= cfg->dr_payload[1] &&
+          model->base_mass + cfg->dr_payload[0] > 0 && cfg->dr_kp_scale[0] <= cfg->dr_kp_scale[1] &&
+          cfg->dr_kp_scale[0] >= 0))
+        return dk_internal_fail(DK_ERR_CONFIG, "invalid domain randomisation range");
     int ndev = 0;
     if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
         return dk_internal_fail(DK_ERR_CUDA, "no such CUDA device");
@@ -252,6 +269,7 @@ int dk_go1_create(const dk_phys_model *model, const dk_go1_config *cfg, int dtyp
     alloc(&e->phase, es * 4 * n);
     alloc(&e->air, es * 4 * n);
     alloc(&e->prev, es * 12 * n);
+    alloc(&e->dr, es * 3 * n);
     alloc((void **)&e->lastc, 4 * n);
     alloc((void **)&e->steps, 4 * n);
     alloc((void **)&e->episode, 4 * n);
@@ -269,7 +287,7 @@ int dk_go1_create(const dk_phys_model *model, const dk_go1_config *cfg, int dtyp
 int dk_go1_destroy(dk_go1_env *e) {
     if (!e) return DK_OK;
     Guard g(e->device);
-    for (void *p : {e->qpos, e->qvel, e->cmd, e->phase, e->air, e->prev, (void *)e->lastc,
+    for (void *p : {e->qpos, e->qvel, e->cmd, e->phase, e->air, e->prev, e->dr, (void *)e->lastc,
                     (void *)e->steps, (void *)e->episode, (void *)e->err, (void *)e->bad})
         cudaFree(p);
     delete e;
@@ -386,6 +404,15 @@ int dk_go1_check(dk_go1_env *e, int64_t *step_index, int64_t *env_index) {
                                 "physics step: mass or Hessian matrix not positive definite");
     }
     return DK_OK;
+}
+
+int dk_go1_get_params(dk_go1_env *e, void *params, void *stream) {
+    if (!e || !params) return dk_internal_fail(DK_ERR_INVALID_INPUT, "null argument");
+    Guard g(e->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    return cuda_rc(e->dtype == DK_F64 ? rows_out<double>(e->dr, params, e->n, 3, st)
+                                      : rows_out<float>(e->dr, params, e->n, 3, st),
+                   "dk_go1_get_params");
 }
 
 int64_t dk_go1_kernel_launches(const dk_go1_env *e) { return e ? e->launches : 0; }

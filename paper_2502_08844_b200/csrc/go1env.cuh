@@ -49,6 +49,7 @@ struct EnvConst {
     T q_default[NJ];
     T phase0[NF];
     double cmd_lo[3], cmd_hi[3], joint_noise, yaw_range;
+    double dr_lo[3], dr_hi[3];  // domain randomisation: friction, payload (kg), kp scale
     double noise[5];
     RewardCfg<T> rc;
 };
@@ -56,6 +57,7 @@ struct EnvConst {
 template <typename T>
 struct EnvState {  // structure of arrays, [field][n]
     T *qpos, *qvel, *cmd, *phase, *air, *prev_action;
+    T *dr;  // [3][n]: friction, trunk mass, kp of the world's current episode
     uint8_t *last_contact;
     int32_t *steps;
     uint32_t *episode;
@@ -130,25 +132,37 @@ __device__ __forceinline__ void foot_kin(const PhysConst<T> &P, const Lane<T> &L
     for (int i = 0; i < 3; ++i) fvel[i] = vel[3 + i] + wr[i];
 }
 
-// per-world reset draw from stream_rng(seed, env, episode, 0): yaw, then the
-// 12 joint offsets, then the 3 command components (Generator.uniform order)
+// per-world reset draw from stream_rng(seed, env, episode, 0): yaw, the 12
+// joint offsets, the 3 command components, then the episode's physical
+// parameters (friction, payload, kp scale) -- Generator.uniform order; the
+// parameters follow randomization.randomize_params' additive / multiplicative
+// kinds (randomization.py:156-181)
 template <typename T>
 __device__ __noinline__ void reset_world(const PhysConst<T> &P, const EnvConst<T> &E, Lane<T> &L, int l,
                             uint64_t env, uint32_t episode, T *cmd, T &phase, T &air,
                             T *prev_action) {
     Philox4x64 rng;
     rng.init(E.seed, env, episode, 0);
-    // 16 draws in Generator.uniform order: yaw, 12 joint offsets, 3 commands
-    // (one rolled loop: a single copy of the Philox block code)
-    double u[16];
+    // 19 draws in Generator.uniform order: yaw, 12 joint offsets, 3 commands,
+    // 3 physical parameters (one rolled loop: a single copy of the Philox code)
+    double u[19];
 #pragma unroll 1
-    for (int i = 0; i < 16; ++i) {
-        const double lo = i == 0 ? -E.yaw_range
-                                 : (i < 13 ? -E.joint_noise : E.cmd_lo[i - 13 < 0 ? 0 : i - 13]);
-        const double hi = i == 0 ? E.yaw_range
-                                 : (i < 13 ? E.joint_noise : E.cmd_hi[i - 13 < 0 ? 0 : i - 13]);
+    for (int i = 0; i < 19; ++i) {
+        double lo, hi;
+        if (i == 0) {
+            lo = -E.yaw_range; hi = E.yaw_range;
+        } else if (i < 13) {
+            lo = -E.joint_noise; hi = E.joint_noise;
+        } else if (i < 16) {
+            lo = E.cmd_lo[i - 13]; hi = E.cmd_hi[i - 13];
+        } else {
+            lo = E.dr_lo[i - 16]; hi = E.dr_hi[i - 16];
+        }
         u[i] = rng.uniform(lo, hi);
     }
+    L.mu = (T)u[16];
+    L.base_mass = (T)((double)P.base_mass + u[17]);
+    L.kp = (T)((double)P.kp * u[18]);
     const double yaw = u[0];
     const double *jn = u + 1;
 #pragma unroll
@@ -172,7 +186,6 @@ __device__ __noinline__ void reset_world(const PhysConst<T> &P, const EnvConst<T
     }
     phase = E.phase0[l];
     air = T(0);
-    (void)P;
 }
 
 // observation noise into the row (lane 0): one out-of-line copy of the
@@ -319,6 +332,9 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
         for (int i = 0; i < 4; ++i) L.quat[i] = st.qpos[(3 + i) * n + w];
         phase = st.phase[l * n + w];
         air = st.air[l * n + w];
+        L.mu = st.dr[w];
+        L.base_mass = st.dr[n + w];
+        L.kp = st.dr[2 * n + w];
         lastc = st.last_contact[l * n + w];
         steps = st.steps[w];
         episode = st.episode[w];
@@ -467,6 +483,11 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
         }
         st.phase[l * n + w] = phase;
         st.air[l * n + w] = air;
+        if (l == 0) {
+            st.dr[w] = L.mu;
+            st.dr[n + w] = L.base_mass;
+            st.dr[2 * n + w] = L.kp;
+        }
         st.last_contact[l * n + w] = lastc;
     }
 }

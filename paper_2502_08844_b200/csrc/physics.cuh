@@ -426,6 +426,8 @@ struct Lane {
     T pos[3], quat[4], q[3];    // trunk pos / quat, own limb joints
     T vlin[3], wb[3], qd[3];    // trunk lin vel (world), ang vel (trunk frame), own joint vels
     T ctrl[3];
+    // per-world physical parameters (the model's, or a domain-randomised draw)
+    T mu, base_mass, kp;
 };
 
 // rows in shared memory: field f of row r of lane t at rows[(r * RF + f) * nt + t]
@@ -479,7 +481,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
         mat_vec3(R0, &P.base_ipos[0], off);
 #pragma unroll
         for (int i = 0; i < 3; ++i) com[i] = p0[i] + off[i];
-        body_inertia(P.base_mass, com, p0, R0, P.base_inertia, Ibase);
+        body_inertia(L.base_mass, com, p0, R0, P.base_inertia, Ibase);
         if (ins && lane_limb == 0)
 #pragma unroll
             for (int i = 0; i < 3; ++i) {
@@ -694,7 +696,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
     T qf_l[3], qf_s[6], act[3];
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
-        T tau = P.kp * (L.ctrl[j] - L.q[j]) - P.kd * L.qd[j];
+        T tau = L.kp * (L.ctrl[j] - L.q[j]) - P.kd * L.qd[j];
         const T lim = lm.tlim[j];
         tau = tau < -lim ? -lim : (tau > lim ? lim : tau);
         act[j] = tau;
@@ -710,7 +712,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
     LM.solve(qf_l, qf_s, a_l, a_s);
 
     // ---------------- collision + constraint rows (lane-local)
-    const T mu = P.mu;
+    const T mu = L.mu;
     int nrow = 0;
     int ncon_lane = 0;
     // contact records of this lane: up to 1 trunk + 3 limb contacts
@@ -842,18 +844,18 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
     const int world_rows = qsumi(nrow);
     int it = 0;
     if (world_rows > 0) {
+        // M a, carried across the iterations (a += alpha d  =>  M a += alpha M d):
+        // one matrix product per iteration instead of three
+        T Ma_l[3], Ma_s[6];
+        arrow_mul(M, a_l, a_s, Ma_l, Ma_s);
         for (; it < P.iterations; ++it) {
             // x = J a - aref, active set, gradient and Hessian pieces
             Arrow<T> H = M;
-            T g_l[3], g_s[6];
-            {
-                T Ma_l[3], Ma_s[6];
-                arrow_mul(M, a_l, a_s, Ma_l, Ma_s);
+            T g_l[3], g_s[6], gsm_l[3], gsm_s[6];  // full / smooth (M a - qfrc) gradient
 #pragma unroll
-                for (int i = 0; i < 3; ++i) g_l[i] = Ma_l[i] - qf_l[i];
+            for (int i = 0; i < 3; ++i) g_l[i] = gsm_l[i] = Ma_l[i] - qf_l[i];
 #pragma unroll
-                for (int i = 0; i < 6; ++i) g_s[i] = Ma_s[i] - qf_s[i];
-            }
+            for (int i = 0; i < 6; ++i) g_s[i] = gsm_s[i] = Ma_s[i] - qf_s[i];
             T gs_part[6] = {T(0), T(0), T(0), T(0), T(0), T(0)};
             T Hs_part[21];
 #pragma unroll
@@ -910,20 +912,19 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
             }
             // line search coefficients
             T c1, c2;
+            T Md_l[3], Md_s[6];
             {
-                T Md_l[3], Md_s[6], Ma_l[3], Ma_s[6];
                 arrow_mul(M, d_l, d_s, Md_l, Md_s);
-                arrow_mul(M, a_l, a_s, Ma_l, Ma_s);
                 T p1 = T(0), p2 = T(0);
 #pragma unroll
                 for (int i = 0; i < 3; ++i) {
-                    p1 = p1 + d_l[i] * (Ma_l[i] - qf_l[i]);
+                    p1 = p1 + d_l[i] * gsm_l[i];
                     p2 = p2 + d_l[i] * Md_l[i];
                 }
                 T s1 = T(0), s2 = T(0);
 #pragma unroll
                 for (int i = 0; i < 6; ++i) {
-                    s1 = s1 + d_s[i] * (Ma_s[i] - qf_s[i]);
+                    s1 = s1 + d_s[i] * gsm_s[i];
                     s2 = s2 + d_s[i] * Md_s[i];
                 }
                 c1 = qsum(p1) + s1;
@@ -977,9 +978,15 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
                 alpha = an;
             }
 #pragma unroll
-            for (int i = 0; i < 3; ++i) a_l[i] = a_l[i] + alpha * d_l[i];
+            for (int i = 0; i < 3; ++i) {
+                a_l[i] = a_l[i] + alpha * d_l[i];
+                Ma_l[i] = Ma_l[i] + alpha * Md_l[i];
+            }
 #pragma unroll
-            for (int i = 0; i < 6; ++i) a_s[i] = a_s[i] + alpha * d_s[i];
+            for (int i = 0; i < 6; ++i) {
+                a_s[i] = a_s[i] + alpha * d_s[i];
+                Ma_s[i] = Ma_s[i] + alpha * Md_s[i];
+            }
             if (qall(exact && piece_bits == act_bits)) {
                 ++it;
                 break;
@@ -1179,6 +1186,9 @@ __global__ void __launch_bounds__(THREADS) phys_kernel(PhysConst<T> pc, PhysArgs
     }
 #pragma unroll
     for (int i = 0; i < 4; ++i) L.quat[i] = a.qpos[(3 + i) * n + w];
+    L.mu = P.mu;
+    L.base_mass = P.base_mass;
+    L.kp = P.kp;
     Rows<T> rows{rowbuf, tid, (int)blockDim.x};
     if constexpr (INSPECT) {
         phys_step(P, L, rows, lane_limb, static_cast<const PhysArgs<T> *>(nullptr), w, &ins);

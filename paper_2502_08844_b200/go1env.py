@@ -32,7 +32,9 @@ class Go1ConfigC(ctypes.Structure):
                 ("term_height", ctypes.c_double), ("cmd_lo", ctypes.c_double * 3),
                 ("cmd_hi", ctypes.c_double * 3), ("joint_noise", ctypes.c_double),
                 ("yaw_range", ctypes.c_double), ("obs_noise", ctypes.c_double * 5),
-                ("seed", ctypes.c_uint64), ("reward", nat.RewardConfigC)]
+                ("seed", ctypes.c_uint64), ("reward", nat.RewardConfigC),
+                ("dr_friction", ctypes.c_double * 2), ("dr_payload", ctypes.c_double * 2),
+                ("dr_kp_scale", ctypes.c_double * 2)]
 
 
 @dataclass
@@ -51,6 +53,10 @@ class Go1Config:
     obs_noise: tuple = (0.05, 0.1, 0.2, 0.01, 1.5)  # ObservationNoise (envkit.py:138-144)
     seed: int = 0
     reward: RewardTermConfig = field(default_factory=RewardTermConfig)
+    # per-world domain randomisation at every reset (friction, payload kg, kp scale)
+    dr_friction: tuple = (0.4, 1.0)
+    dr_payload: tuple = (-0.5, 1.5)
+    dr_kp_scale: tuple = (0.9, 1.1)
 
     def to_c(self) -> Go1ConfigC:
         c = Go1ConfigC()
@@ -64,6 +70,10 @@ class Go1Config:
             c.obs_noise[k] = float(self.obs_noise[k])
         c.seed = int(self.seed) & (2**64 - 1)
         c.reward = _reward_cfg(self.reward)
+        for k in range(2):
+            c.dr_friction[k] = float(self.dr_friction[k])
+            c.dr_payload[k] = float(self.dr_payload[k])
+            c.dr_kp_scale[k] = float(self.dr_kp_scale[k])
         return c
 
     def oracle_dict(self) -> dict:
@@ -75,7 +85,8 @@ class Go1Config:
                     term_height=self.term_height, cmd_lo=tuple(self.cmd_lo),
                     cmd_hi=tuple(self.cmd_hi), joint_noise=self.joint_noise,
                     yaw_range=self.yaw_range, obs_noise=tuple(self.obs_noise), seed=self.seed,
-                    reward=rw)
+                    reward=rw, dr_friction=tuple(self.dr_friction),
+                    dr_payload=tuple(self.dr_payload), dr_kp_scale=tuple(self.dr_kp_scale))
 
 
 class DeviceGo1Env:
@@ -183,6 +194,12 @@ class DeviceGo1Env:
             "qpos", "qvel", "command", "phase", "airtime", "last_contact", "prev_action",
             "steps", "episode")], self._stream()))
         return s
+
+    def params(self):
+        """[N, 3]: each world's friction, trunk mass and kp this episode"""
+        p = self._torch.empty((self.num_envs, 3), dtype=self.dtype, device=self.device)
+        _check(self._lib.dk_go1_get_params(self.h, p.data_ptr(), self._stream()))
+        return p
 
     def check(self):
         self._torch.cuda.current_stream(self.device).synchronize()

@@ -80,6 +80,9 @@ def test_go1_env_f64_matches_oracle(G):
     for k, v in (("qpos", ref.qpos), ("qvel", ref.qvel), ("command", ref.cmd),
                  ("phase", ref.phase), ("airtime", ref.air), ("prev_action", ref.prev)):
         assert _rel(s[k], v, 1e-3) < 1e-9, k
+    # domain randomisation: each world's friction / trunk mass / kp of its episode
+    np.testing.assert_array_equal(env.params().cpu().numpy(), ref.params)
+    assert np.ptp(ref.params[:, 0]) > 0.1  # the draws do vary across worlds
     env.close()
 
 
