@@ -17,9 +17,10 @@
 //   auto-reset                Philox-keyed reset draw (stream_rng(seed, env, episode, 0),
 //                             envkit.py:41-49), terminal observation kept
 // The frame of the reward/observation row is assembled in shared memory by the
-// four lanes, lane 0 evaluates loco_row (locomotion.cuh, the same code as the
-// standalone tail kernel), and the CTA stores its 32 worlds' contiguous output
-// rows cooperatively.  The reference has no Go1 env: the physics is
+// four lanes, the four lanes evaluate the reward and observation row together
+// (loco_row's math, locomotion.cuh, split by joint / foot and quad-reduced) and
+// draw the sensor noise together (each lane its Philox blocks), and the CTA
+// stores its 32 worlds' contiguous output rows cooperatively.  The reference has no Go1 env: the physics is
 // checked against oracle/physics.c, the tail against oracle/locomotion.c, and
 // the glue against oracle/go1env.py (tests/test_gpu_go1env.py) -- UNPINNED.
 #pragma once
@@ -188,12 +189,126 @@ __device__ __noinline__ void reset_world(const PhysConst<T> &P, const EnvConst<T
     air = T(0);
 }
 
-// observation noise into the row (lane 0): one out-of-line copy of the
-// Philox draws for the three call sites
+// Observation noise into the row, quad-parallel: the draws of
+// stream_rng(seed, env, episode, step) in build_locomotion_observation's group
+// order (gravity, lin vel, ang vel, joint pos, joint vel; a group with scale 0
+// draws nothing, envkit.py:176-180).  Word q of the stream is word q % 4 of
+// Philox block q / 4 (philox_seek); lane l computes the blocks b with b % 4 == l
+// and adds the draws of their words, so every element is touched by one lane.
 template <typename T>
-__device__ __noinline__ void go1_noise(T *row, uint64_t seed, uint64_t env, uint32_t episode,
-                                       uint64_t step, const double *noise) {
-    loco_row_noise(row, NJ, seed, env, episode, step, noise);
+__device__ __noinline__ void go1_noise_quad(T *row, uint64_t seed, uint64_t env,
+                                            uint32_t episode, uint64_t step,
+                                            const double *noise, int l) {
+    const int start[5] = {0, 3, 6, 9, 9 + NJ}, len[5] = {3, 3, 3, NJ, NJ};
+    uint64_t q = 0;
+    Philox4x64 r;
+    int64_t have = -1;  // block held in r.buf
+    for (int gi = 0; gi < 5; ++gi) {
+        const double sc = noise[gi];
+        if (!(sc > 0)) continue;
+        for (int e = 0; e < len[gi]; ++e, ++q) {
+            const uint64_t blk = q >> 2;
+            if ((int)(blk & 3) != l) continue;
+            if ((int64_t)blk != have) {
+                philox_seek(r, seed, env, episode, step, blk << 2);
+                have = (int64_t)blk;
+            }
+            const int j = (int)(q & 3);
+            const uint64_t w = j == 0 ? r.buf[0] : j == 1 ? r.buf[1] : j == 2 ? r.buf[2] : r.buf[3];
+            const double range = __dsub_rn(sc, -sc);
+            const double u = __dmul_rn((double)(w >> 11), 1.0 / 9007199254740992.0);
+            row[start[gi] + e] = row[start[gi] + e] + (T)__dadd_rn(-sc, __dmul_rn(range, u));
+        }
+    }
+}
+
+// rewards.total_reward + the clean observation row (loco_row's math,
+// locomotion.cuh), quad-parallel: lane l takes joints 3l..3l+2 and foot l, the
+// ten per-joint / per-foot sums are quad-reduced, lane 0 adds the trunk terms.
+// Returns the unclipped total in every lane; terms16 filled by lane 0.
+template <typename T>
+__device__ __noinline__ T go1_row_quad(const EnvConst<T> &E, const T *fr, const uint8_t *flags,
+                                       bool done, T *row, T *terms16, int l) {
+    const RewardCfg<T> &c = E.rc;
+    const int o_jp = 9, o_jv = 9 + NJ, o_pa = 9 + 2 * NJ, o_cmd = 9 + 3 * NJ;
+    const int o_ph = o_cmd + 3, o_con = S, o_tau = S + NF, o_pert = S + NF + NJ;
+    T tt = 0, jp = 0, ar = 0, en = 0, pose = 0, vv = 0;
+#pragma unroll
+    for (int jj = 0; jj < 3; ++jj) {
+        const int j = 3 * l + jj;
+        const T qj = fr[O_JPOS + j], vj = fr[O_JVEL + j], tj = fr[O_JTAU + j];
+        tt = tt + tj * tj;
+        const T d1 = qj - E.q_default[j];
+        jp = jp + d1 * d1;
+        const T d2 = fr[O_ACT + j] - fr[O_FPA + j];
+        ar = ar + d2 * d2;
+        en = en + fabs(vj * tj);
+        pose = pose + d1 * d1;  // joint_default == joint_nominal == q_default here
+        vv = vv + vj * vj;
+        row[o_jp + j] = qj;
+        row[o_jv + j] = vj;
+        row[o_pa + j] = fr[O_ACT + j];
+        row[o_tau + j] = tj;
+    }
+    T air_s, clr, ph, slip;
+    {
+        const int k = l;
+        const T span = c.airtime_max - c.airtime_min;
+        T gain = (fr[O_AIR + k] - c.airtime_min) * (flags[k] ? T(1) : T(0));
+        air_s = gain < T(0) ? T(0) : (gain > span ? span : gain);
+        const T hk = fr[O_FH + k], err_h = hk - fr[O_FHD + k];
+        const T vx = fr[O_FVEL + 2 * k], vy = fr[O_FVEL + 2 * k + 1];
+        const T sp = RealOps<T>::sqrt_(vx * vx + vy * vy);
+        clr = err_h * err_h * RealOps<T>::sqrt_(sp);
+        T sn, cs;
+        RealOps<T>::sincos_(fr[O_PHASE + k], &sn, &cs);
+        const T tgt = c.swing_height * (sn > T(0) ? sn : T(0));
+        const T dz = hk - tgt;
+        ph = dz * dz;
+        const T m = flags[4 + k] ? T(1) : T(0);
+        const T cx = vx * m, cy = vy * m;
+        slip = cx * cx + cy * cy;
+        row[o_ph + 2 * k] = cs;
+        row[o_ph + 2 * k + 1] = sn;
+        row[o_con + k] = m;
+    }
+    tt = phys::qsum(tt); jp = phys::qsum(jp); ar = phys::qsum(ar); en = phys::qsum(en);
+    pose = phys::qsum(pose); vv = phys::qsum(vv); air_s = phys::qsum(air_s);
+    clr = phys::qsum(clr); ph = phys::qsum(ph); slip = phys::qsum(slip);
+    T t[16];
+    const T *lin = fr + O_LIN, *ang = fr + O_ANG, *fcmd = fr + O_CMD;
+    const T e0 = fcmd[0] - lin[0], e1 = fcmd[1] - lin[1];
+    t[0] = rexp(-(e0 * e0 + e1 * e1) / c.sigma_lin);
+    const T ea = fcmd[2] - ang[2];
+    t[1] = rexp(-(ea * ea) / c.sigma_ang);
+    T g[3];
+    if (!project_gravity(fr + O_Q, g)) g[0] = g[1] = g[2] = T(NAN);
+    t[6] = g[0] * g[0] + g[1] * g[1];
+    t[7] = tt; t[8] = jp; t[9] = ar; t[10] = en;
+    t[11] = rexp(-pose);
+    t[2] = air_s; t[3] = clr; t[4] = rexp(-ph / c.sigma_phase); t[5] = slip;
+    t[12] = done ? T(1) : T(0);
+    const T cn = RealOps<T>::sqrt_(fcmd[0] * fcmd[0] + fcmd[1] * fcmd[1]);
+    t[13] = !c.gated ? cn : (cn > T(0.1) ? T(0) : RealOps<T>::sqrt_(vv));
+    t[14] = lin[2] * lin[2];
+    t[15] = ang[0] * ang[0] + ang[1] * ang[1];
+    T u = T(0);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) u = u + c.w[k] * t[k];
+    if (l == 0) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+            row[i] = g[i];
+            row[3 + i] = lin[i];
+            row[6 + i] = ang[i];
+            row[o_cmd + i] = fcmd[i];
+            row[o_pert + i] = T(0);
+        }
+        if (terms16)
+#pragma unroll
+            for (int k = 0; k < 16; ++k) terms16[k] = t[k];
+    }
+    return u;
 }
 
 // lane-parallel part of the frame of the current state (each lane its limb,
@@ -245,37 +360,6 @@ __device__ __noinline__ bool fill_frame(const PhysConst<T> &Pc, const EnvConst<T
         }
     }
     return contact;
-}
-
-// reward + clean observation row of the frame in `fr` (lane 0 of the quad)
-template <typename T>
-__device__ __noinline__ T build_row(const EnvConst<T> &E, const T *fr, const uint8_t *flags,
-                                    bool done, T *row, T *terms16) {
-    LocoRowIn<T> in;
-    in.q = fr + O_Q;
-    in.lin = fr + O_LIN;
-    in.ang = fr + O_ANG;
-    in.cmd = fr + O_CMD;
-    in.fcmd = fr + O_CMD;
-    in.pa = fr + O_ACT;   // observation: the action just applied
-    in.fpa = fr + O_FPA;  // reward action rate: against the previous action
-    in.nom = E.q_default;
-    in.def = E.q_default;
-    in.jpos = fr + O_JPOS;
-    in.jvel = fr + O_JVEL;
-    in.jtau = fr + O_JTAU;
-    in.act = fr + O_ACT;
-    in.air = fr + O_AIR;
-    in.fh = fr + O_FH;
-    in.fhd = fr + O_FHD;
-    in.fvel = fr + O_FVEL;
-    in.phase = fr + O_PHASE;
-    in.td = flags;
-    in.con = flags + 4;
-    in.done = done;
-    in.pert = nullptr;
-    bool ok;
-    return loco_row<false>(in, E.rc, NJ, NF, row, terms16, ok);
 }
 
 template <typename T>
@@ -340,15 +424,9 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
         episode = st.episode[w];
     }
 
-    auto build = [&](bool done, T *reward, T *terms16) {
-        if (l == 0) {
-            T t[16];
-            const T u = build_row(E, fr, flags, done, row, t);
-            if (reward) *reward = T(0) > u ? T(0) : u;
-            if (terms16)
-#pragma unroll
-                for (int k = 0; k < 16; ++k) terms16[k] = t[k];
-        }
+    auto build = [&](bool done, T *reward, T *terms16) {  // all four lanes of the quad
+        const T u = go1_row_quad(E, fr, flags, done, row, terms16, l);
+        if (reward) *reward = T(0) > u ? T(0) : u;
     };
     // cooperative, coalesced store of the CTA's rows [nlive][cols] (tile pitch P)
     auto store_rows = [&](T *dst, int cols) {
@@ -361,9 +439,8 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
 
     // observation noise key: stream_rng(seed, env, episode, steps + 1) -- step 0
     // of an episode's stream belongs to its reset draw
-    auto add_noise = [&]() {
-        if (l == 0 && E.has_noise)
-            go1_noise(row, E.seed, env, episode, (uint64_t)steps + 1, E.noise);
+    auto add_noise = [&]() {  // all four lanes of the quad
+        if (E.has_noise) go1_noise_quad(row, E.seed, env, episode, (uint64_t)steps + 1, E.noise, l);
     };
     auto do_reset = [&]() {
         reset_world(Pc, E, L, l, env, episode, cmd, phase, air, prev);
