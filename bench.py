@@ -730,7 +730,8 @@ def run_b200(args, rank, world, local_rank, dist):
     extras = {}
     if rank == 0 and not args.no_extra:
         # the pinned analytic task (the reference's own physics) at the same world count
-        extras["cartpole"] = analytic_line(args, dev, rank, world, dist, local_rank)
+        # rank-0-only lines: no collective inside (the other ranks are not there)
+        extras["cartpole"] = analytic_line(args, dev, 0, 1, None, local_rank)
         extras["go1_sweep"] = bench_go1_sweep(args, dev)
         extras["physics_only"] = bench_phys_only(args, dev)
         extras["loco_small"] = bench_loco_small(args, dev)
