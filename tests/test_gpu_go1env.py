@@ -42,14 +42,18 @@ def _cfg(G, **kw):
     return c
 
 
-def test_go1_env_f64_matches_oracle(G):
+@pytest.mark.parametrize("geoms", ["feet", "full"])
+def test_go1_env_f64_matches_oracle(G, geoms):
+    """feet: the default feet-only collision; full: trunk box and thigh capsules
+    collide too (the fused kernel with 19 constraint rows per lane)."""
     from oracle.go1env import OracleGo1Env
     from paper_2502_08844_b200 import physmodel as pm
 
     n, K = 64, 60
     cfg = _cfg(G)
-    env = G.DeviceGo1Env(n, cfg, dtype="float64", env_index_offset=100)
-    ref = OracleGo1Env(pm.go1_model(), cfg.oracle_dict(), n, env_index_offset=100)
+    model = pm.go1_model(**({} if geoms == "feet" else dict(collide_box=1, collide_thigh=1)))
+    env = G.DeviceGo1Env(n, cfg, model=model, dtype="float64", env_index_offset=100)
+    ref = OracleGo1Env(model, cfg.oracle_dict(), n, env_index_offset=100)
     o = env.reset(seed=3)
     r_obs, r_priv = ref.reset(seed=3)
     assert _rel(o["state"].cpu().numpy(), r_obs, 1e-3) < 1e-12
