@@ -81,10 +81,12 @@ template <typename T> struct PMath;
 template <> struct PMath<float> {
     static __device__ __forceinline__ void sincos_(float x, float *s, float *c) { sincosf(x, s, c); }
     static __device__ __forceinline__ float sqrt_(float x) { return sqrtf(x); }
+    static __device__ __forceinline__ float rsqrt_(float x) { return rsqrtf(x); }
 };
 template <> struct PMath<double> {
     static __device__ __forceinline__ void sincos_(double x, double *s, double *c) { sincos(x, s, c); }
     static __device__ __forceinline__ double sqrt_(double x) { return sqrt(x); }
+    static __device__ __forceinline__ double rsqrt_(double x) { return rsqrt(x); }
 };
 
 __device__ __forceinline__ unsigned quad_mask() {
@@ -283,31 +285,40 @@ struct Arrow {
     T B[6];      // limb block, lower: 00 10 11 20 21 22
     T C[6][3];   // coupling (trunk row, limb col)
     T A[21];     // trunk block, lower packed row-major: (i, j<=i) at i(i+1)/2 + j
+    T iB[3], iA[6];  // after factor(): reciprocals of the diagonals of L_B / L_S
 
     static __device__ __forceinline__ int ai(int i, int j) { return i * (i + 1) / 2 + j; }
 
-    // in place: B -> L_B, C -> W, A -> L_S; false if not positive definite
+    // in place: B -> L_B, C -> W, A -> L_S; false if not positive definite.
+    // One division per pivot (its reciprocal, kept in iB / iA), products
+    // elsewhere: the factor and every solve multiply by the reciprocals instead of
+    // dividing (IEEE division is a multi-instruction sequence on every SM pipe).
     __device__ bool factor() {
         bool ok = true;
         // 3x3 Cholesky of B
+        // pivots: 1/l = rsqrt(s), l = s / l = s * (1/l)
         T l00 = B[0];
         ok &= l00 > T(0);
-        l00 = PMath<T>::sqrt_(l00);
-        const T l10 = B[1] / l00, l20 = B[3] / l00;
+        const T i00 = PMath<T>::rsqrt_(l00);
+        l00 = l00 * i00;
+        const T l10 = B[1] * i00, l20 = B[3] * i00;
         T l11 = B[2] - l10 * l10;
         ok &= l11 > T(0);
-        l11 = PMath<T>::sqrt_(l11);
-        const T l21 = (B[4] - l20 * l10) / l11;
+        const T i11 = PMath<T>::rsqrt_(l11);
+        l11 = l11 * i11;
+        const T l21 = (B[4] - l20 * l10) * i11;
         T l22 = (B[5] - l20 * l20) - l21 * l21;
         ok &= l22 > T(0);
-        l22 = PMath<T>::sqrt_(l22);
+        const T i22 = PMath<T>::rsqrt_(l22);
+        l22 = l22 * i22;
         B[0] = l00; B[1] = l10; B[2] = l11; B[3] = l20; B[4] = l21; B[5] = l22;
+        iB[0] = i00; iB[1] = i11; iB[2] = i22;
         // W = C L_B^-T: row b solves L_B w = C_b
 #pragma unroll
         for (int b = 0; b < 6; ++b) {
-            const T w0 = C[b][0] / l00;
-            const T w1 = (C[b][1] - l10 * w0) / l11;
-            const T w2 = ((C[b][2] - l20 * w0) - l21 * w1) / l22;
+            const T w0 = C[b][0] * i00;
+            const T w1 = (C[b][1] - l10 * w0) * i11;
+            const T w2 = ((C[b][2] - l20 * w0) - l21 * w1) * i22;
             C[b][0] = w0; C[b][1] = w1; C[b][2] = w2;
         }
         // Schur complement S = A - sum_l W W^T, reduced across the quad
@@ -325,14 +336,16 @@ struct Arrow {
 #pragma unroll
             for (int k = 0; k < j; ++k) s = s - A[ai(j, k)] * A[ai(j, k)];
             ok &= s > T(0);
-            const T d = PMath<T>::sqrt_(s);
+            const T id = PMath<T>::rsqrt_(s);
+            const T d = s * id;
             A[ai(j, j)] = d;
+            iA[j] = id;
 #pragma unroll
             for (int i = j + 1; i < 6; ++i) {
                 T t = A[ai(i, j)];
 #pragma unroll
                 for (int k = 0; k < j; ++k) t = t - A[ai(i, k)] * A[ai(j, k)];
-                A[ai(i, j)] = t / d;
+                A[ai(i, j)] = t * id;
             }
         }
         return qall(ok);
@@ -340,9 +353,9 @@ struct Arrow {
 
     // forward half: y_l = L_B^-1 b_l (lane), y_s = L_S^-1 (b_s - sum_l W_l y_l)
     __device__ __forceinline__ void fwd(const T *bl, const T *bs, T *yl, T *ys) const {
-        yl[0] = bl[0] / B[0];
-        yl[1] = (bl[1] - B[1] * yl[0]) / B[2];
-        yl[2] = ((bl[2] - B[3] * yl[0]) - B[4] * yl[1]) / B[5];
+        yl[0] = bl[0] * iB[0];
+        yl[1] = (bl[1] - B[1] * yl[0]) * iB[1];
+        yl[2] = ((bl[2] - B[3] * yl[0]) - B[4] * yl[1]) * iB[2];
         T r[6];
 #pragma unroll
         for (int i = 0; i < 6; ++i) r[i] = bs[i] - qsum(dot3(C[i], yl));
@@ -351,9 +364,9 @@ struct Arrow {
     // lane-local variant for a row touching only limb l and the trunk:
     // the other limbs' b_l are zero, so no reduction
     __device__ __forceinline__ void fwd_local(const T *bl, const T *bs, T *yl, T *ys) const {
-        yl[0] = bl[0] / B[0];
-        yl[1] = (bl[1] - B[1] * yl[0]) / B[2];
-        yl[2] = ((bl[2] - B[3] * yl[0]) - B[4] * yl[1]) / B[5];
+        yl[0] = bl[0] * iB[0];
+        yl[1] = (bl[1] - B[1] * yl[0]) * iB[1];
+        yl[2] = ((bl[2] - B[3] * yl[0]) - B[4] * yl[1]) * iB[2];
         T r[6];
 #pragma unroll
         for (int i = 0; i < 6; ++i) r[i] = bs[i] - dot3(C[i], yl);
@@ -365,7 +378,7 @@ struct Arrow {
             T s = r[i];
 #pragma unroll
             for (int k = 0; k < i; ++k) s = s - A[ai(i, k)] * ys[k];
-            ys[i] = s / A[ai(i, i)];
+            ys[i] = s * iA[i];
         }
     }
     // full solve M x = b (b_l per lane, b_s redundant)
@@ -377,7 +390,7 @@ struct Arrow {
             T s = ys[i];
 #pragma unroll
             for (int k = i + 1; k < 6; ++k) s = s - A[ai(k, i)] * xs[k];
-            xs[i] = s / A[ai(i, i)];
+            xs[i] = s * iA[i];
         }
         // x_l = L_B^-T (y_l - W^T x_s)
         T z[3];
@@ -388,9 +401,9 @@ struct Arrow {
             for (int b = 0; b < 6; ++b) s = s - C[b][j] * xs[b];
             z[j] = s;
         }
-        xl[2] = z[2] / B[5];
-        xl[1] = (z[1] - B[4] * xl[2]) / B[2];
-        xl[0] = ((z[0] - B[1] * xl[1]) - B[3] * xl[2]) / B[0];
+        xl[2] = z[2] * iB[2];
+        xl[1] = (z[1] - B[4] * xl[2]) * iB[1];
+        xl[0] = ((z[0] - B[1] * xl[1]) - B[3] * xl[2]) * iB[0];
     }
 };
 
@@ -1105,9 +1118,9 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
             const T n3 = ((q[0] * r[3] + q[1] * r[2]) - q[2] * r[1]) + q[3] * r[0];
             q[0] = n0; q[1] = n1; q[2] = n2; q[3] = n3;
         }
-        const T qn = PMath<T>::sqrt_(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
+        const T iqn = PMath<T>::rsqrt_(((q[0] * q[0] + q[1] * q[1]) + q[2] * q[2]) + q[3] * q[3]);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) q[i] = q[i] / qn;
+        for (int i = 0; i < 4; ++i) q[i] = q[i] * iqn;
     }
 #pragma unroll
     for (int i = 0; i < 3; ++i) L.q[i] = L.q[i] + h * L.qd[i];
