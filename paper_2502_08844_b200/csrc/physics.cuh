@@ -329,23 +329,30 @@ struct Arrow {
                 const T ww = qsum(dot3(C[i], C[j]));
                 A[ai(i, j)] = A[ai(i, j)] - ww;
             }
-        // 6x6 Cholesky (redundant in all lanes)
+        // 6x6 Cholesky (redundant in all lanes).  Constant trip counts with
+        // guards: LLVM unrolls inner loops first, and an inner loop whose bound
+        // depends on j is left rolled ("nounroll") -- which demoted the whole
+        // Arrow to local memory (608-byte stack frame, measured in the PTX)
 #pragma unroll
         for (int j = 0; j < 6; ++j) {
             T s = A[ai(j, j)];
 #pragma unroll
-            for (int k = 0; k < j; ++k) s = s - A[ai(j, k)] * A[ai(j, k)];
+            for (int k = 0; k < 6; ++k)
+                if (k < j) s = s - A[ai(j, k)] * A[ai(j, k)];
             ok &= s > T(0);
             const T id = PMath<T>::rsqrt_(s);
             const T d = s * id;
             A[ai(j, j)] = d;
             iA[j] = id;
 #pragma unroll
-            for (int i = j + 1; i < 6; ++i) {
-                T t = A[ai(i, j)];
+            for (int i = 1; i < 6; ++i) {
+                if (i > j) {
+                    T t = A[ai(i, j)];
 #pragma unroll
-                for (int k = 0; k < j; ++k) t = t - A[ai(i, k)] * A[ai(j, k)];
-                A[ai(i, j)] = t * id;
+                    for (int k = 0; k < 6; ++k)
+                        if (k < j) t = t - A[ai(i, k)] * A[ai(j, k)];
+                    A[ai(i, j)] = t * id;
+                }
             }
         }
         return qall(ok);

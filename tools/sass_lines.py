@@ -12,7 +12,7 @@ import sys
 def main():
     cubin, top = sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 30
     txt = subprocess.run(["nvdisasm", "-gi", cubin], capture_output=True, text=True).stdout
-    fn, cur = None, None
+    fn, cur, fresh = None, None, True
     per_fn = collections.Counter()
     per_line = collections.Counter()
     for line in txt.splitlines():
@@ -22,8 +22,12 @@ def main():
             continue
         m = re.search(r'## File "([^"]+)", line (\d+)', line)
         if m:
-            cur = (m.group(1).split("/")[-1], int(m.group(2)))
+            # the first line-info record of a block is the innermost location
+            if fresh:
+                cur = (m.group(1).split("/")[-1], int(m.group(2)))
+            fresh = False
             continue
+        fresh = True
         if fn and re.match(r"\s+/\*[0-9a-f]{4,}\*/\s+\S", line):
             per_fn[fn] += 1
             if cur:
