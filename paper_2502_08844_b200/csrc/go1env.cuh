@@ -392,7 +392,7 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
     T *fr = frames + (size_t)wl * FR;
     T *row = tile + (size_t)wl * P;
     uint8_t *flags = reinterpret_cast<uint8_t *>(fr + O_FLAGS);
-    Rows<T> rows{rowbuf, tid, nt};
+    Rows<T> rows{rowbuf + (size_t)tid * pc.rows_per_lane * phys::RF};
     const uint64_t env = (uint64_t)(E.env0 + w);
 
     // ---- load the world

@@ -21,8 +21,8 @@
 // trunk block -- so the Cholesky factorisation eliminates the limbs first
 // (lane-local 3x3 factor + 6x3 solve), reduces the 6x6 Schur complement
 // across the quad and factors it redundantly: no fill-in, no 18x18 dense
-// factor.  Constraint rows live in shared memory, laid out [row][field][lane]
-// (conflict-free).  Per step: FK + RNE bias + CRB mass matrix, actuator PD,
+// factor.  Constraint rows live in shared memory, lane-major with an odd
+// per-lane stride (conflict-free).  Per step: FK + RNE bias + CRB mass matrix, actuator PD,
 // unconstrained acceleration, collision (floor vs trunk-box corners, thigh
 // capsule ends, foot spheres), pyramidal contact rows + joint-limit rows with
 // MuJoCo-style soft-constraint parameters, primal Newton with exact
@@ -293,7 +293,10 @@ struct Arrow {
     // One division per pivot (its reciprocal, kept in iB / iA), products
     // elsewhere: the factor and every solve multiply by the reciprocals instead of
     // dividing (IEEE division is a multi-instruction sequence on every SM pipe).
-    __device__ bool factor() {
+    // Apart (nullable): a lane-local addend of the trunk block, reduced across
+    // the quad together with the Schur term -- A + sum_l (Apart_l - W_l W_l^T)
+    // in one quad reduction per entry instead of two
+    __device__ __forceinline__ bool factor(const T *Apart = nullptr) {
         bool ok = true;
         // 3x3 Cholesky of B
         // pivots: 1/l = rsqrt(s), l = s / l = s * (1/l)
@@ -326,8 +329,11 @@ struct Arrow {
         for (int i = 0; i < 6; ++i)
 #pragma unroll
             for (int j = 0; j <= i; ++j) {
-                const T ww = qsum(dot3(C[i], C[j]));
-                A[ai(i, j)] = A[ai(i, j)] - ww;
+                if (Apart) {
+                    A[ai(i, j)] = A[ai(i, j)] + qsum(Apart[ai(i, j)] - dot3(C[i], C[j]));
+                } else {
+                    A[ai(i, j)] = A[ai(i, j)] - qsum(dot3(C[i], C[j]));
+                }
             }
         // 6x6 Cholesky (redundant in all lanes).  Constant trip counts with
         // guards: LLVM unrolls inner loops first, and an inner loop whose bound
@@ -388,10 +394,22 @@ struct Arrow {
             ys[i] = s * iA[i];
         }
     }
-    // full solve M x = b (b_l per lane, b_s redundant)
-    __device__ __forceinline__ void solve(const T *bl, const T *bs, T *xl, T *xs) const {
+    // full solve M x = b (b_l per lane, b_s redundant; bs_part nullable: a
+    // lane-local addend of b_s, reduced with the forward half's own reduction)
+    __device__ __forceinline__ void solve(const T *bl, const T *bs, T *xl, T *xs,
+                                          const T *bs_part = nullptr) const {
         T yl[3], ys[6];
-        fwd(bl, bs, yl, ys);
+        if (bs_part) {
+            yl[0] = bl[0] * iB[0];
+            yl[1] = (bl[1] - B[1] * yl[0]) * iB[1];
+            yl[2] = ((bl[2] - B[3] * yl[0]) - B[4] * yl[1]) * iB[2];
+            T r[6];
+#pragma unroll
+            for (int i = 0; i < 6; ++i) r[i] = bs[i] + qsum(bs_part[i] - dot3(C[i], yl));
+            fwd_s(r, ys);
+        } else {
+            fwd(bl, bs, yl, ys);
+        }
 #pragma unroll
         for (int i = 5; i >= 0; --i) {
             T s = ys[i];
@@ -450,13 +468,16 @@ struct Lane {
     T mu, base_mass, kp;
 };
 
-// rows in shared memory: field f of row r of lane t at rows[(r * RF + f) * nt + t]
-// (nt = threads of the CTA: 128, or fewer when many collision geoms need more rows)
+// rows in shared memory, lane-major: field f of row r of lane t at
+// rows[t * S + r * RF + f], S = rows_per_lane * RF.  S is odd for every model
+// (rows_per_lane = 4 box + 8 thigh + 7 is odd, RF = 13), so the 32 lanes of a
+// warp hit 32 distinct banks; and per lane the fields of a row are immediate
+// offsets from one row pointer (the [row][field][lane] layout this replaces
+// spent 6% of the Go1 kernel's instructions on address arithmetic, ncu).
 template <typename T>
 struct Rows {
-    T *base;
-    int t, nt;
-    __device__ __forceinline__ T &at(int r, int f) const { return base[(r * RF + f) * nt + t]; }
+    T *p;  // this lane's rows
+    __device__ __forceinline__ T &at(int r, int f) const { return p[r * RF + f]; }
 };
 
 enum { F_JB = 0, F_JL = 6, F_AREF = 9, F_D = 10, F_X = 11, F_Y = 12 };
@@ -916,19 +937,20 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
                             Hs_part[Arrow<T>::ai(i, j)] = Hs_part[Arrow<T>::ai(i, j)] + D * jb[i] * jb[j];
                 }
             }
-#pragma unroll
-            for (int i = 0; i < 6; ++i) g_s[i] = g_s[i] + qsum(gs_part[i]);
-#pragma unroll
-            for (int e = 0; e < 21; ++e) H.A[e] = H.A[e] + qsum(Hs_part[e]);
-            ok &= H.factor();
+            // H's trunk block and the gradient's trunk part are reduced across
+            // the quad inside the factor / the solve's forward half
+            ok &= H.factor(Hs_part);
             T d_l[3], d_s[6];
             {
-                T ng_l[3], ng_s[6];
+                T ng_l[3], ng_s[6], ngs_part[6];
 #pragma unroll
                 for (int i = 0; i < 3; ++i) ng_l[i] = -g_l[i];
 #pragma unroll
-                for (int i = 0; i < 6; ++i) ng_s[i] = -g_s[i];
-                H.solve(ng_l, ng_s, d_l, d_s);
+                for (int i = 0; i < 6; ++i) {
+                    ng_s[i] = -g_s[i];
+                    ngs_part[i] = -gs_part[i];
+                }
+                H.solve(ng_l, ng_s, d_l, d_s, ngs_part);
             }
             // line search coefficients
             T c1, c2;
@@ -1209,7 +1231,7 @@ __global__ void __launch_bounds__(THREADS) phys_kernel(PhysConst<T> pc, PhysArgs
     L.mu = P.mu;
     L.base_mass = P.base_mass;
     L.kp = P.kp;
-    Rows<T> rows{rowbuf, tid, (int)blockDim.x};
+    Rows<T> rows{rowbuf + (size_t)tid * pc.rows_per_lane * RF};
     if constexpr (INSPECT) {
         phys_step(P, L, rows, lane_limb, static_cast<const PhysArgs<T> *>(nullptr), w, &ins);
         return;
