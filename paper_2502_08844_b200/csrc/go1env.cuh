@@ -486,11 +486,12 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
             if (!phys::qall(finite) && l == 0 && io.err)
                 atomicMin(io.err, (unsigned long long)(k * n + w));
             bool okp = true;
+            // (a full CTA: every thread steps, so the step's CTA barriers are safe)
             for (int s = 0; s < E.substeps; ++s)
                 okp &= phys::phys_step(Pc, L, rows, l,
                                        static_cast<const phys::PhysArgs<T> *>(nullptr), w,
                                        static_cast<const phys::PhysInspect<T> *>(nullptr),
-                                       s + 1 == E.substeps ? tau : nullptr);
+                                       s + 1 == E.substeps ? tau : nullptr, nlive == wpc);
             if (!okp && l == 0 && io.bad) *io.bad = 1;
             const bool c = fill_frame(Pc, E, L, l, fr, flags, a, tau, prev, cmd, false, lastc,
                                       phase, air);

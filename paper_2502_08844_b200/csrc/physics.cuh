@@ -44,6 +44,9 @@ constexpr int WPC = 32;            // worlds per CTA
 constexpr int THREADS = WPC * QUAD;
 constexpr int RF = 13;             // row fields: J base 6, J limb 3, aref, D, x, y
 constexpr int NS = DK_PHYS_NSENSOR;
+#ifndef DK_PHYS_SYNC_LEVEL
+#define DK_PHYS_SYNC_LEVEL 2  // CTA barriers per step: 1 at the start, 2 + Newton / Euler, 3 + CRB / rows
+#endif
 
 template <typename T>
 struct LimbConst {
@@ -495,7 +498,18 @@ struct PhysInspect {
 template <typename T>
 __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int lane_limb,
                           const PhysArgs<T> *dg, int64_t w, const PhysInspect<T> *ins = nullptr,
-                          T *act_out = nullptr) {
+                          T *act_out = nullptr, bool cta_sync = false) {
+    // CTA barriers at phase boundaries (cta_sync: CTA-uniform, every thread of
+    // the CTA steps).  The step is ~240 KB of straight-line SASS and the SM
+    // runs only ~2 warps per sub-partition at 8K worlds, so warps drifting
+    // through different code each miss in the instruction cache ("no
+    // instruction" was ~48% of stalls); aligned warps share the fetched lines
+    // (measured: Go1 env 2.16e8 -> 3.12e8 physics steps/s with one barrier per
+    // substep).
+    auto phase_sync = [&](int level) {
+        if (cta_sync && level <= DK_PHYS_SYNC_LEVEL) __syncthreads();
+    };
+    phase_sync(1);
     const LimbConst<T> &lm = P.limb[lane_limb];
     const T h = P.h;
     // ---------------- trunk FK and velocity (redundant in the quad)
@@ -642,6 +656,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
         }
     }
 
+    phase_sync(3);
     // ---------------- CRB mass matrix (arrow) + armature + h * damping
     Arrow<T> M;
     {
@@ -752,6 +767,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
     T a_l[3], a_s[6];
     LM.solve(qf_l, qf_s, a_l, a_s);
 
+    phase_sync(3);
     // ---------------- collision + constraint rows (lane-local)
     const T mu = L.mu;
     int nrow = 0;
@@ -881,6 +897,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
     (void)ncon_rows;
     (void)box_mine;
 
+    phase_sync(2);
     // ---------------- primal Newton with exact line search
     const int world_rows = qsumi(nrow);
     int it = 0;
@@ -1123,6 +1140,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
         }
     }
 
+    phase_sync(2);
     // ---------------- semi-implicit Euler
 #pragma unroll
     for (int i = 0; i < 3; ++i) {
@@ -1240,9 +1258,13 @@ __global__ void __launch_bounds__(THREADS) phys_kernel(PhysConst<T> pc, PhysArgs
     const bool want = a.qacc || a.qfrc_bias || a.qfrc_constraint || a.act_force || a.ncon ||
                       a.contact_geom || a.contact_dist || a.contact_pos || a.contact_force ||
                       a.solver_iter;
+    // every thread of a full CTA steps: CTA barriers inside the step are safe
+    const bool full = (int64_t)(blockIdx.x + 1) * (blockDim.x >> 2) <= n;
     for (int64_t s = 0; s < a.num_steps; ++s) {
         const bool last = want && s + 1 == a.num_steps;
-        ok &= phys_step(P, L, rows, lane_limb, last ? &a : nullptr, w);
+        ok &= phys_step(P, L, rows, lane_limb, last ? &a : nullptr, w,
+                        static_cast<const PhysInspect<T> *>(nullptr), static_cast<T *>(nullptr),
+                        full);
     }
     // state back
 #pragma unroll
@@ -1277,8 +1299,6 @@ size_t phys_smem_bytes(const PhysConst<T> &pc, int threads) {
 template <typename T>
 cudaError_t launch_phys(const PhysConst<T> &pc, const PhysArgs<T> &a, const PhysInspect<T> &ins,
                         cudaStream_t st) {
-    // 128 threads (32 worlds) per CTA unless the constraint rows of that many
-    // lanes would not fit two CTAs' worth of shared memory on an SM
     // 128 threads (32 worlds) per CTA unless the constraint rows of that many
     // lanes would not fit two CTAs' worth of shared memory on an SM (measured:
     // 32-thread CTAs run the physics kernel at the same speed and the fused
