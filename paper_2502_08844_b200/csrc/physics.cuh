@@ -901,12 +901,17 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
     // ---------------- primal Newton with exact line search
     const int world_rows = qsumi(nrow);
     int it = 0;
-    if (world_rows > 0) {
+    bool solving = world_rows > 0;
+    // level 4: the iterations run CTA-uniformly (quads that converged sit out)
+    // with a barrier per iteration
+    const bool it_sync = cta_sync && DK_PHYS_SYNC_LEVEL >= 4;
+    if (it_sync ? __syncthreads_or(solving) != 0 : solving) {
         // M a, carried across the iterations (a += alpha d  =>  M a += alpha M d):
         // one matrix product per iteration instead of three
         T Ma_l[3], Ma_s[6];
         arrow_mul(M, a_l, a_s, Ma_l, Ma_s);
-        for (; it < P.iterations; ++it) {
+        // one Newton iteration; true when a is the minimiser
+        auto newton_iter = [&]() -> bool {
             // x = J a - aref, active set, gradient and Hessian pieces
             Arrow<T> H = M;
             T g_l[3], g_s[6], gsm_l[3], gsm_s[6];  // full / smooth (M a - qfrc) gradient
@@ -998,10 +1003,7 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
                              rows.at(r, F_JL + 2) * d_l[2]);
                 rows.at(r, F_Y) = y;
             }
-            if (!(c2 > T(0))) {  // zero step: already the minimiser
-                ++it;
-                break;
-            }
+            if (!(c2 > T(0))) return true;  // zero step: already the minimiser
             T alpha = T(1), lo = T(0), hi = T(-1);  // hi < 0: unbounded
             bool exact = false;
             unsigned piece_bits = 0;
@@ -1046,9 +1048,17 @@ __device__ bool phys_step(const PhysConst<T> &P, Lane<T> &L, Rows<T> rows, int l
                 a_s[i] = a_s[i] + alpha * d_s[i];
                 Ma_s[i] = Ma_s[i] + alpha * Md_s[i];
             }
-            if (qall(exact && piece_bits == act_bits)) {
-                ++it;
+            return qall(exact && piece_bits == act_bits);
+        };
+        for (int k = 0; k < P.iterations; ++k) {
+            if (it_sync) {
+                if (!__syncthreads_or(solving)) break;
+            } else if (!solving) {
                 break;
+            }
+            if (solving) {
+                ++it;
+                if (newton_iter()) solving = false;
             }
         }
     }
