@@ -586,8 +586,7 @@ size_t env_smem_bytes(const PhysConst<T> &pc, int threads) {
 template <typename T>
 cudaError_t launch_env(const PhysConst<T> &pc, const EnvConst<T> &ec, const EnvState<T> &st,
                        const EnvIO<T> &io, cudaStream_t s) {
-    int threads = DK_PHYS_CTA_THREADS;
-    while (threads > 32 && env_smem_bytes(pc, threads) > 110 * 1024) threads /= 2;
+    const int threads = phys::pick_threads(io.n, [&](int t) { return env_smem_bytes(pc, t); });
     const size_t smem = env_smem_bytes(pc, threads);
     static size_t attr = 0;
     if (smem > attr) {

@@ -37,11 +37,13 @@ namespace dk {
 namespace phys {
 
 #ifndef DK_PHYS_CTA_THREADS
-#define DK_PHYS_CTA_THREADS 128
+#define DK_PHYS_CTA_THREADS 256
 #endif
 constexpr int QUAD = 4;
-constexpr int WPC = 32;            // worlds per CTA
-constexpr int THREADS = WPC * QUAD;
+constexpr int THREADS = DK_PHYS_CTA_THREADS;  // largest CTA (launch bounds)
+constexpr int WPC = THREADS / QUAD;           // worlds per (full) CTA
+// shared memory per CTA: two CTAs per SM up to 128 threads, one above
+constexpr size_t kSmemCap = THREADS >= 256 ? 220 * 1024 : 110 * 1024;
 constexpr int RF = 13;             // row fields: J base 6, J limb 3, aref, D, x, y
 constexpr int NS = DK_PHYS_NSENSOR;
 #ifndef DK_PHYS_SYNC_LEVEL
@@ -1306,15 +1308,42 @@ size_t phys_smem_bytes(const PhysConst<T> &pc, int threads) {
            (size_t)pc.rows_per_lane * RF * threads * sizeof(T);
 }
 
+// SM count of the current device (148 on B200), queried once per device
+inline int phys_sm_count() {
+    static int cached[64] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (dev < 0 || dev >= 64) return 148;
+    if (!cached[dev]) {
+        int v = 0;
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        cached[dev] = v > 0 ? v : 148;
+    }
+    return cached[dev];
+}
+
+// Threads per CTA for n worlds: one CTA per SM per wave (the registers of a
+// 256-thread CTA fill the SM), as few waves as 64-world CTAs need, the worlds
+// spread evenly over them -- 8192 worlds: 148 SMs x 56 worlds (224 threads)
+// instead of 128 x 64 with 20 SMs idle.  One CTA per SM also keeps all of an
+// SM's warps under the same phase barriers (measured: 256-thread CTAs 16%
+// faster than two 128-thread CTAs per SM at 8192 worlds, 26% at 65536).
+// Halved while the constraint rows do not fit the shared-memory cap.
+template <class SmemFn>
+inline int pick_threads(int64_t n, SmemFn smem_bytes) {
+    const int64_t sms = phys_sm_count();
+    const int64_t waves = (n + sms * WPC - 1) / (sms * WPC);
+    const int64_t wpc = (n + sms * waves - 1) / (sms * waves);
+    int threads = (int)((wpc * QUAD + 31) / 32 * 32);
+    threads = threads < 32 ? 32 : (threads > THREADS ? THREADS : threads);
+    while (threads > 32 && smem_bytes(threads) > kSmemCap) threads = (threads / 2 + 31) / 32 * 32;
+    return threads;
+}
+
 template <typename T>
 cudaError_t launch_phys(const PhysConst<T> &pc, const PhysArgs<T> &a, const PhysInspect<T> &ins,
                         cudaStream_t st) {
-    // 128 threads (32 worlds) per CTA unless the constraint rows of that many
-    // lanes would not fit two CTAs' worth of shared memory on an SM (measured:
-    // 32-thread CTAs run the physics kernel at the same speed and the fused
-    // env kernel 30% slower -- its per-CTA row stores get narrower)
-    int threads = DK_PHYS_CTA_THREADS;
-    while (threads > 32 && phys_smem_bytes(pc, threads) > 110 * 1024) threads /= 2;
+    const int threads = pick_threads(a.n, [&](int t) { return phys_smem_bytes(pc, t); });
     const size_t smem = phys_smem_bytes(pc, threads);
     static size_t attr = 0;
     if (smem > attr) {
