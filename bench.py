@@ -564,7 +564,7 @@ def measure_go1_e2e(env, args, dev, dist, world):
     import torch
 
     n, K = env.num_envs, args.e2e_steps
-    U = min(args.unroll, K)
+    U = min(args.unroll, K, 10)  # short chunks: the pipeline fills / drains faster
     pin = lambda *s, d=env.dtype: torch.empty(s, dtype=d, pin_memory=True)  # noqa: E731
     acts_h = pin(K, n, 12)
     acts_h.copy_(torch.rand((K, n, 12), dtype=env.dtype) * 2 - 1)
@@ -573,17 +573,38 @@ def measure_go1_e2e(env, args, dev, dist, world):
     dev_out = [env.outputs(U, with_terminal=False) for _ in range(2)]
     dev_act = [torch.empty((U, n, 12), dtype=env.dtype, device=dev) for _ in range(2)]
 
+    # Pipelined like a serving loop: chunk c+1's actions go up on one copy stream
+    # and chunk c's outputs come down on another while chunk c+1 computes (two
+    # device buffer sets; events guard their reuse).
+    main = torch.cuda.current_stream(dev)
+    up, down = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    ev_done, ev_copied = [None, None], [None, None]
+
     def run(k0, k1, slot):
         k = k1 - k0
         a = dev_act[slot][:k]
-        a.copy_(acts_h[k0:k1], non_blocking=True)
+        with torch.cuda.stream(up):
+            if ev_done[slot] is not None:
+                up.wait_event(ev_done[slot])  # the slot's previous rollout has read its actions
+            a.copy_(acts_h[k0:k1], non_blocking=True)
+            ev_up = torch.cuda.Event()
+            ev_up.record(up)
+        main.wait_event(ev_up)
+        if ev_copied[slot] is not None:
+            main.wait_event(ev_copied[slot])  # the slot's previous outputs are on the host
         o = {kk: (v[:k] if v is not None else None) for kk, v in dev_out[slot].items()}
         env.rollout(a, out=o)
-        obs_h[k0:k1].copy_(o["obs"], non_blocking=True)
-        priv_h[k0:k1].copy_(o["privileged_state"], non_blocking=True)
-        rew_h[k0:k1].copy_(o["reward"], non_blocking=True)
-        done_h[k0:k1].copy_(o["done"], non_blocking=True)
-        trunc_h[k0:k1].copy_(o["trunc"], non_blocking=True)
+        ev_done[slot] = torch.cuda.Event()
+        ev_done[slot].record(main)
+        with torch.cuda.stream(down):
+            down.wait_event(ev_done[slot])
+            obs_h[k0:k1].copy_(o["obs"], non_blocking=True)
+            priv_h[k0:k1].copy_(o["privileged_state"], non_blocking=True)
+            rew_h[k0:k1].copy_(o["reward"], non_blocking=True)
+            done_h[k0:k1].copy_(o["done"], non_blocking=True)
+            trunc_h[k0:k1].copy_(o["trunc"], non_blocking=True)
+            ev_copied[slot] = torch.cuda.Event()
+            ev_copied[slot].record(down)
 
     run(0, min(U, K), 0)
     torch.cuda.synchronize(dev)
@@ -604,7 +625,8 @@ def measure_go1_e2e(env, args, dev, dist, world):
             "h2d_bytes_per_step": n * 12 * esz,
             "d2h_bytes_per_step": n * ((56 + 75 + 1) * esz + 2),
             "api": "paper_2502_08844_b200.go1env.DeviceGo1Env.rollout with pinned host "
-                   "actions in and obs / privileged obs / reward / done / trunc out",
+                   "actions in and obs / privileged obs / reward / done / trunc out; "
+                   "copies on two copy streams overlapping the next chunk's rollout",
             "steps": K, "chunk_steps": U}
 
 
