@@ -119,7 +119,7 @@ dk::EnvScalars scalars(const dk_env *e, int autoreset) {
     sc.action_repeat = (int32_t)e->cfg.action_repeat;
     sc.wide_init = e->cfg.wide_init;
     sc.autoreset = autoreset ? 1 : 0;
-    sc.reserved0 = 0;
+    sc.solo_sm = 0;
     sc.reserved1 = 0;
     return sc;
 }

@@ -69,6 +69,8 @@ inline cudaError_t launch_task_rollout_tl(const T *actions, int64_t K, const Env
     // (and its CTAs' set-up) with the previous rollout's drain; the kernel
     // waits (griddepcontrol.wait) before touching anything the previous grid
     // wrote, and each CTA releases its dependents once its producer is done.
+    EnvScalars scl = sc;
+    scl.solo_sm = grid <= sm_count() ? 1 : 0;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)grid);
     cfg.blockDim = dim3(S::THREADS);
@@ -79,7 +81,7 @@ inline cudaError_t launch_task_rollout_tl(const T *actions, int64_t K, const Env
     attr[0].val.programmaticStreamSerializationAllowed = kUsePdl ? 1 : 0;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, kern, actions, K, sc, p, w, out, err);
+    return cudaLaunchKernelEx(&cfg, kern, actions, K, scl, p, w, out, err);
 }
 
 template <class Task, typename T>
