@@ -90,6 +90,34 @@ def test_go1_env_f64_matches_oracle(G, geoms):
     env.close()
 
 
+def test_go1_env_f64_multiwarp_ctas(G):
+    """A world count whose CTAs span several warps (the step's CTA barriers are
+    active) with a partial last CTA (no barriers there): 2003 worlds -> 126 CTAs
+    of 16 worlds / 64 threads, the last one with 3 worlds."""
+    from oracle.go1env import OracleGo1Env
+    from paper_2502_08844_b200 import physmodel as pm
+
+    n, K = 2003, 4
+    cfg = _cfg(G)
+    env = G.DeviceGo1Env(n, cfg, dtype="float64")
+    ref = OracleGo1Env(pm.go1_model(), cfg.oracle_dict(), n)
+    o = env.reset(seed=8)
+    r_obs, _ = ref.reset(seed=8)
+    assert _rel(o["state"].cpu().numpy(), r_obs, 1e-3) < 1e-12
+    acts = np.random.default_rng(4).uniform(-1.3, 1.3, (K, n, 12))
+    out = env.rollout(torch.as_tensor(acts, device="cuda"))
+    env.check()
+    for k in range(K):
+        r = ref.step(acts[k])
+        np.testing.assert_array_equal(out["done"][k].cpu().numpy().astype(bool), r["done"])
+        assert _rel(out["reward"][k].cpu().numpy(), r["reward"], 1e-3) < 1e-9, k
+        assert _rel(out["obs"][k].cpu().numpy(), r["obs"], 1e-3) < 1e-9, k
+    s = env.state()
+    assert _rel(s["qpos"].cpu().numpy(), ref.qpos, 1e-3) < 1e-9
+    assert _rel(s["qvel"].cpu().numpy(), ref.qvel, 1e-3) < 1e-9
+    env.close()
+
+
 def test_go1_env_f32_first_steps(G):
     from oracle.go1env import OracleGo1Env
     from paper_2502_08844_b200 import physmodel as pm
