@@ -293,6 +293,39 @@ int dk_dr_curriculum(int64_t n, int64_t *state, const uint8_t *success, int64_t 
 int dk_ppo_sample(int64_t n, int action_dim, const float *mean, const float *log_std,
                   int64_t log_std_stride, const float *eps, float *pre_tanh, float *action,
                   float *log_prob, int *nan_flag, void *stream);
+/* The per-step bookkeeping of ppo.collect_rollout (ppo.py:295-378) around the
+ * policy call, the env step and the value call, float32 observations / float64
+ * batch fields, each value computed as the reference's separate ops do.
+ * dk_ppo_norm: a RunningNormalizer's device statistics for normalizer_apply
+ * (mathcore.py:254-262: clip((x - mean) / sqrt(var + eps), -10, 10); copy = 1
+ * while count == 0; present = 0: no normaliser, the identity). */
+typedef struct {
+    const double *mean, *var;
+    double epsilon;
+    int32_t copy, present;
+} dk_ppo_norm;
+/* obs_p [n, dp] / obs_v [n, dv] -> raw copies raw_p / raw_v (nullable), the
+ * normalised policy input pol [n, dp], the normalised value input val [n, dv]
+ * and its copy val2 (nullable; e.g. the first half of the value call's input). */
+int dk_ppo_step_inputs(int64_t n, int dp, int dv, const float *obs_p, const float *obs_v,
+                       const dk_ppo_norm *norm_p, const dk_ppo_norm *norm_v, float *raw_p,
+                       float *raw_v, float *pol, float *val, float *val2, void *stream);
+/* after the env step: boot = trunc & ~done & terminal_mask (the truncation
+ * bootstrap, ppo.py:327-341), val_term [n, dv] = normalised (boot ? terminal_obs
+ * : 0), dones [n] = float64(done | trunc). */
+int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
+                          const uint8_t *terminal_mask, const float *terminal_obs,
+                          const dk_ppo_norm *norm_v, float *val_term, uint8_t *boot,
+                          double *dones, void *stream);
+/* after the value call on [value inputs; terminal inputs] (values2 [2n]):
+ * rewards_out = reward * reward_scaling + discounting * (boot ? values2[n + i] : 0),
+ * values_out = values2[:n], actions_out = float64(action) [n, action_dim], and
+ * reward_partial[dk_ppo_record_blocks(n)] = float64 reward sums per block. */
+int64_t dk_ppo_record_blocks(int64_t n);
+int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const uint8_t *boot,
+                       const float *values2, const float *action, double reward_scaling,
+                       double discounting, double *rewards_out, double *values_out,
+                       double *actions_out, double *reward_partial, void *stream);
 int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
                const void *values, const void *dones, const void *bootstrap, double gamma,
                double lam, void *advantages, void *returns, void *stream);

@@ -53,6 +53,12 @@ FRAME_FIELDS = ("base_orientation", "base_lin_vel", "base_ang_vel", "joint_pos",
                 "joint_nominal", "joint_default", "done")
 
 
+class PpoNormC(ctypes.Structure):
+    """dk_ppo_norm (include/deskrl_b200.h)"""
+    _fields_ = [("mean", ctypes.c_void_p), ("var", ctypes.c_void_p), ("epsilon", ctypes.c_double),
+                ("copy", ctypes.c_int32), ("present", ctypes.c_int32)]
+
+
 class RewardConfigC(ctypes.Structure):
     _fields_ = [(f, ctypes.c_double) for f in REWARD_FIELDS] + [
         ("standstill_gated", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -170,6 +176,13 @@ _SIGS = {
                                      _vp, _vp]),
     "dk_ppo_gae": (ctypes.c_int, [ctypes.c_int, _i64, _i64, _vp, _vp, _vp, _vp, ctypes.c_double,
                                   ctypes.c_double, _vp, _vp, _vp]),
+    "dk_ppo_step_inputs": (ctypes.c_int, [_i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp,
+                                          _vp, _vp, _vp, _vp, _vp, _vp]),
+    "dk_ppo_step_bootstrap": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
+                                             _vp, _vp, _vp]),
+    "dk_ppo_record_blocks": (_i64, [_i64]),
+    "dk_ppo_step_record": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_double,
+                                          ctypes.c_double, _vp, _vp, _vp, _vp, _vp]),
     "dk_norm_update": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,
                                       _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dk_norm_workspace_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int]),

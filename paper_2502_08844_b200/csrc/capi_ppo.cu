@@ -108,6 +108,88 @@ __global__ void ppo_sample_kernel(int64_t n, int A, const float *mean, const flo
     if (bad) atomicOr(nan_flag, 1);
 }
 
+// ---------------------------------------------------------------------------
+// The per-step bookkeeping of collect_rollout (ppo.py:295-378) in three
+// kernels around the policy call, the env step and the value call (the torch
+// version was ~25 small elementwise / copy / reduction launches per step).
+// Every value is computed exactly as the separate torch ops did: normaliser
+// apply in float64 (norm_apply_kernel's expression), conversions to float64,
+// the reward target reward * scale + discount * term_value with two roundings.
+
+__device__ __forceinline__ float norm_f32(float x, const dk_ppo_norm &nm, int j) {
+    if (!nm.present || nm.copy) return x;
+    const double sd = __dsqrt_rn(__dadd_rn(nm.var[j], nm.epsilon));
+    double y = __ddiv_rn(__dsub_rn((double)x, nm.mean[j]), sd);
+    y = y < -10.0 ? -10.0 : (y > 10.0 ? 10.0 : y);  // np.clip (NaN passes through)
+    return (float)y;
+}
+
+// obs_p [n, dp] / obs_v [n, dv] -> raw copies (nullable), the normalised policy
+// input pol [n, dp], the value input val [n, dv] and its copy val2 (nullable)
+__global__ void ppo_inputs_kernel(int64_t n, int dp, int dv, const float *obs_p,
+                                  const float *obs_v, dk_ppo_norm np_, dk_ppo_norm nv_,
+                                  float *raw_p, float *raw_v, float *pol, float *val, float *val2) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t tp = n * dp;
+    if (e < tp) {
+        const float x = obs_p[e];
+        if (raw_p) raw_p[e] = x;
+        pol[e] = norm_f32(x, np_, (int)(e % dp));
+    }
+    if (e < n * dv) {
+        const float x = obs_v[e];
+        if (raw_v) raw_v[e] = x;
+        const float y = norm_f32(x, nv_, (int)(e % dv));
+        val[e] = y;
+        if (val2) val2[e] = y;
+    }
+}
+
+// after the env step: boot = trunc & ~done & terminal_mask (ppo.py:327-341),
+// val_term = norm_v(boot ? terminal_obs : 0), dones = float64(done | trunc)
+__global__ void ppo_bootstrap_kernel(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
+                                     const uint8_t *tmask, const float *term_obs,
+                                     dk_ppo_norm nv_, float *val_term, uint8_t *boot,
+                                     double *dones) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= n * dv) return;
+    const int64_t i = e / dv;
+    const int j = (int)(e - i * dv);
+    const bool b = trunc[i] && !done[i] && tmask[i];
+    val_term[e] = norm_f32(b ? term_obs[e] : 0.0f, nv_, j);
+    if (j == 0) {
+        boot[i] = b ? 1 : 0;
+        dones[i] = (done[i] || trunc[i]) ? 1.0 : 0.0;
+    }
+}
+
+// after the value call on [inputs; terminal obs] (v2 [2n]): the reward target,
+// the value, the float64 action, and per-block float64 reward sums (summed in
+// a fixed order by the caller: deterministic)
+constexpr int kRecordThreads = 256;
+__global__ void __launch_bounds__(kRecordThreads)
+ppo_record_kernel(int64_t n, int A, const float *reward, const uint8_t *boot, const float *v2,
+                  const float *action, double scale, double discount, double *rew_out,
+                  double *val_out, double *act_out, double *reward_partial) {
+    __shared__ double red[kRecordThreads];
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double r = 0.0;
+    if (i < n) {
+        r = (double)reward[i];
+        const double tv = boot[i] ? (double)v2[n + i] : 0.0;
+        rew_out[i] = __dadd_rn(__dmul_rn(r, scale), __dmul_rn(discount, tv));
+        val_out[i] = (double)v2[i];
+        for (int a = 0; a < A; ++a) act_out[i * A + a] = (double)action[i * A + a];
+    }
+    red[threadIdx.x] = r;
+    __syncthreads();
+    for (int s = kRecordThreads / 2; s > 0; s >>= 1) {
+        if ((int)threadIdx.x < s) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) reward_partial[blockIdx.x] = red[0];
+}
+
 extern "C" {
 
 int dk_ppo_sample(int64_t n, int action_dim, const float *mean, const float *log_std,
@@ -227,6 +309,55 @@ int dk_norm_apply(int dtype, int64_t rows, int dim, const void *batch, double co
         dk::norm_apply_kernel<float><<<blocks(total, 256), 256, 0, st>>>(
             total, dim, (const float *)batch, mean, var, epsilon, copy, invert, (float *)out);
     return cuda_rc(cudaGetLastError(), "normalizer apply launch");
+}
+
+
+int dk_ppo_step_inputs(int64_t n, int dp, int dv, const float *obs_p, const float *obs_v,
+                       const dk_ppo_norm *norm_p, const dk_ppo_norm *norm_v, float *raw_p,
+                       float *raw_v, float *pol, float *val, float *val2, void *stream) {
+    dk::PtrDeviceGuard dg_(obs_p);
+    if (n < 0 || dp < 1 || dv < 1 || !obs_p || !obs_v || !pol || !val)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_inputs: bad arguments");
+    if (n == 0) return DK_OK;
+    dk_ppo_norm off = {};
+    const int64_t tot = n * (dp > dv ? dp : dv);
+    ppo_inputs_kernel<<<blocks(tot, 256), 256, 0, (cudaStream_t)stream>>>(
+        n, dp, dv, obs_p, obs_v, norm_p ? *norm_p : off, norm_v ? *norm_v : off, raw_p, raw_v, pol,
+        val, val2);
+    return cuda_rc(cudaGetLastError(), "dk_ppo_step_inputs launch");
+}
+
+int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
+                          const uint8_t *terminal_mask, const float *terminal_obs,
+                          const dk_ppo_norm *norm_v, float *val_term, uint8_t *boot,
+                          double *dones, void *stream) {
+    dk::PtrDeviceGuard dg_(done);
+    if (n < 0 || dv < 1 || !done || !trunc || !terminal_mask || !terminal_obs || !val_term ||
+        !boot || !dones)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_bootstrap: bad arguments");
+    if (n == 0) return DK_OK;
+    dk_ppo_norm off = {};
+    ppo_bootstrap_kernel<<<blocks(n * dv, 256), 256, 0, (cudaStream_t)stream>>>(
+        n, dv, done, trunc, terminal_mask, terminal_obs, norm_v ? *norm_v : off, val_term, boot,
+        dones);
+    return cuda_rc(cudaGetLastError(), "dk_ppo_step_bootstrap launch");
+}
+
+int64_t dk_ppo_record_blocks(int64_t n) { return (n + kRecordThreads - 1) / kRecordThreads; }
+
+int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const uint8_t *boot,
+                       const float *values2, const float *action, double reward_scaling,
+                       double discounting, double *rewards_out, double *values_out,
+                       double *actions_out, double *reward_partial, void *stream) {
+    dk::PtrDeviceGuard dg_(reward);
+    if (n < 0 || action_dim < 1 || !reward || !boot || !values2 || !action || !rewards_out ||
+        !values_out || !actions_out || !reward_partial)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_record: bad arguments");
+    if (n == 0) return DK_OK;
+    ppo_record_kernel<<<blocks(n, kRecordThreads), kRecordThreads, 0, (cudaStream_t)stream>>>(
+        n, action_dim, reward, boot, values2, action, reward_scaling, discounting, rewards_out,
+        values_out, actions_out, reward_partial);
+    return cuda_rc(cudaGetLastError(), "dk_ppo_step_record launch");
 }
 
 }  // extern "C"

@@ -20,8 +20,10 @@ reference's CPU ``torch.randn`` draws, for parity tests) or a CUDA generator.
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
+from . import _native as nat
 from .envkit import ConfigError, _check
 
 
@@ -154,20 +156,22 @@ def tanh_gaussian_log_prob(mean, log_std, pre_tanh):
     return (base - correction).sum(-1)
 
 
-def _sample(mean, log_std, eps, nan_flag):
+def _sample(mean, log_std, eps, nan_flag, out=None):
     """policy_forward's sampling + tanh_gaussian_log_prob (ppo.py:204-217): one
     fused kernel (dk_ppo_sample) for float32 networks, else the torch
-    expressions; NaN means set nan_flag."""
+    expressions; NaN means set nan_flag.  out: optional (pre_tanh, action,
+    log_prob) float32 buffers to write."""
     import torch
 
     if (mean.dtype == torch.float32 and eps.dtype == torch.float32 and mean.dim() == 2
             and log_std.dtype == torch.float32 and log_std.stride(-1) == 1):
-        from . import _native as nat
-
         m, e = mean.contiguous(), eps.contiguous()
         n, A = m.shape
-        pre, act = torch.empty_like(m), torch.empty_like(m)
-        lp = torch.empty((n,), dtype=torch.float32, device=m.device)
+        if out is not None:
+            pre, act, lp = out
+        else:
+            pre, act = torch.empty_like(m), torch.empty_like(m)
+            lp = torch.empty((n,), dtype=torch.float32, device=m.device)
         _check(nat.lib().dk_ppo_sample(n, A, m.data_ptr(), log_std.data_ptr(), log_std.stride(0),
                                        e.data_ptr(), pre.data_ptr(), act.data_ptr(),
                                        lp.data_ptr(), nan_flag.data_ptr(),
@@ -175,7 +179,12 @@ def _sample(mean, log_std, eps, nan_flag):
         return pre, act, lp
     nan_flag |= torch.isnan(mean).any().to(nan_flag.dtype)
     pre_tanh = mean + torch.exp(log_std) * eps
-    return pre_tanh, torch.tanh(pre_tanh), tanh_gaussian_log_prob(mean, log_std, pre_tanh)
+    res = pre_tanh, torch.tanh(pre_tanh), tanh_gaussian_log_prob(mean, log_std, pre_tanh)
+    if out is not None:
+        for o, r in zip(out, res):
+            o.copy_(r)
+        return out
+    return res
 
 
 def _route(obs: dict, cfg):
@@ -224,6 +233,10 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
         if pixel_policy:  # NCHW view of an NHWC (channels_last) tensor: 2x faster cuDNN convs
             return pixel_normalize(x, channels_first=False).permute(0, 3, 1, 2)
         return prep(policy_normalizer, x)
+
+    if not pixel_policy and _fused_ok(env, obs, cfg, policy_normalizer, value_normalizer):
+        return _collect_fused(env, policy, value, cfg, obs, policy_normalizer, value_normalizer,
+                              noise, generator, update_normalizers, nan_flag, out)
 
     with torch.no_grad():
         for t in range(T):
@@ -276,6 +289,101 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
     if update_normalizers:
         _update(batch, policy_normalizer, value_normalizer)
     return batch, obs, raw_reward_sum / T
+
+
+def _fused_ok(env, obs, cfg, pn, vn):
+    """The fused bookkeeping path (dk_ppo_step_*) takes float32 state
+    observations and device normalisers (or none)."""
+    import torch
+
+    from .ppo import DeviceRunningNormalizer
+
+    if env.dtype != torch.float32:
+        return False
+    for key in (cfg.policy_obs_key, cfg.value_obs_key):
+        x = obs.get(key)
+        if x is None or x.dtype != torch.float32 or x.dim() != 2:
+            return False
+    return all(n is None or isinstance(n, DeviceRunningNormalizer) for n in (pn, vn))
+
+
+def _norm_c(normalizer):
+    if normalizer is None:
+        return nat.PpoNormC(None, None, 0.0, 0, 0)
+    return nat.PpoNormC(normalizer.mean.data_ptr(), normalizer.var.data_ptr(),
+                        float(normalizer.epsilon), int(normalizer.count == 0.0), 1)
+
+
+def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, update_normalizers,
+                   nan_flag, out):
+    """collect_rollout_device with the per-step bookkeeping in three kernels
+    (dk_ppo_step_inputs / _bootstrap / _record) writing straight into the
+    phase's [T, N, ...] batch buffers: eight launches per control step (inputs,
+    policy, noise, sampling, env step, bootstrap, value, record) instead of ~30.
+    Same values as the op-by-op path (tests/test_gpu_rollout.py)."""
+    import torch
+
+    T, N = int(cfg.unroll_length), env.num_envs
+    dev = env.device
+    lib = nat.lib()
+    st = lambda: torch.cuda.current_stream(dev).cuda_stream  # noqa: E731
+    f32, f64 = torch.float32, torch.float64
+    pol_in, val_in = _route(obs, cfg)
+    dp, dv, A = pol_in.shape[1], val_in.shape[1], env.action_dim
+    e = lambda *s_, d=f32: torch.empty(s_, dtype=d, device=dev)  # noqa: E731
+    p_obs, v_obs = e(T, N, dp), e(T, N, dv)
+    raw_p = e(T, N, dp) if pn is not None else None
+    raw_v = e(T, N, dv) if vn is not None else None
+    acts, pres, lps = e(T, N, A, d=f64), e(T, N, A), e(T, N)
+    rews, dns, vals = e(T, N, d=f64), e(T, N, d=f64), e(T, N, d=f64)
+    vin = e(2 * N, dv)  # the value call's rows: this step's inputs, then the terminal obs
+    boot = torch.empty((N,), dtype=torch.uint8, device=dev)
+    act = e(N, A)
+    nb = int(lib.dk_ppo_record_blocks(N))
+    partial = e(T, nb, d=f64)
+    np_c, nv_c = _norm_c(pn), _norm_c(vn)
+    ptr = lambda x: None if x is None else x.data_ptr()  # noqa: E731
+    with torch.no_grad():
+        for t in range(T):
+            pol_in, val_in = _route(obs, cfg)
+            pol_in, val_in = pol_in.contiguous(), val_in.contiguous()
+            _check(lib.dk_ppo_step_inputs(
+                N, dp, dv, pol_in.data_ptr(), val_in.data_ptr(), ctypes.byref(np_c),
+                ctypes.byref(nv_c), ptr(None if raw_p is None else raw_p[t]),
+                ptr(None if raw_v is None else raw_v[t]), p_obs[t].data_ptr(), v_obs[t].data_ptr(),
+                vin.data_ptr(), st()))
+            mean, log_std = policy(p_obs[t])
+            eps = noise[t].to(mean.dtype) if noise is not None else torch.randn(
+                mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
+            _sample(mean, log_std, eps, nan_flag, out=(pres[t], act, lps[t]))
+            step = env.step(act, autoreset=True, with_info=False, out=out)
+            _check(lib.dk_ppo_step_bootstrap(
+                N, dv, step["done"].data_ptr(), step["trunc"].data_ptr(),
+                step["terminal_mask"].data_ptr(), step["terminal_obs"].data_ptr(),
+                ctypes.byref(nv_c), vin[N:].data_ptr(), boot.data_ptr(), dns[t].data_ptr(), st()))
+            vv = value(vin)
+            if vv.dtype != f32 or not vv.is_contiguous():
+                vv = vv.to(f32).contiguous()
+            _check(lib.dk_ppo_step_record(
+                N, A, step["reward"].data_ptr(), boot.data_ptr(), vv.data_ptr(), act.data_ptr(),
+                float(cfg.reward_scaling), float(cfg.discounting), rews[t].data_ptr(),
+                vals[t].data_ptr(), acts[t].data_ptr(), partial[t].data_ptr(), st()))
+            nxt = step["obs"]  # read by the next step's inputs kernel before the env overwrites it
+            obs = {"state": nxt, "privileged_state": nxt}
+        nxt = obs["state"].clone()
+        obs = {"state": nxt, "privileged_state": nxt}
+        _, val_in = _route(obs, cfg)
+        bootstrap = value(vn.apply(val_in).to(f32) if vn is not None else val_in).to(f64)
+    batch = DeviceRolloutBatch(p_obs, v_obs, acts, pres, lps, rews, dns, vals, bootstrap)
+    batch.raw_policy_obs = raw_p.reshape(T * N, dp) if raw_p is not None else None
+    batch.raw_value_obs = raw_v.reshape(T * N, dv) if raw_v is not None else None
+    batch.nan_flag = nan_flag
+    if not torch.cuda.is_current_stream_capturing():
+        _check_phase(env, batch)
+    if update_normalizers:
+        _update(batch, pn, vn)
+    mean_reward = (partial.sum(1) / N).sum() / T
+    return batch, obs, mean_reward
 
 
 def _check_phase(env, batch):
