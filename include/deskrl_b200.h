@@ -311,21 +311,25 @@ int dk_ppo_step_inputs(int64_t n, int dp, int dv, const float *obs_p, const floa
                        const dk_ppo_norm *norm_p, const dk_ppo_norm *norm_v, float *raw_p,
                        float *raw_v, float *pol, float *val, float *val2, void *stream);
 /* after the env step: boot = trunc & ~done & terminal_mask (the truncation
- * bootstrap, ppo.py:327-341), val_term [n, dv] = normalised (boot ? terminal_obs
- * : 0), dones [n] = float64(done | trunc). */
+ * bootstrap, ppo.py:327-341), dones [n] = float64(done | trunc), and the boot
+ * rows' normalised terminal observations compacted into val_term[0, *count)
+ * (pos[i] = the row's slot, -1 for the other rows, whose bootstrap term is 0):
+ * the value of the terminal observations is needed for those rows only. */
 int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
                           const uint8_t *terminal_mask, const float *terminal_obs,
-                          const dk_ppo_norm *norm_v, float *val_term, uint8_t *boot,
-                          double *dones, void *stream);
-/* after the value call on [value inputs; terminal inputs] (values2 [2n]):
- * rewards_out = reward * reward_scaling + discounting * (boot ? values2[n + i] : 0),
- * values_out = values2[:n], actions_out = float64(action) [n, action_dim], and
+                          const dk_ppo_norm *norm_v, float *val_term, int64_t *count,
+                          int32_t *pos, double *dones, void *stream);
+/* after the value calls (values [n] of the step's inputs, term_values[pos[i]]
+ * of the compacted terminal rows): rewards_out = reward * reward_scaling +
+ * discounting * (pos[i] >= 0 ? term_values[pos[i]] : 0), values_out =
+ * float64(values), actions_out = float64(action) [n, action_dim], and
  * reward_partial[dk_ppo_record_blocks(n)] = float64 reward sums per block. */
 int64_t dk_ppo_record_blocks(int64_t n);
-int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const uint8_t *boot,
-                       const float *values2, const float *action, double reward_scaling,
-                       double discounting, double *rewards_out, double *values_out,
-                       double *actions_out, double *reward_partial, void *stream);
+int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const int32_t *pos,
+                       const float *values, const float *term_values, const float *action,
+                       double reward_scaling, double discounting, double *rewards_out,
+                       double *values_out, double *actions_out, double *reward_partial,
+                       void *stream);
 int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
                const void *values, const void *dones, const void *bootstrap, double gamma,
                double lam, void *advantages, void *returns, void *stream);
@@ -584,6 +588,11 @@ int dk_mlp_pack(const float *w, int n, int k, void *w_hi, void *w_lo, void *stre
 int dk_mlp_forward(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride, float *y,
                    int64_t y_stride, void *stream);
 /* developer hook: desc_swap = 1 swaps the descriptors' LBO / SBO (layout check) */
+/* the same forward with the row count read on the device (*rows_dev <=
+ * max_rows; e.g. a count produced by an earlier kernel on the stream). */
+int dk_mlp_forward_count(const dk_mlp *net, int64_t max_rows, const int64_t *rows_dev,
+                         const float *x, int64_t x_stride, float *y, int64_t y_stride,
+                         void *stream);
 int dk_mlp_forward_dbg(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride,
                        float *y, int64_t y_stride, int desc_swap, void *stream);
 

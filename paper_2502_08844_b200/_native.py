@@ -115,6 +115,7 @@ _SIGS = {
     "dk_mlp_pack": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp]),
     "dk_mlp_forward": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "dk_mlp_forward_dbg": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, ctypes.c_int, _vp]),
+    "dk_mlp_forward_count": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
     "dk_last_error": (ctypes.c_char_p, []),
     "dk_task_id": (ctypes.c_int, [ctypes.c_char_p]),
     "dk_task_dims": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),
@@ -179,10 +180,11 @@ _SIGS = {
     "dk_ppo_step_inputs": (ctypes.c_int, [_i64, ctypes.c_int, ctypes.c_int, _vp, _vp, _vp, _vp,
                                           _vp, _vp, _vp, _vp, _vp, _vp]),
     "dk_ppo_step_bootstrap": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
-                                             _vp, _vp, _vp]),
+                                             _vp, _vp, _vp, _vp]),
     "dk_ppo_record_blocks": (_i64, [_i64]),
-    "dk_ppo_step_record": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, ctypes.c_double,
-                                          ctypes.c_double, _vp, _vp, _vp, _vp, _vp]),
+    "dk_ppo_step_record": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
+                                          ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp,
+                                          _vp]),
     "dk_norm_update": (ctypes.c_int, [ctypes.c_int, _i64, ctypes.c_int, _vp, ctypes.c_double,
                                       _vp, _vp, _vp, ctypes.c_size_t, _vp]),
     "dk_norm_workspace_bytes": (ctypes.c_size_t, [_i64, ctypes.c_int]),

@@ -31,8 +31,28 @@ int dk_mlp_pack(const float *w, int n, int k, void *w_hi, void *w_lo, void *stre
     return cuda_rc(cudaGetLastError(), "dk_mlp_pack");
 }
 
+namespace {
+int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const float *x,
+                int64_t x_stride, float *y, int64_t y_stride, int desc_swap, void *stream);
+}
+
 int dk_mlp_forward_dbg(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride,
                        float *y, int64_t y_stride, int desc_swap, void *stream) {
+    return mlp_forward(net, rows, nullptr, x, x_stride, y, y_stride, desc_swap, stream);
+}
+
+int dk_mlp_forward_count(const dk_mlp *net, int64_t max_rows, const int64_t *rows_dev,
+                         const float *x, int64_t x_stride, float *y, int64_t y_stride,
+                         void *stream) {
+    if (!rows_dev) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward_count: null");
+    return mlp_forward(net, max_rows, rows_dev, x, x_stride, y, y_stride, 0, stream);
+}
+
+}  // extern "C"
+
+namespace {
+int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const float *x,
+                int64_t x_stride, float *y, int64_t y_stride, int desc_swap, void *stream) {
     if (!net || !x || !y) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward: null");
     dk::PtrDeviceGuard dg_(x);
     const int H = net->hidden;
@@ -60,6 +80,7 @@ int dk_mlp_forward_dbg(const dk_mlp *net, int64_t rows, const float *x, int64_t 
     a.y = y;
     a.y_stride = y_stride;
     a.desc_swap = desc_swap;
+    a.rows_dev = rows_dev;
     const size_t smem = dk::mlp::mlp_smem_bytes(H, net->d_in, net->n_tc, net->n_out);
     if (smem > 227 * 1024)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward: network too large");
@@ -75,6 +96,9 @@ int dk_mlp_forward_dbg(const dk_mlp *net, int64_t rows, const float *x, int64_t 
     dk::mlp::mlp_tc_kernel<<<grid, dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(a);
     return cuda_rc(cudaGetLastError(), "mlp_tc_kernel");
 }
+}  // namespace
+
+extern "C" {
 
 int dk_mlp_forward(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride, float *y,
                    int64_t y_stride, void *stream) {

@@ -146,39 +146,47 @@ __global__ void ppo_inputs_kernel(int64_t n, int dp, int dv, const float *obs_p,
 }
 
 // after the env step: boot = trunc & ~done & terminal_mask (ppo.py:327-341),
-// val_term = norm_v(boot ? terminal_obs : 0), dones = float64(done | trunc)
+// dones = float64(done | trunc), and the boot rows' normalised terminal
+// observations compacted into val_term[0, *count) (pos[i] = the row's slot, -1
+// if not a boot row).  Only those rows need a value: every other world's
+// bootstrap term is masked to 0, so the value call runs on *count rows instead
+// of n (a truncation is one step in episode_length).  The slot order follows
+// the atomics; each world's value does not depend on it (rows are independent).
 __global__ void ppo_bootstrap_kernel(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
                                      const uint8_t *tmask, const float *term_obs,
-                                     dk_ppo_norm nv_, float *val_term, uint8_t *boot,
-                                     double *dones) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= n * dv) return;
-    const int64_t i = e / dv;
-    const int j = (int)(e - i * dv);
+                                     dk_ppo_norm nv_, float *val_term, int64_t *count,
+                                     int32_t *pos, double *dones) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
     const bool b = trunc[i] && !done[i] && tmask[i];
-    val_term[e] = norm_f32(b ? term_obs[e] : 0.0f, nv_, j);
-    if (j == 0) {
-        boot[i] = b ? 1 : 0;
-        dones[i] = (done[i] || trunc[i]) ? 1.0 : 0.0;
+    dones[i] = (done[i] || trunc[i]) ? 1.0 : 0.0;
+    int32_t slot = -1;
+    if (b) {
+        slot = (int32_t)atomicAdd(reinterpret_cast<unsigned long long *>(count), 1ull);
+        for (int j = 0; j < dv; ++j)
+            val_term[(int64_t)slot * dv + j] = norm_f32(term_obs[i * dv + j], nv_, j);
     }
+    pos[i] = slot;
 }
 
-// after the value call on [inputs; terminal obs] (v2 [2n]): the reward target,
-// the value, the float64 action, and per-block float64 reward sums (summed in
-// a fixed order by the caller: deterministic)
+// after the value calls (values [n] of the step's inputs, term_values[pos[i]]
+// of the boot rows' terminal observations): the reward target, the value, the
+// float64 action, and per-block float64 reward sums (summed in a fixed order by
+// the caller: deterministic)
 constexpr int kRecordThreads = 256;
 __global__ void __launch_bounds__(kRecordThreads)
-ppo_record_kernel(int64_t n, int A, const float *reward, const uint8_t *boot, const float *v2,
-                  const float *action, double scale, double discount, double *rew_out,
-                  double *val_out, double *act_out, double *reward_partial) {
+ppo_record_kernel(int64_t n, int A, const float *reward, const int32_t *pos, const float *values,
+                  const float *term_values, const float *action, double scale, double discount,
+                  double *rew_out, double *val_out, double *act_out, double *reward_partial) {
     __shared__ double red[kRecordThreads];
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     double r = 0.0;
     if (i < n) {
         r = (double)reward[i];
-        const double tv = boot[i] ? (double)v2[n + i] : 0.0;
+        const int32_t p = pos[i];
+        const double tv = p >= 0 ? (double)term_values[p] : 0.0;
         rew_out[i] = __dadd_rn(__dmul_rn(r, scale), __dmul_rn(discount, tv));
-        val_out[i] = (double)v2[i];
+        val_out[i] = (double)values[i];
         for (int a = 0; a < A; ++a) act_out[i * A + a] = (double)action[i * A + a];
     }
     red[threadIdx.x] = r;
@@ -329,35 +337,38 @@ int dk_ppo_step_inputs(int64_t n, int dp, int dv, const float *obs_p, const floa
 
 int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
                           const uint8_t *terminal_mask, const float *terminal_obs,
-                          const dk_ppo_norm *norm_v, float *val_term, uint8_t *boot,
-                          double *dones, void *stream) {
+                          const dk_ppo_norm *norm_v, float *val_term, int64_t *count,
+                          int32_t *pos, double *dones, void *stream) {
     dk::PtrDeviceGuard dg_(done);
     if (n < 0 || dv < 1 || !done || !trunc || !terminal_mask || !terminal_obs || !val_term ||
-        !boot || !dones)
+        !count || !pos || !dones)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_bootstrap: bad arguments");
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int64_t), st);
+    if (e != cudaSuccess) return cuda_rc(e, "dk_ppo_step_bootstrap count");
     if (n == 0) return DK_OK;
     dk_ppo_norm off = {};
-    ppo_bootstrap_kernel<<<blocks(n * dv, 256), 256, 0, (cudaStream_t)stream>>>(
-        n, dv, done, trunc, terminal_mask, terminal_obs, norm_v ? *norm_v : off, val_term, boot,
-        dones);
+    ppo_bootstrap_kernel<<<blocks(n, 256), 256, 0, st>>>(n, dv, done, trunc, terminal_mask,
+                                                         terminal_obs, norm_v ? *norm_v : off,
+                                                         val_term, count, pos, dones);
     return cuda_rc(cudaGetLastError(), "dk_ppo_step_bootstrap launch");
 }
 
 int64_t dk_ppo_record_blocks(int64_t n) { return (n + kRecordThreads - 1) / kRecordThreads; }
 
-int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const uint8_t *boot,
-                       const float *values2, const float *action, double reward_scaling,
-                       double discounting, double *rewards_out, double *values_out,
-                       double *actions_out, double *reward_partial, void *stream) {
+int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const int32_t *pos,
+                       const float *values, const float *term_values, const float *action,
+                       double reward_scaling, double discounting, double *rewards_out,
+                       double *values_out, double *actions_out, double *reward_partial,
+                       void *stream) {
     dk::PtrDeviceGuard dg_(reward);
-    if (n < 0 || action_dim < 1 || !reward || !boot || !values2 || !action || !rewards_out ||
-        !values_out || !actions_out || !reward_partial)
+    if (n < 0 || action_dim < 1 || !reward || !pos || !values || !term_values || !action ||
+        !rewards_out || !values_out || !actions_out || !reward_partial)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_record: bad arguments");
     if (n == 0) return DK_OK;
     ppo_record_kernel<<<blocks(n, kRecordThreads), kRecordThreads, 0, (cudaStream_t)stream>>>(
-        n, action_dim, reward, boot, values2, action, reward_scaling, discounting, rewards_out,
-        values_out, actions_out, reward_partial);
+        n, action_dim, reward, pos, values, term_values, action, reward_scaling, discounting,
+        rewards_out, values_out, actions_out, reward_partial);
     return cuda_rc(cudaGetLastError(), "dk_ppo_step_record launch");
 }
-
 }  // extern "C"

@@ -43,6 +43,8 @@ struct MlpArgs {
     float *y;                         // [rows][y_stride]
     int64_t y_stride;
     int desc_swap;                    // debug: swap LBO / SBO
+    const int64_t *rows_dev;          // nullable: the row count, read on the device
+                                      // (<= rows; tiles past it exit at once)
 };
 
 // ------------------------------------------------------------------ PTX glue
@@ -189,6 +191,11 @@ __global__ void pack_weights_kernel(const float *w, int N, int K, __nv_bfloat16 
 
 __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    if (a.rows_dev) {  // a device-side row count (e.g. the compacted bootstrap rows)
+        const int64_t rd = *a.rows_dev;
+        a.rows = rd < a.rows ? rd : a.rows;
+        if ((int64_t)blockIdx.x * M >= a.rows) return;  // the whole CTA: uniform
+    }
     const int H = a.H, din = a.d_in, nout = a.n_out;
     const uint32_t a_bytes = (uint32_t)M * H * 2;           // one of A_hi / A_lo
     const uint32_t b_chunk = (uint32_t)H * KC * 2;          // one B chunk (hi or lo)

@@ -120,6 +120,22 @@ class TensorCoreMLP:
                                             self.desc_swap, stream))
         return y.reshape(*x.shape[:-1], self.n_out)
 
+    def forward_count(self, x, count):
+        """Rows [0, *count) of x [R, d_in] (count: a 1-element int64 CUDA tensor
+        written by an earlier kernel on the stream); y [R, n_out], rows past the
+        count untouched."""
+        torch = self._torch
+        self._pack()
+        if x.dtype != torch.float32 or x.stride(-1) != 1 or x.dim() != 2:
+            raise ConfigError("forward_count: x must be a 2-D float32 row-major tensor")
+        rows = x.shape[0]
+        y = torch.empty((rows, self.n_out), dtype=torch.float32, device=x.device)
+        stream = ctypes.c_void_p(torch.cuda.current_stream(x.device).cuda_stream)
+        _check(self._lib.dk_mlp_forward_count(ctypes.byref(self._net), rows, count.data_ptr(),
+                                              x.data_ptr(), x.stride(0), y.data_ptr(),
+                                              y.stride(0), stream))
+        return y
+
 
 class _TCPolicy:
     """MLPPolicy.forward on the tensor cores: (mean, log_std.expand_as(mean))."""
@@ -146,6 +162,10 @@ class _TCValue:
 
     def __call__(self, obs):
         return self.mlp(obs).squeeze(-1)
+
+    def call_count(self, obs, count):
+        """values of rows [0, *count) of obs (device-side count)"""
+        return self.mlp.forward_count(obs, count).squeeze(-1)
 
     def parameters(self):
         return self.module.parameters()

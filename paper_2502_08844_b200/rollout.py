@@ -336,8 +336,12 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     raw_v = e(T, N, dv) if vn is not None else None
     acts, pres, lps = e(T, N, A, d=f64), e(T, N, A), e(T, N)
     rews, dns, vals = e(T, N, d=f64), e(T, N, d=f64), e(T, N, d=f64)
-    vin = e(2 * N, dv)  # the value call's rows: this step's inputs, then the terminal obs
-    boot = torch.empty((N,), dtype=torch.uint8, device=dev)
+    vin = e(N, dv)  # the value call's rows: this step's normalised inputs
+    # the boot rows' terminal observations, compacted (count on the device)
+    vterm = torch.zeros((N, dv), dtype=f32, device=dev)
+    count = torch.zeros((1,), dtype=torch.int64, device=dev)
+    pos = torch.empty((N,), dtype=torch.int32, device=dev)
+    value_count = getattr(value, "call_count", None)
     act = e(N, A)
     nb = int(lib.dk_ppo_record_blocks(N))
     partial = e(T, nb, d=f64)
@@ -360,14 +364,19 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
             _check(lib.dk_ppo_step_bootstrap(
                 N, dv, step["done"].data_ptr(), step["trunc"].data_ptr(),
                 step["terminal_mask"].data_ptr(), step["terminal_obs"].data_ptr(),
-                ctypes.byref(nv_c), vin[N:].data_ptr(), boot.data_ptr(), dns[t].data_ptr(), st()))
-            vv = value(vin)
-            if vv.dtype != f32 or not vv.is_contiguous():
-                vv = vv.to(f32).contiguous()
+                ctypes.byref(nv_c), vterm.data_ptr(), count.data_ptr(), pos.data_ptr(),
+                dns[t].data_ptr(), st()))
+            v = value(vin)
+            # terminal values: the compacted boot rows only (tensor-core MLP with a
+            # device-side row count), else the whole buffer (rows past the count unread)
+            vt = value_count(vterm, count) if value_count is not None else value(vterm)
+            v, vt = (x if x.dtype == f32 and x.is_contiguous() else x.to(f32).contiguous()
+                     for x in (v, vt))
             _check(lib.dk_ppo_step_record(
-                N, A, step["reward"].data_ptr(), boot.data_ptr(), vv.data_ptr(), act.data_ptr(),
-                float(cfg.reward_scaling), float(cfg.discounting), rews[t].data_ptr(),
-                vals[t].data_ptr(), acts[t].data_ptr(), partial[t].data_ptr(), st()))
+                N, A, step["reward"].data_ptr(), pos.data_ptr(), v.data_ptr(), vt.data_ptr(),
+                act.data_ptr(), float(cfg.reward_scaling), float(cfg.discounting),
+                rews[t].data_ptr(), vals[t].data_ptr(), acts[t].data_ptr(),
+                partial[t].data_ptr(), st()))
             nxt = step["obs"]  # read by the next step's inputs kernel before the env overwrites it
             obs = {"state": nxt, "privileged_state": nxt}
         nxt = obs["state"].clone()
