@@ -588,6 +588,12 @@ int dk_mlp_pack(const float *w, int n, int k, void *w_hi, void *w_lo, void *stre
 int dk_mlp_forward(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride, float *y,
                    int64_t y_stride, void *stream);
 /* developer hook: desc_swap = 1 swaps the descriptors' LBO / SBO (layout check) */
+/* two networks in one launch (their row tiles share the GPU: e.g. the PPO
+ * policy and value on the same observations), each as dk_mlp_forward. */
+int dk_mlp_forward_pair(const dk_mlp *net0, int64_t rows0, const float *x0, int64_t x0_stride,
+                        float *y0, int64_t y0_stride, const dk_mlp *net1, int64_t rows1,
+                        const float *x1, int64_t x1_stride, float *y1, int64_t y1_stride,
+                        void *stream);
 /* the same forward with the row count read on the device (*rows_dev <=
  * max_rows; e.g. a count produced by an earlier kernel on the stream). */
 int dk_mlp_forward_count(const dk_mlp *net, int64_t max_rows, const int64_t *rows_dev,

@@ -116,6 +116,8 @@ _SIGS = {
     "dk_mlp_forward": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp]),
     "dk_mlp_forward_dbg": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, ctypes.c_int, _vp]),
     "dk_mlp_forward_count": (ctypes.c_int, [_vp, _i64, _vp, _vp, _i64, _vp, _i64, _vp]),
+    "dk_mlp_forward_pair": (ctypes.c_int, [_vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _vp, _i64,
+                                           _vp, _i64, _vp]),
     "dk_last_error": (ctypes.c_char_p, []),
     "dk_task_id": (ctypes.c_int, [ctypes.c_char_p]),
     "dk_task_dims": (ctypes.c_int, [ctypes.c_int, ctypes.POINTER(ctypes.c_int),

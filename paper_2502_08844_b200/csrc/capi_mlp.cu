@@ -17,52 +17,18 @@ int cuda_rc(cudaError_t e, const char *what) {
 }
 }  // namespace
 
-extern "C" {
-
-int dk_mlp_pack(const float *w, int n, int k, void *w_hi, void *w_lo, void *stream) {
-    dk::PtrDeviceGuard dg_(w);
-    if (!w || !w_hi || !w_lo) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_pack: null");
-    if (n <= 0 || k <= 0 || n % 8 || k % dk::mlp::KC)
-        return dk_internal_fail(DK_ERR_INVALID_INPUT,
-                                "dk_mlp_pack: n must be a multiple of 8 and k of 32");
-    const int total = n * k;
-    dk::mlp::pack_weights_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
-        w, n, k, (__nv_bfloat16 *)w_hi, (__nv_bfloat16 *)w_lo);
-    return cuda_rc(cudaGetLastError(), "dk_mlp_pack");
-}
-
 namespace {
-int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const float *x,
-                int64_t x_stride, float *y, int64_t y_stride, int desc_swap, void *stream);
-}
-
-int dk_mlp_forward_dbg(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride,
-                       float *y, int64_t y_stride, int desc_swap, void *stream) {
-    return mlp_forward(net, rows, nullptr, x, x_stride, y, y_stride, desc_swap, stream);
-}
-
-int dk_mlp_forward_count(const dk_mlp *net, int64_t max_rows, const int64_t *rows_dev,
-                         const float *x, int64_t x_stride, float *y, int64_t y_stride,
-                         void *stream) {
-    if (!rows_dev) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward_count: null");
-    return mlp_forward(net, max_rows, rows_dev, x, x_stride, y, y_stride, 0, stream);
-}
-
-}  // extern "C"
-
-namespace {
-int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const float *x,
-                int64_t x_stride, float *y, int64_t y_stride, int desc_swap, void *stream) {
+// validated kernel arguments of one network call (DK_OK or an error code)
+int mlp_args(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const float *x,
+             int64_t x_stride, float *y, int64_t y_stride, int desc_swap, dk::mlp::MlpArgs &a,
+             size_t &smem) {
     if (!net || !x || !y) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward: null");
-    dk::PtrDeviceGuard dg_(x);
     const int H = net->hidden;
     if (!(H == 128 || H == 256) || net->d_in < 1 || net->d_in > 16 || net->n_out < 1 ||
         net->n_out > 4 || net->n_tc < 1)
         return dk_internal_fail(DK_ERR_INVALID_INPUT,
                                 "dk_mlp_forward: hidden must be 128 or 256, d_in <= 16, "
                                 "1 <= n_out <= 4, at least one hidden x hidden layer");
-    if (rows <= 0) return DK_OK;
-    dk::mlp::MlpArgs a;
     a.x = x;
     a.rows = rows;
     a.x_stride = x_stride;
@@ -81,9 +47,17 @@ int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const 
     a.y_stride = y_stride;
     a.desc_swap = desc_swap;
     a.rows_dev = rows_dev;
-    const size_t smem = dk::mlp::mlp_smem_bytes(H, net->d_in, net->n_tc, net->n_out);
+    smem = dk::mlp::mlp_smem_bytes(H, net->d_in, net->n_tc, net->n_out);
     if (smem > 227 * 1024)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward: network too large");
+    return DK_OK;
+}
+
+int64_t tiles(int64_t rows) { return rows > 0 ? (rows + dk::mlp::M - 1) / dk::mlp::M : 0; }
+
+int mlp_launch(const dk::mlp::MlpArgs &a0, int64_t t0, const dk::mlp::MlpArgs &a1, int64_t t1,
+               size_t smem, void *stream) {
+    if (t0 + t1 == 0) return DK_OK;
     static size_t attr = 0;
     if (smem > attr) {
         cudaError_t e = cudaFuncSetAttribute(dk::mlp::mlp_tc_kernel,
@@ -92,17 +66,68 @@ int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const 
         if (e != cudaSuccess) return cuda_rc(e, "dk_mlp_forward attribute");
         attr = smem;
     }
-    const unsigned grid = (unsigned)((rows + dk::mlp::M - 1) / dk::mlp::M);
-    dk::mlp::mlp_tc_kernel<<<grid, dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(a);
+    dk::mlp::mlp_tc_kernel<<<(unsigned)(t0 + t1), dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(
+        a0, a1, t0);
     return cuda_rc(cudaGetLastError(), "mlp_tc_kernel");
+}
+
+int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const float *x,
+                int64_t x_stride, float *y, int64_t y_stride, int desc_swap, void *stream) {
+    if (!x) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward: null");
+    dk::PtrDeviceGuard dg_(x);
+    dk::mlp::MlpArgs a;
+    size_t smem = 0;
+    const int rc = mlp_args(net, rows, rows_dev, x, x_stride, y, y_stride, desc_swap, a, smem);
+    if (rc != DK_OK) return rc;
+    if (rows <= 0) return DK_OK;
+    return mlp_launch(a, tiles(rows), a, 0, smem, stream);
 }
 }  // namespace
 
 extern "C" {
 
+int dk_mlp_pack(const float *w, int n, int k, void *w_hi, void *w_lo, void *stream) {
+    dk::PtrDeviceGuard dg_(w);
+    if (!w || !w_hi || !w_lo) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_pack: null");
+    if (n <= 0 || k <= 0 || n % 8 || k % dk::mlp::KC)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT,
+                                "dk_mlp_pack: n must be a multiple of 8 and k of 32");
+    const int total = n * k;
+    dk::mlp::pack_weights_kernel<<<(total + 255) / 256, 256, 0, (cudaStream_t)stream>>>(
+        w, n, k, (__nv_bfloat16 *)w_hi, (__nv_bfloat16 *)w_lo);
+    return cuda_rc(cudaGetLastError(), "dk_mlp_pack");
+}
+
+int dk_mlp_forward_dbg(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride,
+                       float *y, int64_t y_stride, int desc_swap, void *stream) {
+    return mlp_forward(net, rows, nullptr, x, x_stride, y, y_stride, desc_swap, stream);
+}
+
+int dk_mlp_forward_count(const dk_mlp *net, int64_t max_rows, const int64_t *rows_dev,
+                         const float *x, int64_t x_stride, float *y, int64_t y_stride,
+                         void *stream) {
+    if (!rows_dev) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward_count: null");
+    return mlp_forward(net, max_rows, rows_dev, x, x_stride, y, y_stride, 0, stream);
+}
+
 int dk_mlp_forward(const dk_mlp *net, int64_t rows, const float *x, int64_t x_stride, float *y,
                    int64_t y_stride, void *stream) {
     return dk_mlp_forward_dbg(net, rows, x, x_stride, y, y_stride, 0, stream);
+}
+
+int dk_mlp_forward_pair(const dk_mlp *net0, int64_t rows0, const float *x0, int64_t x0_stride,
+                        float *y0, int64_t y0_stride, const dk_mlp *net1, int64_t rows1,
+                        const float *x1, int64_t x1_stride, float *y1, int64_t y1_stride,
+                        void *stream) {
+    if (!x0 || !x1) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward_pair: null");
+    dk::PtrDeviceGuard dg_(x0);
+    dk::mlp::MlpArgs a0, a1;
+    size_t s0 = 0, s1 = 0;
+    int rc = mlp_args(net0, rows0, nullptr, x0, x0_stride, y0, y0_stride, 0, a0, s0);
+    if (rc != DK_OK) return rc;
+    rc = mlp_args(net1, rows1, nullptr, x1, x1_stride, y1, y1_stride, 0, a1, s1);
+    if (rc != DK_OK) return rc;
+    return mlp_launch(a0, tiles(rows0), a1, tiles(rows1), s0 > s1 ? s0 : s1, stream);
 }
 
 }  // extern "C"

@@ -189,12 +189,20 @@ __global__ void pack_weights_kernel(const float *w, int N, int K, __nv_bfloat16 
     lo[e] = l;
 }
 
-__global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a) {
+// One launch may evaluate two networks (e.g. the PPO policy on this step's
+// observations and the value function on the same observations): CTAs
+// [0, tiles0) take network a0, the rest a1 -- the two calls' latency-bound
+// tiles then share the GPU instead of running back to back.
+__global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs a1,
+                                                            int64_t tiles0) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    const bool second = (int64_t)blockIdx.x >= tiles0;
+    MlpArgs a = second ? a1 : a0;
+    const int64_t tile = second ? (int64_t)blockIdx.x - tiles0 : (int64_t)blockIdx.x;
     if (a.rows_dev) {  // a device-side row count (e.g. the compacted bootstrap rows)
         const int64_t rd = *a.rows_dev;
         a.rows = rd < a.rows ? rd : a.rows;
-        if ((int64_t)blockIdx.x * M >= a.rows) return;  // the whole CTA: uniform
+        if (tile * M >= a.rows) return;  // the whole CTA: uniform
     }
     const int H = a.H, din = a.d_in, nout = a.n_out;
     const uint32_t a_bytes = (uint32_t)M * H * 2;           // one of A_hi / A_lo
@@ -213,7 +221,7 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a) {
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int q = warp & 3, quarter = warp >> 2;            // TMEM lane group, column quarter
     const int row = 32 * q + lane;
-    const int64_t r_glob = (int64_t)blockIdx.x * M + row;
+    const int64_t r_glob = tile * M + row;
     const int HQ = H / 4;                                    // columns per thread (32 or 64)
 
     for (int i = tid; i < H * din; i += THREADS) s_w0[i] = a.w0[i];

@@ -137,6 +137,26 @@ class TensorCoreMLP:
         return y
 
 
+def forward_pair(m0, x0, m1, x1):
+    """Two TensorCoreMLP forwards in one launch (dk_mlp_forward_pair): the
+    networks' row tiles run side by side.  x0 / x1: 2-D float32 row-major CUDA
+    tensors on one device.  Returns (y0, y1)."""
+    torch = m0._torch
+    m0._pack()
+    m1._pack()
+    for x in (x0, x1):
+        if x.dtype != torch.float32 or x.dim() != 2 or x.stride(-1) != 1:
+            raise ConfigError("forward_pair: inputs must be 2-D float32 row-major tensors")
+    y0 = torch.empty((x0.shape[0], m0.n_out), dtype=torch.float32, device=x0.device)
+    y1 = torch.empty((x1.shape[0], m1.n_out), dtype=torch.float32, device=x1.device)
+    stream = ctypes.c_void_p(torch.cuda.current_stream(x0.device).cuda_stream)
+    _check(m0._lib.dk_mlp_forward_pair(
+        ctypes.byref(m0._net), x0.shape[0], x0.data_ptr(), x0.stride(0), y0.data_ptr(),
+        y0.stride(0), ctypes.byref(m1._net), x1.shape[0], x1.data_ptr(), x1.stride(0),
+        y1.data_ptr(), y1.stride(0), stream))
+    return y0, y1
+
+
 class _TCPolicy:
     """MLPPolicy.forward on the tensor cores: (mean, log_std.expand_as(mean))."""
 
@@ -181,4 +201,4 @@ def tc_value(value):
     return _TCValue(value) if hasattr(value, "trunk") and supported(value.trunk) else value
 
 
-__all__ = ["TensorCoreMLP", "supported", "tc_policy", "tc_value"]
+__all__ = ["TensorCoreMLP", "forward_pair", "supported", "tc_policy", "tc_value"]

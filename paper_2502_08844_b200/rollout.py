@@ -342,6 +342,9 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     count = torch.zeros((1,), dtype=torch.int64, device=dev)
     pos = torch.empty((N,), dtype=torch.int32, device=dev)
     value_count = getattr(value, "call_count", None)
+    from .mlp import _TCPolicy, _TCValue, forward_pair
+
+    pair = isinstance(policy, _TCPolicy) and isinstance(value, _TCValue)
     act = e(N, A)
     nb = int(lib.dk_ppo_record_blocks(N))
     partial = e(T, nb, d=f64)
@@ -356,7 +359,12 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
                 ctypes.byref(nv_c), ptr(None if raw_p is None else raw_p[t]),
                 ptr(None if raw_v is None else raw_v[t]), p_obs[t].data_ptr(), v_obs[t].data_ptr(),
                 vin.data_ptr(), st()))
-            mean, log_std = policy(p_obs[t])
+            if pair:  # policy and value of this step's observations in one launch
+                mean, v = forward_pair(policy.mlp, p_obs[t], value.mlp, vin)
+                log_std = policy.module.log_std.expand_as(mean)
+                v = v.squeeze(-1)
+            else:
+                mean, log_std = policy(p_obs[t])
             eps = noise[t].to(mean.dtype) if noise is not None else torch.randn(
                 mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
             _sample(mean, log_std, eps, nan_flag, out=(pres[t], act, lps[t]))
@@ -366,7 +374,8 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
                 step["terminal_mask"].data_ptr(), step["terminal_obs"].data_ptr(),
                 ctypes.byref(nv_c), vterm.data_ptr(), count.data_ptr(), pos.data_ptr(),
                 dns[t].data_ptr(), st()))
-            v = value(vin)
+            if not pair:
+                v = value(vin)
             # terminal values: the compacted boot rows only (tensor-core MLP with a
             # device-side row count), else the whole buffer (rows past the count unread)
             vt = value_count(vterm, count) if value_count is not None else value(vterm)

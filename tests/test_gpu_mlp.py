@@ -70,3 +70,21 @@ def test_tc_mlp_layout_check(M):
     bad = M.TensorCoreMLP(net.trunk, desc_swap=1)(x).squeeze(-1)
     assert _err(good, ref) < 2e-5
     assert _err(bad, ref) > 1e-3
+
+
+def test_tc_mlp_pair_launch_equals_separate_calls(M):
+    """dk_mlp_forward_pair (the PPO policy and value in one launch) gives
+    bit-identical outputs to the two separate forwards; the count-limited
+    forward (device-side row count) matches on its rows."""
+    from paper_2502_08844_b200 import rollout as R
+
+    torch.manual_seed(3)
+    pol, val = R.make_policy(5, 1).cuda(), R.make_value(5).cuda()
+    tp, tv = M.tc_policy(pol), M.tc_value(val)
+    xp, xv = torch.randn(1000, 5, device="cuda"), torch.randn(777, 5, device="cuda")
+    yp, yv = M.forward_pair(tp.mlp, xp, tv.mlp, xv)
+    torch.testing.assert_close(yp, tp.mlp(xp), rtol=0, atol=0)
+    torch.testing.assert_close(yv, tv.mlp(xv), rtol=0, atol=0)
+    count = torch.tensor([300], dtype=torch.int64, device="cuda")
+    yc = tv.call_count(xv, count)
+    torch.testing.assert_close(yc[:300], tv(xv)[:300], rtol=0, atol=0)
