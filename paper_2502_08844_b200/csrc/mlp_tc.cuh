@@ -21,6 +21,7 @@
 // the output layer's four partial sums per row are added in quarter order.
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -28,7 +29,11 @@ namespace dk {
 namespace mlp {
 
 constexpr int M = 128;          // rows per CTA (= TMEM lanes)
-constexpr int THREADS = 512;    // 16 warps: warp w -> TMEM lanes 32 (w % 4), column quarter w / 4
+constexpr int EPI_WARPS = 16;   // warp w < 16 -> TMEM lanes 32 (w % 4), column quarter w / 4
+constexpr int THREADS = 32 * (EPI_WARPS + 1);  // + warp 16: weight copies and MMA issue
+constexpr int MAXCH = 8;        // K chunks of a hidden layer (H / KC)
+// layer 0's padded input width: 4, 8 or 16 columns
+__host__ __device__ constexpr int din_pad(int d_in) { return d_in <= 4 ? 4 : (d_in <= 8 ? 8 : 16); }
 constexpr int KC = 32;          // K columns per chunk
 constexpr int MAXH = 256;
 
@@ -189,6 +194,15 @@ __global__ void pack_weights_kernel(const float *w, int N, int K, __nv_bfloat16 
     lo[e] = l;
 }
 
+// Warp-specialised and pipelined across layers: warp 16 streams the weights and
+// issues the MMAs; warps 0-15 run layer 0 and the epilogues.  Two TMEM
+// accumulators alternate between layers, and the activations of layer l + 1
+// are handed to the MMA warp K-chunk by K-chunk (an mbarrier per 32-column
+// chunk): layer l + 1's MMAs start on the first chunks while layer l's
+// epilogue is still producing the rest, and the first hidden layer's MMAs
+// overlap layer 0.  (The serial MMA -> epilogue -> MMA chain was most of a
+// call: r02 A/B.)
+//
 // One launch may evaluate two networks (e.g. the PPO policy on this step's
 // observations and the value function on the same observations): CTAs
 // [0, tiles0) take network a0, the rest a1 -- the two calls' latency-bound
@@ -205,16 +219,22 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
         if (tile * M >= a.rows) return;  // the whole CTA: uniform
     }
     const int H = a.H, din = a.d_in, nout = a.n_out;
+    const int nch = H / KC;
     const uint32_t a_bytes = (uint32_t)M * H * 2;           // one of A_hi / A_lo
     const uint32_t b_chunk = (uint32_t)H * KC * 2;          // one B chunk (hi or lo)
     unsigned char *A_hi = smem;
     unsigned char *A_lo = smem + a_bytes;
     unsigned char *Bst = smem + 2 * a_bytes;                // [2 stages][hi, lo][b_chunk]
-    uint64_t *bars = reinterpret_cast<uint64_t *>(Bst + 4 * b_chunk);  // full[2], empty[2], done
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 5);
+    // full[2] empty[2] (weight ring), done[2] (accumulator of layer l: done[l & 1]),
+    // achunk[MAXCH] (K chunk c of the current layer's input written)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(Bst + 4 * b_chunk);
+    uint64_t *full = bars, *empty = bars + 2, *done = bars + 4, *achunk = bars + 6;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6 + MAXCH);
     // the float32 parameters used on the CUDA cores, staged once
-    float *s_w0 = reinterpret_cast<float *>(bars + 6);      // [H][din]
-    float *s_b0 = s_w0 + H * din;                            // [H]
+    // layer 0's weight rows padded to DP columns (zeros past d_in) for 16-byte loads
+    const int DP = din_pad(din);
+    float *s_w0 = reinterpret_cast<float *>(bars + 8 + MAXCH);  // [H][DP]
+    float *s_b0 = s_w0 + H * DP;                             // [H]
     float *s_bh = s_b0 + H;                                  // [n_tc][H]
     float *s_wo = s_bh + a.n_tc * H;                         // [nout][H]
     float *s_red = s_wo + nout * H;                          // [4 quarters][M][4] partial outputs
@@ -223,147 +243,181 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
     const int row = 32 * q + lane;
     const int64_t r_glob = tile * M + row;
     const int HQ = H / 4;                                    // columns per thread (32 or 64)
+    const uint32_t tcols = 2u * (uint32_t)H;                 // two accumulators
 
-    for (int i = tid; i < H * din; i += THREADS) s_w0[i] = a.w0[i];
+    for (int i = tid; i < H * DP; i += THREADS) {
+        const int j = i / DP, k = i - j * DP;
+        s_w0[i] = k < din ? a.w0[j * din + k] : 0.0f;
+    }
     for (int i = tid; i < H; i += THREADS) s_b0[i] = a.b0[i];
     for (int i = tid; i < a.n_tc * H; i += THREADS) s_bh[i] = a.bh[i];
     for (int i = tid; i < nout * H; i += THREADS) s_wo[i] = a.wout[i];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
                          smem_u32(tmem_slot)),
-                     "r"(256));
+                     "r"(tcols));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
-        for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
+        for (int c = 0; c < MAXCH; ++c) mbar_init(&achunk[c], 4);  // the 4 warps of a quarter
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // K chunks are consumed in the order the epilogue finishes them: each column
+    // quarter writes its chunks in turn, so the first of every quarter comes first
+    const int cpq = nch / 4;                                 // chunks per quarter (1 or 2)
+    auto kchunk = [&](int i) { return (i % 4) * cpq + i / 4; };
 
-    // ---- layer 0 on the CUDA cores (float32): this thread's row, its column quarter
-    {
-        float x[16];
+    if (warp == EPI_WARPS) {
+        // ---------------------------------------------- weights and MMA issue
+        if (lane == 0) {
+            const uint32_t total = (uint32_t)(a.n_tc * nch);
+            auto load = [&](uint32_t gg) {
+                const int s = gg & 1;
+                const int ll = (int)(gg / nch), c = kchunk((int)(gg % nch));
+                if (gg >= 2) mbar_wait(&empty[s], ((gg - 2) >> 1) & 1);  // stage free
+                mbar_expect_tx(&full[s], 2 * b_chunk);
+                const size_t off = (size_t)ll * H * H + (size_t)c * H * KC;
+                bulk_g2s(Bst + (2 * s) * b_chunk, a.whi + off, b_chunk, &full[s]);
+                bulk_g2s(Bst + (2 * s + 1) * b_chunk, a.wlo + off, b_chunk, &full[s]);
+            };
+            load(0);
+            const uint32_t idesc = instr_desc_bf16(M, H);
+            const uint32_t lbo = a.desc_swap ? 512u : 128u, sbo = a.desc_swap ? 128u : 512u;
+            for (int l = 0; l < a.n_tc; ++l) {
+                const uint32_t tacc = tmem + (uint32_t)((l & 1) * H);
+                for (int i = 0; i < nch; ++i) {
+                    const int c = kchunk(i);
+                    const uint32_t gc = (uint32_t)(l * nch + i);
+                    const int s = gc & 1;
+                    mbar_wait(&achunk[c], l & 1);   // this layer's input, K chunk c
+                    mbar_wait(&full[s], (gc >> 1) & 1);  // its weights
+                    tc_fence_after();
+                    const uint32_t a_hi = smem_u32(A_hi) + c * (M * KC * 2);
+                    const uint32_t a_lo = smem_u32(A_lo) + c * (M * KC * 2);
+                    const uint32_t b_hi = smem_u32(Bst + (2 * s) * b_chunk);
+                    const uint32_t b_lo = smem_u32(Bst + (2 * s + 1) * b_chunk);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-            x[i] = (i < din && r_glob < a.rows) ? a.x[r_glob * a.x_stride + i] : 0.0f;
-        for (int j0 = quarter * HQ; j0 < (quarter + 1) * HQ; j0 += 8) {
-            float v[8];
-#pragma unroll
-            for (int jj = 0; jj < 8; ++jj) {
-                const int j = j0 + jj;
-                float s = s_b0[j];
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (i < din) s = fmaf(s_w0[j * din + i], x[i], s);
-                v[jj] = r_glob < a.rows ? silu(s) : 0.0f;
+                    for (int ks = 0; ks < KC / 16; ++ks) {
+                        const uint32_t o = ks * 256;  // two core matrices along K
+                        const uint64_t dah = smem_desc(a_hi + o, lbo, sbo);
+                        const uint64_t dal = smem_desc(a_lo + o, lbo, sbo);
+                        const uint64_t dbh = smem_desc(b_hi + o, lbo, sbo);
+                        const uint64_t dbl = smem_desc(b_lo + o, lbo, sbo);
+                        mma_bf16(tacc, dah, dbh, idesc, (i | ks) != 0);
+                        mma_bf16(tacc, dah, dbl, idesc, 1);
+                        mma_bf16(tacc, dal, dbh, idesc, 1);
+                    }
+                    mma_commit(&empty[s]);  // stage s free once these MMAs complete
+                    if (i + 1 == nch) mma_commit(&done[l & 1]);  // layer l's accumulator final
+                    // the next weight chunk after this chunk's MMAs are queued (its
+                    // stage-free wait is on the previous chunk's MMAs)
+                    if (gc + 1 < total) load(gc + 1);
+                }
             }
-            store_split8(A_hi, A_lo, row, j0, v);
         }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ layer 0 and epilogues
+        // hand K chunk c of the next layer's input to the MMA warp: stores
+        // visible to the tensor core (async proxy), TMEM reads ordered before
+        auto publish = [&](int c) {
+            fence_async_smem();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
+                                            smem_u32(&achunk[c]))
+                                        : "memory");
+        };
+        // layer 0 on the CUDA cores (float32): this thread's row, its column quarter;
+        // padded weight rows read 16 bytes at a time (the padding adds exact zeros)
+        auto layer0 = [&](auto dp_c) {
+            constexpr int DPC = decltype(dp_c)::value;
+            float x[DPC];
+#pragma unroll
+            for (int i = 0; i < DPC; ++i)
+                x[i] = (i < din && r_glob < a.rows) ? a.x[r_glob * a.x_stride + i] : 0.0f;
+            for (int j0 = quarter * HQ; j0 < (quarter + 1) * HQ; j0 += 8) {
+                float v[8];
+#pragma unroll
+                for (int jj = 0; jj < 8; ++jj) {
+                    const int j = j0 + jj;
+                    float s = s_b0[j];
+                    const float4 *w = reinterpret_cast<const float4 *>(s_w0 + j * DPC);
+#pragma unroll
+                    for (int i4 = 0; i4 < DPC / 4; ++i4) {
+                        const float4 q4 = w[i4];
+                        s = fmaf(q4.x, x[4 * i4], s);
+                        s = fmaf(q4.y, x[4 * i4 + 1], s);
+                        s = fmaf(q4.z, x[4 * i4 + 2], s);
+                        s = fmaf(q4.w, x[4 * i4 + 3], s);
+                    }
+                    v[jj] = r_glob < a.rows ? silu(s) : 0.0f;
+                }
+                store_split8(A_hi, A_lo, row, j0, v);
+                if ((j0 + 8) % KC == 0) publish(j0 / KC);
+            }
+        };
+        if (DP == 4) layer0(std::integral_constant<int, 4>{});
+        else if (DP == 8) layer0(std::integral_constant<int, 8>{});
+        else layer0(std::integral_constant<int, 16>{});
+        float out_acc[4] = {0.f, 0.f, 0.f, 0.f};
+        for (int l = 0; l < a.n_tc; ++l) {
+            mbar_wait(&done[l & 1], (l >> 1) & 1);
+            tc_fence_after();
+            // ---- epilogue (this thread's row and column quarter): bias, SiLU; split
+            // into the next layer's input, or partial output-layer dot products
+            const bool last = l + 1 == a.n_tc;
+            const float *bias = s_bh + (size_t)l * H;
+            const uint32_t tacc = tmem + (uint32_t)((l & 1) * H);
+            for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
+                float v[32];
+                tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + cc * 32, v);
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = silu(v[i] + bias[cc * 32 + i]);
+                if (last) {
+#pragma unroll
+                    for (int o = 0; o < 4; ++o) {
+                        if (o < nout) {
+                            const float *wr = s_wo + (size_t)o * H + cc * 32;
+                            float s = out_acc[o];
+#pragma unroll
+                            for (int i = 0; i < 32; ++i) s = fmaf(wr[i], v[i], s);
+                            out_acc[o] = s;
+                        }
+                    }
+                } else {
+#pragma unroll
+                    for (int k8 = 0; k8 < 4; ++k8)
+                        store_split8(A_hi, A_lo, row, cc * 32 + k8 * 8, v + 8 * k8);
+                    publish(cc);
+                }
+            }
+        }
+        // output layer: the four column quarters' partial sums, in quarter order
+#pragma unroll
+        for (int o = 0; o < 4; ++o) s_red[(quarter * M + row) * 4 + o] = out_acc[o];
     }
-    fence_async_smem();
     tc_fence_before();
     __syncthreads();
-    tc_fence_after();
-
-    const uint32_t idesc = instr_desc_bf16(M, H);
-    const int nch = H / KC;
-    const uint32_t lbo = a.desc_swap ? 512u : 128u, sbo = a.desc_swap ? 128u : 512u;
-    float out_acc[4] = {0.f, 0.f, 0.f, 0.f};
-    uint32_t g = 0;  // global chunk counter (stage = g & 1) across layers
-
-    for (int l = 0; l < a.n_tc; ++l) {
-        const __nv_bfloat16 *whi = a.whi + (size_t)l * H * H, *wlo = a.wlo + (size_t)l * H * H;
-        if (tid == 0) {
-            auto load = [&](uint32_t gg, int c) {
-                const int s = gg & 1;
-                if (gg >= 2) mbar_wait(&bars[2 + s], ((gg - 2) >> 1) & 1);  // stage free
-                mbar_expect_tx(&bars[s], 2 * b_chunk);
-                bulk_g2s(Bst + (2 * s) * b_chunk, whi + (size_t)c * H * KC, b_chunk, &bars[s]);
-                bulk_g2s(Bst + (2 * s + 1) * b_chunk, wlo + (size_t)c * H * KC, b_chunk, &bars[s]);
-            };
-            const uint32_t g0 = g;
-            load(g0, 0);
-            for (int c = 0; c < nch; ++c) {
-                const uint32_t gc = g0 + c;
-                const int s = gc & 1;
-                if (c + 1 < nch) load(gc + 1, c + 1);
-                mbar_wait(&bars[s], (gc >> 1) & 1);  // chunk landed
-                tc_fence_after();
-                const uint32_t a_hi = smem_u32(A_hi) + c * (M * KC * 2);
-                const uint32_t a_lo = smem_u32(A_lo) + c * (M * KC * 2);
-                const uint32_t b_hi = smem_u32(Bst + (2 * s) * b_chunk);
-                const uint32_t b_lo = smem_u32(Bst + (2 * s + 1) * b_chunk);
-#pragma unroll
-                for (int ks = 0; ks < KC / 16; ++ks) {
-                    const uint32_t o = ks * 256;  // two core matrices along K
-                    const uint64_t dah = smem_desc(a_hi + o, lbo, sbo);
-                    const uint64_t dal = smem_desc(a_lo + o, lbo, sbo);
-                    const uint64_t dbh = smem_desc(b_hi + o, lbo, sbo);
-                    const uint64_t dbl = smem_desc(b_lo + o, lbo, sbo);
-                    mma_bf16(tmem, dah, dbh, idesc, (c | ks) != 0);
-                    mma_bf16(tmem, dah, dbl, idesc, 1);
-                    mma_bf16(tmem, dal, dbh, idesc, 1);
-                }
-                mma_commit(&bars[2 + s]);  // stage s free once these MMAs complete
-            }
-            mma_commit(&bars[4]);  // the layer's accumulator is final
-        }
-        g += nch;
-        __syncwarp();
-        mbar_wait(&bars[4], l & 1);
-        tc_fence_after();
-        // ---- epilogue (this thread's row and column quarter): bias, SiLU; split
-        // into A for the next layer, or partial output-layer dot products
-        const bool last = l + 1 == a.n_tc;
-        const float *bias = s_bh + (size_t)l * H;
-        for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
-            float v[32];
-            tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + cc * 32, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = silu(v[i] + bias[cc * 32 + i]);
-            if (last) {
-#pragma unroll
-                for (int o = 0; o < 4; ++o) {
-                    if (o < nout) {
-                        const float *wr = s_wo + (size_t)o * H + cc * 32;
-                        float s = out_acc[o];
-#pragma unroll
-                        for (int i = 0; i < 32; ++i) s = fmaf(wr[i], v[i], s);
-                        out_acc[o] = s;
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int k8 = 0; k8 < 4; ++k8) store_split8(A_hi, A_lo, row, cc * 32 + k8 * 8, v + 8 * k8);
-            }
-        }
-        fence_async_smem();
-        tc_fence_before();
-        __syncthreads();
-        tc_fence_after();
-    }
-    // output layer: the four column quarters' partial sums, in quarter order
-#pragma unroll
-    for (int o = 0; o < 4; ++o) s_red[(quarter * M + row) * 4 + o] = out_acc[o];
-    __syncthreads();
-    if (quarter == 0 && r_glob < a.rows)
+    if (warp < EPI_WARPS && quarter == 0 && r_glob < a.rows)
         for (int o = 0; o < nout && o < 4; ++o) {
             const float s = ((s_red[(0 * M + row) * 4 + o] + s_red[(1 * M + row) * 4 + o]) +
                              (s_red[(2 * M + row) * 4 + o] + s_red[(3 * M + row) * 4 + o]));
             a.y[r_glob * a.y_stride + o] = s + a.bout[o];
         }
-    tc_fence_before();
-    __syncthreads();
     if (warp == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(256));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem),
+                     "r"(tcols));
 }
 
 inline size_t mlp_smem_bytes(int H, int d_in, int n_tc, int n_out) {
-    return 2 * (size_t)M * H * 2 + 4 * (size_t)H * KC * 2 + 6 * 8 +
-           4 * ((size_t)H * d_in + H + (size_t)n_tc * H + (size_t)n_out * H + 4 * M * 4);
+    return 2 * (size_t)M * H * 2 + 4 * (size_t)H * KC * 2 + 8 * (8 + MAXCH) +
+           4 * ((size_t)H * din_pad(d_in) + H + (size_t)n_tc * H + (size_t)n_out * H + 4 * M * 4);
 }
 
 }  // namespace mlp
