@@ -154,7 +154,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
     for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
+// x * sigmoid(x) = x / (1 + 2^(-x log2 e)): MUFU.EX2 and MUFU.RCP without the
+// range fix-ups of __expf / __fdividef (x -> -inf: e = inf, rcp = 0, -0; x -> +inf:
+// e = 0, x; NaN propagates)
+__device__ __forceinline__ float silu(float x) {
+    float e, r;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
+    return x * r;
+}
 
 // element (row r, column k) of a K-major canonical operand made of 32-column
 // chunks: chunk k / 32 at chunk_bytes * (k / 32); inside a chunk, core matrix
@@ -166,18 +174,23 @@ __host__ __device__ __forceinline__ uint32_t op_offset(int r, int k, int rows_to
            (uint32_t)(r % 8) * 16 + (uint32_t)(k % 8) * 2;
 }
 
-// store 8 consecutive float activations (row r, columns k..k+7) split into bf16 hi / lo
+// store 8 consecutive float activations (row r, columns k..k+7) split into bf16
+// hi / lo (x = hi + lo, both rounded to nearest), two values per conversion
 __device__ __forceinline__ void store_split8(unsigned char *ahi, unsigned char *alo, int r, int k,
                                              const float *v) {
-    __align__(16) __nv_bfloat16 hi[8], lo[8];
+    uint4 h4, l4;
+    uint32_t *hp = &h4.x, *lp = &l4.x;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        hi[i] = __float2bfloat16_rn(v[i]);
-        lo[i] = __float2bfloat16_rn(v[i] - __bfloat162float(hi[i]));
+    for (int i = 0; i < 4; ++i) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * i], v[2 * i + 1]);
+        const float2 hf = __bfloat1622float2(h);
+        const __nv_bfloat162 l = __floats2bfloat162_rn(v[2 * i] - hf.x, v[2 * i + 1] - hf.y);
+        hp[i] = *reinterpret_cast<const uint32_t *>(&h);
+        lp[i] = *reinterpret_cast<const uint32_t *>(&l);
     }
     const uint32_t off = op_offset(r, k, M);
-    *reinterpret_cast<uint4 *>(ahi + off) = *reinterpret_cast<const uint4 *>(hi);
-    *reinterpret_cast<uint4 *>(alo + off) = *reinterpret_cast<const uint4 *>(lo);
+    *reinterpret_cast<uint4 *>(ahi + off) = h4;
+    *reinterpret_cast<uint4 *>(alo + off) = l4;
 }
 
 // fp32 W [N][K] (torch Linear weight: out x in, K contiguous) -> packed bf16 hi / lo
@@ -377,16 +390,29 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
             for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
                 float v[32];
                 tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + cc * 32, v);
+                const float4 *b4 = reinterpret_cast<const float4 *>(bias + cc * 32);
 #pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = silu(v[i] + bias[cc * 32 + i]);
+                for (int i4 = 0; i4 < 8; ++i4) {
+                    const float4 bb = b4[i4];
+                    v[4 * i4] = silu(v[4 * i4] + bb.x);
+                    v[4 * i4 + 1] = silu(v[4 * i4 + 1] + bb.y);
+                    v[4 * i4 + 2] = silu(v[4 * i4 + 2] + bb.z);
+                    v[4 * i4 + 3] = silu(v[4 * i4 + 3] + bb.w);
+                }
                 if (last) {
 #pragma unroll
                     for (int o = 0; o < 4; ++o) {
                         if (o < nout) {
-                            const float *wr = s_wo + (size_t)o * H + cc * 32;
+                            const float4 *w4 = reinterpret_cast<const float4 *>(s_wo + (size_t)o * H + cc * 32);
                             float s = out_acc[o];
 #pragma unroll
-                            for (int i = 0; i < 32; ++i) s = fmaf(wr[i], v[i], s);
+                            for (int i4 = 0; i4 < 8; ++i4) {
+                                const float4 ww = w4[i4];
+                                s = fmaf(ww.x, v[4 * i4], s);
+                                s = fmaf(ww.y, v[4 * i4 + 1], s);
+                                s = fmaf(ww.z, v[4 * i4 + 2], s);
+                                s = fmaf(ww.w, v[4 * i4 + 3], s);
+                            }
                             out_acc[o] = s;
                         }
                     }
