@@ -160,3 +160,30 @@ def test_go1_env_errors(G):
     env.rollout(torch.zeros((2, 40, 12), device="cuda"))
     env.check()  # the error was reported once
     env.close()
+
+
+def test_go1_env_world_count_invariance(G):
+    """A world's trajectory does not depend on how many worlds share the launch:
+    the CTA size follows the world count (one CTA per SM per wave; 1 to 64
+    worlds per CTA, the step's CTA barriers only in full CTAs), so the same
+    worlds stepped within batches of 5, 300 and 9001 are bit-identical, float32
+    and float64."""
+    K = 6
+    for dt in ("float32", "float64"):
+        ref = None
+        for n in (9001, 300, 5):
+            env = G.DeviceGo1Env(n, _cfg(G, episode_length=4), dtype=dt)
+            env.reset(seed=12)
+            acts = torch.as_tensor(np.random.default_rng(2).uniform(-1, 1, (K, 9001, 12))[:, :n],
+                                   device="cuda", dtype=env.dtype)
+            out = env.rollout(acts.contiguous())
+            env.check()
+            got = (out["obs"].cpu().numpy(), out["reward"].cpu().numpy(),
+                   env.state()["qpos"].cpu().numpy())
+            env.close()
+            if ref is None:
+                ref = got
+                continue
+            np.testing.assert_array_equal(got[0], ref[0][:, :n])
+            np.testing.assert_array_equal(got[1], ref[1][:, :n])
+            np.testing.assert_array_equal(got[2], ref[2][:n])
