@@ -58,14 +58,9 @@ int64_t tiles(int64_t rows) { return rows > 0 ? (rows + dk::mlp::M - 1) / dk::ml
 int mlp_launch(const dk::mlp::MlpArgs &a0, int64_t t0, const dk::mlp::MlpArgs &a1, int64_t t1,
                size_t smem, void *stream) {
     if (t0 + t1 == 0) return DK_OK;
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(dk::mlp::mlp_tc_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)smem);
-        if (e != cudaSuccess) return cuda_rc(e, "dk_mlp_forward attribute");
-        attr = smem;
-    }
+    static dk::SmemOptIn optin;
+    cudaError_t e = optin.ensure((const void *)dk::mlp::mlp_tc_kernel, smem);
+    if (e != cudaSuccess) return cuda_rc(e, "dk_mlp_forward attribute");
     dk::mlp::mlp_tc_kernel<<<(unsigned)(t0 + t1), dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(
         a0, a1, t0);
     return cuda_rc(cudaGetLastError(), "mlp_tc_kernel");

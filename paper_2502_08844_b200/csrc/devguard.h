@@ -26,4 +26,21 @@ struct PtrDeviceGuard {
         if (dev >= 0 && prev >= 0) cudaSetDevice(prev);
     }
 };
+
+// Dynamic shared memory above 48 KB is a per-device function attribute: opt a
+// kernel in once per device (and again when a launch needs more).
+struct SmemOptIn {
+    size_t bytes[64] = {};
+    cudaError_t ensure(const void *fn, size_t smem) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (dev < 0 || dev >= 64)
+            return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (smem <= bytes[dev]) return cudaSuccess;
+        cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (e == cudaSuccess) bytes[dev] = smem;
+        return e;
+    }
+};
 }  // namespace dk

@@ -3,6 +3,7 @@
 // --fmad=false to keep the reference's two-rounding arithmetic).
 #pragma once
 #include "envstep_kernels.cuh"
+#include "devguard.h"
 
 namespace dk {
 
@@ -53,14 +54,13 @@ inline cudaError_t launch_task_rollout_tl(const T *actions, int64_t K, const Env
                                           const StepOut<T> &out, unsigned long long *err,
                                           cudaStream_t st) {
     using S = RolloutShape<Task, T, TL>;
-    static bool attr_set = false;  // per instantiation; opt in above 48 KB once
-    if (!attr_set) {
-        for (auto kk : {rollout_kernel<Task, T, true, TL>, rollout_kernel<Task, T, false, TL>}) {
-            cudaError_t e = cudaFuncSetAttribute(kk, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)launch_smem<S>());
-            if (e != cudaSuccess) return e;
-        }
-        attr_set = true;
+    static SmemOptIn optin[2];  // per device and instantiation; opt in above 48 KB
+    {
+        cudaError_t e = optin[0].ensure((const void *)rollout_kernel<Task, T, true, TL>,
+                                        launch_smem<S>());
+        if (e == cudaSuccess)
+            e = optin[1].ensure((const void *)rollout_kernel<Task, T, false, TL>, launch_smem<S>());
+        if (e != cudaSuccess) return e;
     }
     auto kern = sc.action_repeat == 1 ? rollout_kernel<Task, T, true, TL>
                                       : rollout_kernel<Task, T, false, TL>;

@@ -588,13 +588,9 @@ cudaError_t launch_env(const PhysConst<T> &pc, const EnvConst<T> &ec, const EnvS
                        const EnvIO<T> &io, cudaStream_t s) {
     const int threads = phys::pick_threads(io.n, [&](int t) { return env_smem_bytes(pc, t); });
     const size_t smem = env_smem_bytes(pc, threads);
-    static size_t attr = 0;
-    if (smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(go1_env_kernel<T>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
+    static SmemOptIn optin;  // per device
+    cudaError_t e = optin.ensure((const void *)go1_env_kernel<T>, smem);
+    if (e != cudaSuccess) return e;
     const int wpc = threads / 4;
     const unsigned grid = (unsigned)((io.n + wpc - 1) / wpc);
     go1_env_kernel<T><<<grid, threads, smem, s>>>(pc, ec, st, io);

@@ -32,6 +32,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/deskrl_b200.h"
+#include "devguard.h"
 
 namespace dk {
 namespace phys {
@@ -1345,14 +1346,11 @@ cudaError_t launch_phys(const PhysConst<T> &pc, const PhysArgs<T> &a, const Phys
                         cudaStream_t st) {
     const int threads = pick_threads(a.n, [&](int t) { return phys_smem_bytes(pc, t); });
     const size_t smem = phys_smem_bytes(pc, threads);
-    static size_t attr = 0;
-    if (smem > attr) {
-        for (auto k : {phys_kernel<T, false>, phys_kernel<T, true>}) {
-            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
-            if (e != cudaSuccess) return e;
-        }
-        attr = smem;
+    static SmemOptIn optin[2];  // per device; [0] step, [1] inspect
+    for (int k = 0; k < 2; ++k) {
+        cudaError_t e = optin[k].ensure(
+            k ? (const void *)phys_kernel<T, true> : (const void *)phys_kernel<T, false>, smem);
+        if (e != cudaSuccess) return e;
     }
     const int wpc = threads / QUAD;
     const unsigned grid = (unsigned)((a.n + wpc - 1) / wpc);
