@@ -1413,6 +1413,10 @@ def main():
         torch.cuda.set_device(local_rank)
         backend = os.environ.get("DK_BENCH_BACKEND", "nccl")
         if backend == "nccl":
+            # communicator set-up lines on stderr (the JSON line is on stdout): the
+            # transport NCCL picked (NVLink / NVLS) is in the driver's logs
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             tdist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
         else:
             tdist.init_process_group(backend)
