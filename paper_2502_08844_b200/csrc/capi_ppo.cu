@@ -66,9 +66,9 @@ int norm_update(int64_t rows, int dim, const T *batch, double count, double *mea
     double *partial = w.p, *b_mean = w.p + lanes * dim, *b_var = b_mean + dim;
     const int64_t P = lanes * dim;
     dk::colsum_kernel<T><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes, batch, nullptr, partial);
-    dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, rows, partial, b_mean);
+    dk::colreduce_kernel<<<(unsigned)dim, dk::kColReduceThreads, 0, st>>>(dim, lanes, rows, partial, b_mean);
     dk::colsum_kernel<T><<<blocks(P, 256), 256, 0, st>>>(rows, dim, lanes, batch, b_mean, partial);
-    dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, rows, partial, b_var);
+    dk::colreduce_kernel<<<(unsigned)dim, dk::kColReduceThreads, 0, st>>>(dim, lanes, rows, partial, b_var);
     dk::norm_merge_kernel<<<blocks(dim, 128), 128, 0, st>>>(dim, count, (double)rows, b_mean,
                                                            b_var, mean, var);
     return cuda_rc(cudaGetLastError(), "normalizer update launch");
@@ -283,7 +283,7 @@ int dk_norm_colsum(int dtype, int64_t rows, int dim, const void *batch, const do
                                                                 (const float *)batch, center,
                                                                 partial);
     // rows = 1: colreduce divides by it, so out = the plain column sums
-    dk::colreduce_kernel<<<blocks(dim, 8), 256, 0, st>>>(dim, lanes, 1, partial, sums);
+    dk::colreduce_kernel<<<(unsigned)dim, dk::kColReduceThreads, 0, st>>>(dim, lanes, 1, partial, sums);
     return cuda_rc(cudaGetLastError(), "normalizer colsum launch");
 }
 
