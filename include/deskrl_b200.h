@@ -582,6 +582,8 @@ typedef struct dk_mlp {
     const void *w_hi, *w_lo;     /* packed [n_tc][hidden * hidden] bf16 */
     const float *b_hidden;       /* [n_tc][hidden] */
     const float *w_out, *b_out;  /* [n_out, hidden], [n_out] */
+    const void *w0_hi, *w0_lo;   /* d_in > 16: layer 0 packed [hidden * K0] bf16, K0 = d_in
+                                    rounded up to 32 (zero columns), on the tensor cores */
 } dk_mlp;
 
 int dk_mlp_pack(const float *w, int n, int k, void *w_hi, void *w_lo, void *stream);

@@ -24,11 +24,14 @@ int mlp_args(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const flo
              size_t &smem) {
     if (!net || !x || !y) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward: null");
     const int H = net->hidden;
-    if (!(H == 128 || H == 256) || net->d_in < 1 || net->d_in > 16 || net->n_out < 1 ||
-        net->n_out > 4 || net->n_tc < 1)
+    if (!(H == 128 || H == 256) || net->d_in < 1 || net->d_in > dk::mlp::MAXDIN ||
+        net->n_out < 1 || net->n_out > dk::mlp::MAXOUT || net->n_tc < 1)
         return dk_internal_fail(DK_ERR_INVALID_INPUT,
-                                "dk_mlp_forward: hidden must be 128 or 256, d_in <= 16, "
-                                "1 <= n_out <= 4, at least one hidden x hidden layer");
+                                "dk_mlp_forward: hidden must be 128 or 256, d_in <= 128, "
+                                "1 <= n_out <= 16, at least one hidden x hidden layer");
+    if (dk::mlp::tc_layer0(net->d_in) && (!net->w0_hi || !net->w0_lo))
+        return dk_internal_fail(DK_ERR_INVALID_INPUT,
+                                "dk_mlp_forward: d_in > 16 needs the packed layer-0 weights");
     a.x = x;
     a.rows = rows;
     a.x_stride = x_stride;
@@ -43,6 +46,8 @@ int mlp_args(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const flo
     a.bh = net->b_hidden;
     a.wout = net->w_out;
     a.bout = net->b_out;
+    a.w0hi = (const __nv_bfloat16 *)net->w0_hi;
+    a.w0lo = (const __nv_bfloat16 *)net->w0_lo;
     a.y = y;
     a.y_stride = y_stride;
     a.desc_swap = desc_swap;
@@ -58,11 +63,18 @@ int64_t tiles(int64_t rows) { return rows > 0 ? (rows + dk::mlp::M - 1) / dk::ml
 int mlp_launch(const dk::mlp::MlpArgs &a0, int64_t t0, const dk::mlp::MlpArgs &a1, int64_t t1,
                size_t smem, void *stream) {
     if (t0 + t1 == 0) return DK_OK;
-    static dk::SmemOptIn optin;
-    cudaError_t e = optin.ensure((const void *)dk::mlp::mlp_tc_kernel, smem);
+    const bool wide = a0.n_out > 4 || (t1 > 0 && a1.n_out > 4);
+    const void *fn = wide ? (const void *)dk::mlp::mlp_tc_kernel<dk::mlp::MAXOUT>
+                          : (const void *)dk::mlp::mlp_tc_kernel<4>;
+    static dk::SmemOptIn optin[2];
+    cudaError_t e = optin[wide ? 1 : 0].ensure(fn, smem);
     if (e != cudaSuccess) return cuda_rc(e, "dk_mlp_forward attribute");
-    dk::mlp::mlp_tc_kernel<<<(unsigned)(t0 + t1), dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(
-        a0, a1, t0);
+    if (wide)
+        dk::mlp::mlp_tc_kernel<dk::mlp::MAXOUT>
+            <<<(unsigned)(t0 + t1), dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(a0, a1, t0);
+    else
+        dk::mlp::mlp_tc_kernel<4>
+            <<<(unsigned)(t0 + t1), dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(a0, a1, t0);
     return cuda_rc(cudaGetLastError(), "mlp_tc_kernel");
 }
 

@@ -32,10 +32,15 @@ constexpr int M = 128;          // rows per CTA (= TMEM lanes)
 constexpr int EPI_WARPS = 16;   // warp w < 16 -> TMEM lanes 32 (w % 4), column quarter w / 4
 constexpr int THREADS = 32 * (EPI_WARPS + 1);  // + warp 16: weight copies and MMA issue
 constexpr int MAXCH = 8;        // K chunks of a hidden layer (H / KC)
+constexpr int MAXOUT = 16;      // output-layer width
+constexpr int MAXDIN = 128;     // input width (> 16: layer 0 on the tensor cores)
 // layer 0's padded input width: 4, 8 or 16 columns
 __host__ __device__ constexpr int din_pad(int d_in) { return d_in <= 4 ? 4 : (d_in <= 8 ? 8 : 16); }
+// d_in > 16: layer 0 is a tensor-core layer over K0 = d_in rounded up to 32
+__host__ __device__ constexpr bool tc_layer0(int d_in) { return d_in > 16; }
 constexpr int KC = 32;          // K columns per chunk
 constexpr int MAXH = 256;
+__host__ __device__ constexpr int k0_pad(int d_in) { return (d_in + KC - 1) / KC * KC; }
 
 struct MlpArgs {
     const float *x;        // [rows][x_stride], first d_in columns used
@@ -45,6 +50,8 @@ struct MlpArgs {
     const __nv_bfloat16 *whi, *wlo;   // packed hidden weights [n_tc][H*H]
     const float *bh;                  // [n_tc][H]
     const float *wout, *bout;         // [n_out][H], [n_out]
+    const __nv_bfloat16 *w0hi, *w0lo; // d_in > 16: layer 0 packed [H][K0] (K0 = d_in rounded
+                                      // up to 32), run on the tensor cores like the rest
     float *y;                         // [rows][y_stride]
     int64_t y_stride;
     int desc_swap;                    // debug: swap LBO / SBO
@@ -220,6 +227,8 @@ __global__ void pack_weights_kernel(const float *w, int N, int K, __nv_bfloat16 
 // observations and the value function on the same observations): CTAs
 // [0, tiles0) take network a0, the rest a1 -- the two calls' latency-bound
 // tiles then share the GPU instead of running back to back.
+// MO: output-layer accumulators per thread (4, or MAXOUT for wider heads)
+template <int MO>
 __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs a1,
                                                             int64_t tiles0) {
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -243,14 +252,17 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
     uint64_t *bars = reinterpret_cast<uint64_t *>(Bst + 4 * b_chunk);
     uint64_t *full = bars, *empty = bars + 2, *done = bars + 4, *achunk = bars + 6;
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6 + MAXCH);
-    // the float32 parameters used on the CUDA cores, staged once
-    // layer 0's weight rows padded to DP columns (zeros past d_in) for 16-byte loads
-    const int DP = din_pad(din);
+    // the float32 parameters used on the CUDA cores, staged once; layer 0's weight
+    // rows (CUDA-core layer 0 only) padded to DP columns (zeros past d_in) for
+    // 16-byte loads
+    const bool tc0 = tc_layer0(din);
+    const int DP = tc0 ? 0 : din_pad(din);
+    const int NO = nout <= 4 ? 4 : MAXOUT;                   // partial-sum slots per row
     float *s_w0 = reinterpret_cast<float *>(bars + 8 + MAXCH);  // [H][DP]
     float *s_b0 = s_w0 + H * DP;                             // [H]
     float *s_bh = s_b0 + H;                                  // [n_tc][H]
     float *s_wo = s_bh + a.n_tc * H;                         // [nout][H]
-    float *s_red = s_wo + nout * H;                          // [4 quarters][M][4] partial outputs
+    float *s_red = s_wo + nout * H;                          // [4 quarters][M][NO] partial outputs
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int q = warp & 3, quarter = warp >> 2;            // TMEM lane group, column quarter
     const int row = 32 * q + lane;
@@ -282,32 +294,61 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
     const uint32_t tmem = *tmem_slot;
     // K chunks are consumed in the order the epilogue finishes them: each column
     // quarter writes its chunks in turn, so the first of every quarter comes first
+    // (a tensor-core layer 0 reads x, staged one 32-column chunk per quarter)
     const int cpq = nch / 4;                                 // chunks per quarter (1 or 2)
     auto kchunk = [&](int i) { return (i % 4) * cpq + i / 4; };
+    const int nl = a.n_tc + (tc0 ? 1 : 0);                   // tensor-core layers
+    const int nch0 = tc0 ? k0_pad(din) / KC : nch;           // K chunks of layer 0
+    auto layer_chunks = [&](int l) { return l == 0 ? nch0 : nch; };
 
     if (warp == EPI_WARPS) {
         // ---------------------------------------------- weights and MMA issue
         if (lane == 0) {
-            const uint32_t total = (uint32_t)(a.n_tc * nch);
+            const uint32_t total = (uint32_t)(nch0 + (nl - 1) * nch);
+            // global weight chunk gg -> (layer, K chunk, source)
             auto load = [&](uint32_t gg) {
                 const int s = gg & 1;
-                const int ll = (int)(gg / nch), c = kchunk((int)(gg % nch));
+                int ll, i;
+                if (gg < (uint32_t)nch0) {
+                    ll = 0;
+                    i = (int)gg;
+                } else {
+                    ll = 1 + (int)((gg - nch0) / nch);
+                    i = (int)((gg - nch0) % nch);
+                }
                 if (gg >= 2) mbar_wait(&empty[s], ((gg - 2) >> 1) & 1);  // stage free
                 mbar_expect_tx(&full[s], 2 * b_chunk);
-                const size_t off = (size_t)ll * H * H + (size_t)c * H * KC;
-                bulk_g2s(Bst + (2 * s) * b_chunk, a.whi + off, b_chunk, &full[s]);
-                bulk_g2s(Bst + (2 * s + 1) * b_chunk, a.wlo + off, b_chunk, &full[s]);
+                const __nv_bfloat16 *hi, *lo;
+                int c;
+                if (tc0 && ll == 0) {
+                    c = i;
+                    hi = a.w0hi + (size_t)c * H * KC;
+                    lo = a.w0lo + (size_t)c * H * KC;
+                } else {
+                    c = kchunk(i);
+                    const size_t off = (size_t)(ll - (tc0 ? 1 : 0)) * H * H + (size_t)c * H * KC;
+                    hi = a.whi + off;
+                    lo = a.wlo + off;
+                }
+                bulk_g2s(Bst + (2 * s) * b_chunk, hi, b_chunk, &full[s]);
+                bulk_g2s(Bst + (2 * s + 1) * b_chunk, lo, b_chunk, &full[s]);
             };
             load(0);
             const uint32_t idesc = instr_desc_bf16(M, H);
             const uint32_t lbo = a.desc_swap ? 512u : 128u, sbo = a.desc_swap ? 128u : 512u;
-            for (int l = 0; l < a.n_tc; ++l) {
+            uint32_t gbase = 0;
+            for (int l = 0; l < nl; ++l) {
                 const uint32_t tacc = tmem + (uint32_t)((l & 1) * H);
-                for (int i = 0; i < nch; ++i) {
-                    const int c = kchunk(i);
-                    const uint32_t gc = (uint32_t)(l * nch + i);
+                const int lch = layer_chunks(l);
+                for (int i = 0; i < lch; ++i) {
+                    const int c = (tc0 && l == 0) ? i : kchunk(i);
+                    const uint32_t gc = gbase + (uint32_t)i;
                     const int s = gc & 1;
-                    mbar_wait(&achunk[c], l & 1);   // this layer's input, K chunk c
+                    // this layer's input, K chunk c: its barrier completed once per
+                    // earlier layer whose input had chunk c (a tensor-core layer 0
+                    // reads only x's nch0 chunks)
+                    const int ph = (tc0 && l > 0 && c >= nch0) ? l - 1 : l;
+                    mbar_wait(&achunk[c], ph & 1);
                     mbar_wait(&full[s], (gc >> 1) & 1);  // its weights
                     tc_fence_after();
                     const uint32_t a_hi = smem_u32(A_hi) + c * (M * KC * 2);
@@ -326,11 +367,12 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                         mma_bf16(tacc, dal, dbh, idesc, 1);
                     }
                     mma_commit(&empty[s]);  // stage s free once these MMAs complete
-                    if (i + 1 == nch) mma_commit(&done[l & 1]);  // layer l's accumulator final
+                    if (i + 1 == lch) mma_commit(&done[l & 1]);  // layer l's accumulator final
                     // the next weight chunk after this chunk's MMAs are queued (its
                     // stage-free wait is on the previous chunk's MMAs)
                     if (gc + 1 < total) load(gc + 1);
                 }
+                gbase += (uint32_t)lch;
             }
         }
         __syncwarp();
@@ -375,17 +417,35 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                 if ((j0 + 8) % KC == 0) publish(j0 / KC);
             }
         };
-        if (DP == 4) layer0(std::integral_constant<int, 4>{});
+        if (tc0) {
+            // stage x (K0 columns, zeros past d_in) as the first layer's operand:
+            // quarter c splits chunk c of its 32 rows
+            if (quarter < nch0) {
+                for (int k8 = 0; k8 < KC; k8 += 8) {
+                    float v[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        const int col = quarter * KC + k8 + i;
+                        v[i] = (col < din && r_glob < a.rows) ? a.x[r_glob * a.x_stride + col]
+                                                              : 0.0f;
+                    }
+                    store_split8(A_hi, A_lo, row, quarter * KC + k8, v);
+                }
+                publish(quarter);
+            }
+        } else if (DP == 4) layer0(std::integral_constant<int, 4>{});
         else if (DP == 8) layer0(std::integral_constant<int, 8>{});
         else layer0(std::integral_constant<int, 16>{});
-        float out_acc[4] = {0.f, 0.f, 0.f, 0.f};
-        for (int l = 0; l < a.n_tc; ++l) {
+        float out_acc[MO];
+#pragma unroll
+        for (int o = 0; o < MO; ++o) out_acc[o] = 0.f;
+        for (int l = 0; l < nl; ++l) {
             mbar_wait(&done[l & 1], (l >> 1) & 1);
             tc_fence_after();
             // ---- epilogue (this thread's row and column quarter): bias, SiLU; split
             // into the next layer's input, or partial output-layer dot products
-            const bool last = l + 1 == a.n_tc;
-            const float *bias = s_bh + (size_t)l * H;
+            const bool last = l + 1 == nl;
+            const float *bias = (tc0 && l == 0) ? s_b0 : s_bh + (size_t)(l - (tc0 ? 1 : 0)) * H;
             const uint32_t tacc = tmem + (uint32_t)((l & 1) * H);
             for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
                 float v[32];
@@ -401,7 +461,7 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                 }
                 if (last) {
 #pragma unroll
-                    for (int o = 0; o < 4; ++o) {
+                    for (int o = 0; o < MO; ++o) {
                         if (o < nout) {
                             const float4 *w4 = reinterpret_cast<const float4 *>(s_wo + (size_t)o * H + cc * 32);
                             float s = out_acc[o];
@@ -426,14 +486,15 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
         }
         // output layer: the four column quarters' partial sums, in quarter order
 #pragma unroll
-        for (int o = 0; o < 4; ++o) s_red[(quarter * M + row) * 4 + o] = out_acc[o];
+        for (int o = 0; o < MO; ++o)
+            if (o < nout) s_red[(quarter * M + row) * NO + o] = out_acc[o];
     }
     tc_fence_before();
     __syncthreads();
     if (warp < EPI_WARPS && quarter == 0 && r_glob < a.rows)
-        for (int o = 0; o < nout && o < 4; ++o) {
-            const float s = ((s_red[(0 * M + row) * 4 + o] + s_red[(1 * M + row) * 4 + o]) +
-                             (s_red[(2 * M + row) * 4 + o] + s_red[(3 * M + row) * 4 + o]));
+        for (int o = 0; o < nout; ++o) {
+            const float s = ((s_red[(0 * M + row) * NO + o] + s_red[(1 * M + row) * NO + o]) +
+                             (s_red[(2 * M + row) * NO + o] + s_red[(3 * M + row) * NO + o]));
             a.y[r_glob * a.y_stride + o] = s + a.bout[o];
         }
     if (warp == 0)
@@ -442,8 +503,10 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
 }
 
 inline size_t mlp_smem_bytes(int H, int d_in, int n_tc, int n_out) {
+    const size_t dp = tc_layer0(d_in) ? 0 : (size_t)din_pad(d_in);
+    const size_t no = n_out <= 4 ? 4 : MAXOUT;
     return 2 * (size_t)M * H * 2 + 4 * (size_t)H * KC * 2 + 8 * (8 + MAXCH) +
-           4 * ((size_t)H * din_pad(d_in) + H + (size_t)n_tc * H + (size_t)n_out * H + 4 * M * 4);
+           4 * ((size_t)H * dp + H + (size_t)n_tc * H + (size_t)n_out * H + 4 * M * no);
 }
 
 }  // namespace mlp

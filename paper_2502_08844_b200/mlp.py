@@ -4,7 +4,7 @@ MLPPolicy, MLPValue: Linear + Swish layers).
 
 ``TensorCoreMLP(seq)`` wraps a torch ``nn.Sequential`` of the reference's shape
 -- Linear(d_in, H), SiLU, [Linear(H, H), SiLU] x n, Linear(H, n_out) with
-H in {128, 256}, d_in <= 16, n_out <= 4 -- and evaluates it in one kernel:
+H in {128, 256}, d_in <= 128, n_out <= 16 -- and evaluates it in one kernel:
 layer 0 and the output layer in float32 on the CUDA cores, the H x H layers
 on tcgen05 with a BF16x3 operand split (float32 accumulation; ~1e-6 relative
 to a float32 evaluation).  The packed weights are rebuilt when a parameter
@@ -26,7 +26,8 @@ class MlpC(ctypes.Structure):
                 ("n_out", ctypes.c_int32), ("w0", ctypes.c_void_p), ("b0", ctypes.c_void_p),
                 ("w_hi", ctypes.c_void_p), ("w_lo", ctypes.c_void_p),
                 ("b_hidden", ctypes.c_void_p), ("w_out", ctypes.c_void_p),
-                ("b_out", ctypes.c_void_p)]
+                ("b_out", ctypes.c_void_p), ("w0_hi", ctypes.c_void_p),
+                ("w0_lo", ctypes.c_void_p)]
 
 
 def _linears(seq):
@@ -56,7 +57,7 @@ def supported(seq) -> bool:
         return False
     H = lins[0].out_features
     hidden = lins[1:-1]
-    return (H in (128, 256) and lins[0].in_features <= 16 and lins[-1].out_features <= 4
+    return (H in (128, 256) and lins[0].in_features <= 128 and lins[-1].out_features <= 16
             and all(m.in_features == H and m.out_features == H for m in hidden)
             and lins[-1].in_features == H and all(m.bias is not None for m in lins))
 
@@ -100,9 +101,20 @@ class TensorCoreMLP:
                                          self.w_lo[i].data_ptr(), stream))
         self.b_h = torch.stack([f32(m.bias) for m in self.lins[1:-1]]).contiguous()
         self.w_out, self.b_out = f32(self.lins[-1].weight), f32(self.lins[-1].bias)
+        w0p = [None, None]
+        if self.d_in > 16:  # layer 0 on the tensor cores: packed, K padded to 32
+            k0 = (self.d_in + 31) // 32 * 32
+            w0pad = torch.zeros((H, k0), dtype=torch.float32, device=dev)
+            w0pad[:, :self.d_in] = self.w0
+            self.w0_hi = torch.empty((H * k0,), dtype=torch.bfloat16, device=dev)
+            self.w0_lo = torch.empty((H * k0,), dtype=torch.bfloat16, device=dev)
+            _check(self._lib.dk_mlp_pack(w0pad.data_ptr(), H, k0, self.w0_hi.data_ptr(),
+                                         self.w0_lo.data_ptr(), stream))
+            self._w0pad = w0pad
+            w0p = [self.w0_hi.data_ptr(), self.w0_lo.data_ptr()]
         self._net = MlpC(self.d_in, H, n, self.n_out, self.w0.data_ptr(), self.b0.data_ptr(),
                          self.w_hi.data_ptr(), self.w_lo.data_ptr(), self.b_h.data_ptr(),
-                         self.w_out.data_ptr(), self.b_out.data_ptr())
+                         self.w_out.data_ptr(), self.b_out.data_ptr(), w0p[0], w0p[1])
         self._key = key
         self.packs += 1
 

@@ -88,3 +88,30 @@ def test_tc_mlp_pair_launch_equals_separate_calls(M):
     count = torch.tensor([300], dtype=torch.int64, device="cuda")
     yc = tv.call_count(xv, count)
     torch.testing.assert_close(yc[:300], tv(xv)[:300], rtol=0, atol=0)
+
+
+@pytest.mark.parametrize("d_in,hidden,n_layers,n_out,rows", [
+    (56, 128, 4, 12, 8192),   # a Go1 joystick policy: noisy observation -> 12 joint means
+    (75, 256, 5, 1, 3000),    # its critic on the privileged observation
+    (17, 128, 3, 16, 129),
+])
+def test_tc_mlp_wide_inputs_and_outputs(M, d_in, hidden, n_layers, n_out, rows):
+    """d_in > 16 runs layer 0 on the tensor cores too (K padded to 32); up to 16
+    outputs: against a float64 evaluation."""
+    import torch.nn as nn
+
+    torch.manual_seed(d_in)
+    mods = [nn.Linear(d_in, hidden), nn.SiLU()]
+    for _ in range(n_layers - 2):
+        mods += [nn.Linear(hidden, hidden), nn.SiLU()]
+    mods += [nn.Linear(hidden, n_out)]
+    net = nn.Sequential(*mods).cuda()
+    assert M.supported(net)
+    tc = M.TensorCoreMLP(net)
+    x = torch.randn(rows, d_in, device="cuda") * 2
+    got = tc(x)
+    ref = net.double()(x.double())
+    net.float()
+    err = _err(got, ref)
+    print(d_in, hidden, n_out, "max rel err vs float64 %.2e" % err)
+    assert err < 2e-5, err
