@@ -761,6 +761,7 @@ def run_b200(args, rank, world, local_rank, dist):
         extras["sweep"] = bench_sweep(args, dev)
         extras["all_tasks"] = bench_tasks(args, dev)
         extras["ppo_rollout"] = bench_ppo_rollout(args, dev)
+        extras["go1_ppo_rollout"] = bench_go1_ppo_rollout(args, dev)
         extras["pixels"] = bench_pixels(args, dev)
     if not args.no_tail:
         extras["go1_tail"] = bench_go1_tail(args, dev, rank)
@@ -1043,6 +1044,57 @@ def bench_ppo_rollout(args, dev, T=30, reps=5):
             "reference_cpu": {"value": 9.7e3, "unit": "env_steps/s",
                               "sample": "ppo.collect_rollout, N=1024, T=30, 16 torch threads, "
                                         "build container (not the GPU box)"}}
+
+
+def bench_go1_ppo_rollout(args, dev, T=30, reps=3):
+    """The PPO rollout on the headline env: DeviceGo1Env at the bench's worlds,
+    an asymmetric actor-critic of the reference's shapes (MLPPolicy on the
+    56-wide noisy observation -> 12 joint means, MLPValue on the 75-wide
+    privileged one) on the tensor cores, the fused step bookkeeping, truncation
+    bootstraps from the terminal privileged rows; eager phases (collect_rollout_device)."""
+    import torch
+
+    from paper_2502_08844_b200 import go1env as G
+    from paper_2502_08844_b200 import ppo as P
+    from paper_2502_08844_b200 import rollout as R
+
+    class Cfg:
+        unroll_length, reward_scaling, discounting = T, 1.0, 0.97
+        policy_obs_key, value_obs_key = "state", "privileged_state"
+
+    n = args.num_envs
+    res = {}
+    for graph in (True, False):
+        torch.manual_seed(0)
+        env = G.DeviceGo1Env(n, G.Go1Config(), dtype="float32", device=dev.index)
+        obs = env.reset(seed=0)
+        pol, val = R.make_policy(56, 12).cuda(dev), R.make_value(75).cuda(dev)
+        pn, vn = P.DeviceRunningNormalizer(56), P.DeviceRunningNormalizer(75)
+        if graph:
+            rg = R.RolloutGraph(env, pol, val, Cfg, obs, pn, vn)
+            phase = lambda o: rg.run()  # noqa: E731
+        else:
+            phase = lambda o: R.collect_rollout_device(env, pol, val, Cfg, o, pn, vn)  # noqa: E731
+        batch, obs, _ = phase(obs)
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        for _ in range(reps):
+            batch, obs, _ = phase(obs)
+            P.compute_gae_batch(batch.rewards, batch.values, batch.bootstrap, batch.dones, 0.97,
+                                0.95)
+        b.record()
+        torch.cuda.synchronize(dev)
+        env.check()
+        res["graph" if graph else "eager"] = a.elapsed_time(b) / reps
+        env.close()
+    ms = res["graph"]
+    return {"metric": "env-steps/s of on-device PPO rollout collection on the Go1 joystick env "
+                      "(asymmetric actor-critic on tcgen05, CUDA graph)",
+            "value": T * n / (ms / 1e3), "unit": "env_steps/s", "ms_per_phase": ms,
+            "physics_steps_per_s": T * n * GO1_SUBSTEPS / (ms / 1e3),
+            "eager": {"value": T * n / (res["eager"] / 1e3), "ms_per_phase": res["eager"]},
+            "unroll_length": T, "worlds": n}
 
 
 def bench_dropin_step(args, dev, steps=300):

@@ -554,6 +554,13 @@ int dk_go1_reset(dk_go1_env *env, int has_seed, uint64_t seed, void *obs, void *
 int dk_go1_step(dk_go1_env *env, int64_t num_steps, const void *actions, void *obs, void *priv,
                 void *reward, uint8_t *done, uint8_t *trunc, void *terms, void *terminal_obs,
                 uint8_t *terminal_mask, void *stream);
+/* the same with the auto-reset worlds' terminal PRIVILEGED rows too
+ * (terminal_priv [K, N, 75], nullable: the clean last observation of an episode
+ * for an asymmetric critic's truncation bootstrap) */
+int dk_go1_step_ex(dk_go1_env *env, int64_t num_steps, const void *actions, void *obs,
+                   void *priv, void *reward, uint8_t *done, uint8_t *trunc, void *terms,
+                   void *terminal_obs, void *terminal_priv, uint8_t *terminal_mask,
+                   void *stream);
 /* state as row-major device buffers (each nullable): qpos [N,19], qvel [N,18],
  * command [N,3], phase [N,4], airtime [N,4], last_contact u8 [N,4],
  * prev_action [N,12], steps i32 [N], episode u32 [N] */

@@ -108,6 +108,8 @@ _SIGS = {
     "dk_go1_reset": (ctypes.c_int, [_vp, ctypes.c_int, ctypes.c_uint64, _vp, _vp, _vp]),
     "dk_go1_step": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _u8p, _u8p, _vp, _vp, _u8p,
                                    _vp]),
+    "dk_go1_step_ex": (ctypes.c_int, [_vp, _i64, _vp, _vp, _vp, _vp, _u8p, _u8p, _vp, _vp, _vp,
+                                      _u8p, _vp]),
     "dk_go1_get_state": (ctypes.c_int, [_vp] + [_vp] * 9 + [_vp]),
     "dk_go1_check": (ctypes.c_int, [_vp, ctypes.POINTER(_i64), ctypes.POINTER(_i64)]),
     "dk_go1_kernel_launches": (ctypes.c_int64, [_vp]),

@@ -317,6 +317,13 @@ int dk_go1_reset(dk_go1_env *e, int has_seed, uint64_t seed, void *obs, void *pr
 int dk_go1_step(dk_go1_env *e, int64_t K, const void *actions, void *obs, void *priv,
                 void *reward, uint8_t *done, uint8_t *trunc, void *terms, void *terminal_obs,
                 uint8_t *terminal_mask, void *stream) {
+    return dk_go1_step_ex(e, K, actions, obs, priv, reward, done, trunc, terms, terminal_obs,
+                          nullptr, terminal_mask, stream);
+}
+
+int dk_go1_step_ex(dk_go1_env *e, int64_t K, const void *actions, void *obs, void *priv,
+                   void *reward, uint8_t *done, uint8_t *trunc, void *terms, void *terminal_obs,
+                   void *terminal_priv, uint8_t *terminal_mask, void *stream) {
     if (!e) return dk_internal_fail(DK_ERR_INVALID_INPUT, "null handle");
     if (!e->was_reset) return dk_internal_fail(DK_ERR_USAGE, "call reset() before step()");
     if (K < 0) return dk_internal_fail(DK_ERR_INVALID_INPUT, "num_steps must be >= 0");
@@ -335,6 +342,7 @@ int dk_go1_step(dk_go1_env *e, int64_t K, const void *actions, void *obs, void *
         io.trunc = trunc;
         io.terms = (T *)terms;
         io.terminal_obs = (T *)terminal_obs;
+        io.terminal_priv = (T *)terminal_priv;
         io.terminal_mask = terminal_mask;
     };
     if (e->dtype == DK_F64) {

@@ -74,6 +74,7 @@ struct EnvIO {
     uint8_t *done, *trunc;  // [K][n]
     T *terms;               // [K][n][16] nullable
     T *terminal_obs;        // [K][n][56] nullable (rows of auto-reset worlds)
+    T *terminal_priv;       // [K][n][75] nullable: their privileged rows (asymmetric critics)
     uint8_t *terminal_mask; // [K][n] nullable
     unsigned long long *err;  // first (step * n + world) with a non-finite action
     int32_t *bad;             // set when a physics factorisation broke down
@@ -520,6 +521,11 @@ go1_env_kernel(PhysConst<T> pc, EnvConst<T> ec, EnvState<T> st, EnvIO<T> io) {
             }
             // auto-reset: emit the terminal observation, start the next episode
             if (done || trunc) {
+                if (io.terminal_priv) {  // the clean row, before the sensor noise
+                    __syncwarp(qm);
+                    for (int c2 = l; c2 < P; c2 += 4) io.terminal_priv[(k * n + w) * P + c2] = row[c2];
+                    __syncwarp(qm);
+                }
                 add_noise();
                 __syncwarp(qm);
                 if (io.terminal_obs)

@@ -130,7 +130,8 @@ class DeviceGo1Env:
     def _p(t):
         return None if t is None else t.data_ptr()
 
-    def outputs(self, K: int | None, with_priv=True, with_terms=False, with_terminal=True):
+    def outputs(self, K: int | None, with_priv=True, with_terms=False, with_terminal=True,
+                with_terminal_priv=False):
         torch = self._torch
         lead = () if K is None else (int(K),)
         n, dt, dev = self.num_envs, self.dtype, self.device
@@ -140,7 +141,13 @@ class DeviceGo1Env:
                 "reward": e(), "done": e(d=u8), "trunc": e(d=u8),
                 "terms": e(NUM_TERMS) if with_terms else None,
                 "terminal_obs": e(OBS_DIM) if with_terminal else None,
+                "terminal_privileged_state": e(PRIV_DIM) if with_terminal_priv else None,
                 "terminal_mask": e(d=u8) if with_terminal else None}
+
+    def _outputs(self, lead, with_info):
+        """DeviceBatchEnv-style reusable step buffers (collect_rollout_device): one
+        step, with the terminal privileged rows an asymmetric critic bootstraps from."""
+        return self.outputs(None, with_terminal_priv=True)
 
     def reset(self, seed: int | None = None) -> dict:
         torch = self._torch
@@ -162,16 +169,22 @@ class DeviceGo1Env:
         a = a.contiguous()
         K = int(a.shape[0])
         o = out or self.outputs(K, with_terms=with_terms)
-        _check(self._lib.dk_go1_step(
+        _check(self._lib.dk_go1_step_ex(
             self.h, K, a.data_ptr(), o["obs"].data_ptr(), self._p(o.get("privileged_state")),
             o["reward"].data_ptr(), o["done"].data_ptr(), o["trunc"].data_ptr(),
             self._p(o.get("terms")), self._p(o.get("terminal_obs")),
-            self._p(o.get("terminal_mask")), self._stream()))
+            self._p(o.get("terminal_privileged_state")), self._p(o.get("terminal_mask")),
+            self._stream()))
         self._keep = a
         return o
 
-    def step(self, actions, out: dict | None = None, with_terms=False) -> dict:
-        """One control step; actions [N, 12]; outputs without the K axis."""
+    def step(self, actions, out: dict | None = None, with_terms=False, autoreset=True,
+             with_info=False) -> dict:
+        """One control step; actions [N, 12]; outputs without the K axis.  (The
+        episode auto-resets always; ``autoreset`` / ``with_info`` are accepted
+        for collect_rollout_device's DeviceBatchEnv-style calls.)"""
+        if not autoreset:
+            raise ConfigError("DeviceGo1Env always auto-resets")
         a = self._torch.as_tensor(actions, device=self.device, dtype=self.dtype)
         o = out or self.outputs(None, with_terms=with_terms)
         view = {k: (v.unsqueeze(0) if v is not None else None) for k, v in o.items()}

@@ -196,7 +196,8 @@ def _route(obs: dict, cfg):
 
 def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer=None,
                            value_normalizer=None, noise=None, generator=None,
-                           update_normalizers: bool = True, tensor_cores: bool = True):
+                           update_normalizers: bool = True, tensor_cores: bool = True,
+                           _op_by_op: bool = False):
     """Unroll ``cfg.unroll_length`` control steps across the batch on the GPU.
 
     env: DeviceBatchEnv; policy / value: CUDA ``nn.Module``s with the
@@ -234,7 +235,8 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             return pixel_normalize(x, channels_first=False).permute(0, 3, 1, 2)
         return prep(policy_normalizer, x)
 
-    if not pixel_policy and _fused_ok(env, obs, cfg, policy_normalizer, value_normalizer):
+    if not (pixel_policy or _op_by_op) and _fused_ok(env, obs, cfg, policy_normalizer,
+                                                     value_normalizer):
         return _collect_fused(env, policy, value, cfg, obs, policy_normalizer, value_normalizer,
                               noise, generator, update_normalizers, nan_flag, out)
 
@@ -255,8 +257,8 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             raw_reward_sum += reward.mean()
             # truncation bootstraps through the terminal observation (ppo.py:327-341),
             # for every world at once, masked to the truncated, non-terminated ones
-            boot = step["trunc"] & ~step["done"] & step["terminal_mask"]
-            term_in = torch.where(boot[:, None], step["terminal_obs"],
+            boot = step["trunc"].bool() & ~step["done"].bool() & step["terminal_mask"].bool()
+            term_in = torch.where(boot[:, None], step[_terminal_key(step, cfg)],
                                   torch.zeros((), dtype=env.dtype, device=env.device))
             # the value of the observation and of the terminal observation in one
             # network call (rows are independent): 2N rows fill twice the SMs
@@ -271,8 +273,7 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
             rews.append(reward * cfg.reward_scaling + cfg.discounting * term_val)
             dns.append((step["done"] | step["trunc"]).to(torch.float64))
             vals.append(v.to(torch.float64))
-            nxt = step["obs"].clone()
-            obs = {"state": nxt, "privileged_state": nxt}
+            obs = _next_obs(step, clone=True)
             if "pixels" in step:
                 obs["pixels"] = step["pixels"].clone()
         _, val_in = _route(obs, cfg)
@@ -289,6 +290,27 @@ def collect_rollout_device(env, policy, value, cfg, obs: dict, policy_normalizer
     if update_normalizers:
         _update(batch, policy_normalizer, value_normalizer)
     return batch, obs, raw_reward_sum / T
+
+
+def _next_obs(step, clone=False):
+    """The step's observation dict: the policy's ``state`` and the critic's
+    ``privileged_state`` (the same tensor for the analytic tasks; the Go1 env
+    returns both)."""
+    s = step["obs"]
+    p = step.get("privileged_state")
+    p = s if p is None else p
+    if clone:
+        s = s.clone()
+        p = s if p is step["obs"] else p.clone()
+    return {"state": s, "privileged_state": p}
+
+
+def _terminal_key(step, cfg):
+    """The terminal rows the critic bootstraps from: the privileged ones when the
+    value network reads ``privileged_state`` and the env returns them."""
+    if cfg.value_obs_key == "privileged_state" and step.get("terminal_privileged_state") is not None:
+        return "terminal_privileged_state"
+    return "terminal_obs"
 
 
 def _fused_ok(env, obs, cfg, pn, vn):
@@ -371,7 +393,7 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
             step = env.step(act, autoreset=True, with_info=False, out=out)
             _check(lib.dk_ppo_step_bootstrap(
                 N, dv, step["done"].data_ptr(), step["trunc"].data_ptr(),
-                step["terminal_mask"].data_ptr(), step["terminal_obs"].data_ptr(),
+                step["terminal_mask"].data_ptr(), step[_terminal_key(step, cfg)].data_ptr(),
                 ctypes.byref(nv_c), vterm.data_ptr(), count.data_ptr(), pos.data_ptr(),
                 dns[t].data_ptr(), st()))
             if not pair:
@@ -386,10 +408,10 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
                 act.data_ptr(), float(cfg.reward_scaling), float(cfg.discounting),
                 rews[t].data_ptr(), vals[t].data_ptr(), acts[t].data_ptr(),
                 partial[t].data_ptr(), st()))
-            nxt = step["obs"]  # read by the next step's inputs kernel before the env overwrites it
-            obs = {"state": nxt, "privileged_state": nxt}
-        nxt = obs["state"].clone()
-        obs = {"state": nxt, "privileged_state": nxt}
+            # read by the next step's inputs kernel before the env overwrites them
+            obs = _next_obs(step)
+        if T > 0:
+            obs = _next_obs(step, clone=True)  # the phase's last observations, kept
         _, val_in = _route(obs, cfg)
         bootstrap = value(vn.apply(val_in).to(f32) if vn is not None else val_in).to(f64)
     batch = DeviceRolloutBatch(p_obs, v_obs, acts, pres, lps, rews, dns, vals, bootstrap)
@@ -493,45 +515,57 @@ class RolloutGraph:
         batch, obs, self.mean_reward = collect_rollout_device(
             env, policy, value, cfg, obs, policy_normalizer, value_normalizer,
             tensor_cores=False)  # (already wrapped above when requested)
-        self.obs_in = obs["state"].clone()
+        # static observation inputs of the graph: one tensor when the policy and
+        # the critic read the same observation, two for an asymmetric critic
+        st = obs["state"].clone()
+        pv = obs.get("privileged_state")
+        pv = st if pv is None or pv is obs["state"] else pv.clone()
+        self.obs_in = {"state": st, "privileged_state": pv}
         self.last = batch
         # the capture warm-up really steps the env: snapshot the worlds (state,
         # counters, episode) and the sampling generator, and restore both
         # afterwards so the first replay continues exactly where the eager
-        # phase stopped
-        snap = env.state()
+        # phase stopped (envs without set_state -- the Go1 env -- advance one
+        # extra phase here instead)
+        restorable = hasattr(env, "set_state")
+        snap = env.state() if restorable else None
         gen_state = torch.cuda.get_rng_state(env.device)
         side = torch.cuda.Stream(device=env.device)
         side.wait_stream(torch.cuda.current_stream(env.device))
         with torch.cuda.stream(side):  # capture warm-up on a side stream
-            collect_rollout_device(env, policy, value, cfg,
-                                   {"state": self.obs_in, "privileged_state": self.obs_in},
-                                   policy_normalizer, value_normalizer,
-                                   update_normalizers=False, tensor_cores=False)
+            _, warm_obs, _ = collect_rollout_device(env, policy, value, cfg, dict(self.obs_in),
+                                                    policy_normalizer, value_normalizer,
+                                                    update_normalizers=False, tensor_cores=False)
         torch.cuda.current_stream(env.device).wait_stream(side)
         torch.cuda.synchronize(env.device)
-        env.set_state(state=snap[0], target=snap[1], steps=snap[2], episode=snap[3],
-                      needs_reset=snap[4])
+        if restorable:
+            env.set_state(state=snap[0], target=snap[1], steps=snap[2], episode=snap[3],
+                          needs_reset=snap[4])
+        else:
+            self._copy_obs(warm_obs)
         torch.cuda.set_rng_state(gen_state, env.device)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.batch, self.obs_out, self.reward_out = collect_rollout_device(
-                env, policy, value, cfg, {"state": self.obs_in, "privileged_state": self.obs_in},
-                policy_normalizer, value_normalizer, update_normalizers=False,
-                tensor_cores=False)
+                env, policy, value, cfg, dict(self.obs_in), policy_normalizer, value_normalizer,
+                update_normalizers=False, tensor_cores=False)
+
+    def _copy_obs(self, obs):
+        self.obs_in["state"].copy_(obs["state"])
+        if self.obs_in["privileged_state"] is not self.obs_in["state"]:
+            self.obs_in["privileged_state"].copy_(obs["privileged_state"])
 
     def run(self, obs: dict | None = None):
         """One phase from ``obs`` (default: where the previous phase stopped).
         Returns (batch, next obs, mean raw reward); the batch tensors are the
         graph's static outputs, overwritten by the next ``run``."""
-        if obs is not None and obs["state"].data_ptr() != self.obs_in.data_ptr():
-            self.obs_in.copy_(obs["state"])
+        if obs is not None and obs["state"].data_ptr() != self.obs_in["state"].data_ptr():
+            self._copy_obs(obs)
         self.graph.replay()
         _check_phase(self.env, self.batch)
         _update(self.batch, self.pn, self.vn)
-        self.obs_in.copy_(self.obs_out["state"])
-        return self.batch, {"state": self.obs_in, "privileged_state": self.obs_in}, \
-            self.reward_out
+        self._copy_obs(self.obs_out)
+        return self.batch, dict(self.obs_in), self.reward_out
 
 
 __all__ = ["DeviceRolloutBatch", "RolloutGraph", "collect_rollout_device", "evaluate_device",
