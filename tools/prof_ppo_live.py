@@ -1,6 +1,6 @@
 """Per-kernel device time of the PPO rollout phase as it runs (CUDA-graph
 replay, no serialisation): torch.profiler's CUPTI activity over a few
-RolloutGraph phases.  python tools/prof_ppo_live.py"""
+RolloutGraph phases.  python tools/prof_ppo_live.py [--go1]"""
 import os
 import sys
 
@@ -22,11 +22,18 @@ def main():
 
     torch.manual_seed(0)
     n = 8192
-    env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance"), n, dtype="float32")
+    if "--go1" in sys.argv:  # the Go1 joystick env, asymmetric actor-critic
+        from paper_2502_08844_b200 import go1env as G
+        Cfg.value_obs_key = "privileged_state"
+        env = G.DeviceGo1Env(n, G.Go1Config(), dtype="float32")
+        dp, dv, na = 56, 75, 12
+    else:
+        env = dk.DeviceBatchEnv(dk.EnvConfig(task="cartpole-balance"), n, dtype="float32")
+        dp, dv, na = 5, 5, 1
     obs = env.reset(seed=0)
-    policy, value = R.make_policy(5, 1).cuda(), R.make_value(5).cuda()
-    rg = R.RolloutGraph(env, policy, value, Cfg, obs, P.DeviceRunningNormalizer(5),
-                        P.DeviceRunningNormalizer(5))
+    policy, value = R.make_policy(dp, na).cuda(), R.make_value(dv).cuda()
+    rg = R.RolloutGraph(env, policy, value, Cfg, obs, P.DeviceRunningNormalizer(dp),
+                        P.DeviceRunningNormalizer(dv))
     for _ in range(3):
         rg.run()
     torch.cuda.synchronize()
