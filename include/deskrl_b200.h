@@ -322,7 +322,9 @@ int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t 
 /* after the value calls (values [n] of the step's inputs, term_values[pos[i]]
  * of the compacted terminal rows): rewards_out = reward * reward_scaling +
  * discounting * (pos[i] >= 0 ? term_values[pos[i]] : 0), values_out =
- * float64(values), actions_out = float64(action) [n, action_dim], and
+ * float64(values) (values NULL: values_out not written -- the caller evaluates
+ * the phase's values in one call after it), actions_out = float64(action)
+ * [n, action_dim], and
  * reward_partial[dk_ppo_record_blocks(n)] = float64 reward sums per block. */
 int64_t dk_ppo_record_blocks(int64_t n);
 int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const int32_t *pos,

@@ -169,7 +169,8 @@ __global__ void ppo_bootstrap_kernel(int64_t n, int dv, const uint8_t *done, con
     pos[i] = slot;
 }
 
-// after the value calls (values [n] of the step's inputs, term_values[pos[i]]
+// after the value calls (values [n] of the step's inputs, nullable when the
+// caller evaluates the phase's values in one launch after it; term_values[pos[i]]
 // of the boot rows' terminal observations): the reward target, the value, the
 // float64 action, and per-block float64 reward sums (summed in a fixed order by
 // the caller: deterministic)
@@ -186,7 +187,7 @@ ppo_record_kernel(int64_t n, int A, const float *reward, const int32_t *pos, con
         const int32_t p = pos[i];
         const double tv = p >= 0 ? (double)term_values[p] : 0.0;
         rew_out[i] = __dadd_rn(__dmul_rn(r, scale), __dmul_rn(discount, tv));
-        val_out[i] = (double)values[i];
+        if (values) val_out[i] = (double)values[i];
         for (int a = 0; a < A; ++a) act_out[i * A + a] = (double)action[i * A + a];
     }
     red[threadIdx.x] = r;
@@ -362,8 +363,8 @@ int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const int
                        double *values_out, double *actions_out, double *reward_partial,
                        void *stream) {
     dk::PtrDeviceGuard dg_(reward);
-    if (n < 0 || action_dim < 1 || !reward || !pos || !values || !term_values || !action ||
-        !rewards_out || !values_out || !actions_out || !reward_partial)
+    if (n < 0 || action_dim < 1 || !reward || !pos || !term_values || !action ||
+        !rewards_out || (values && !values_out) || !actions_out || !reward_partial)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_record: bad arguments");
     if (n == 0) return DK_OK;
     ppo_record_kernel<<<blocks(n, kRecordThreads), kRecordThreads, 0, (cudaStream_t)stream>>>(

@@ -341,8 +341,10 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     """collect_rollout_device with the per-step bookkeeping in three kernels
     (dk_ppo_step_inputs / _bootstrap / _record) writing straight into the
     phase's [T, N, ...] batch buffers: eight launches per control step (inputs,
-    policy, noise, sampling, env step, bootstrap, value, record) instead of ~30.
-    Same values as the op-by-op path (tests/test_gpu_rollout.py)."""
+    policy, noise, sampling, env step, bootstrap, terminal value, record)
+    instead of ~30.  With the tensor-core networks the step values of the whole
+    phase (and the bootstrap values) are one launch after it.  Same values as
+    the op-by-op path (tests/test_gpu_rollout.py)."""
     import torch
 
     T, N = int(cfg.unroll_length), env.num_envs
@@ -358,7 +360,6 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     raw_v = e(T, N, dv) if vn is not None else None
     acts, pres, lps = e(T, N, A, d=f64), e(T, N, A), e(T, N)
     rews, dns, vals = e(T, N, d=f64), e(T, N, d=f64), e(T, N, d=f64)
-    vin = e(N, dv)  # the value call's rows: this step's normalised inputs
     # the boot rows' terminal observations, compacted (count on the device)
     vterm = torch.zeros((N, dv), dtype=f32, device=dev)
     count = torch.zeros((1,), dtype=torch.int64, device=dev)
@@ -367,6 +368,9 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     from .mlp import _TCPolicy, _TCValue, forward_pair
 
     pair = isinstance(policy, _TCPolicy) and isinstance(value, _TCValue)
+    # the per-step value call's rows (this step's normalised inputs); with the
+    # tensor-core nets the values are evaluated after the phase from v_obs
+    vin = None if pair else e(N, dv)
     act = e(N, A)
     nb = int(lib.dk_ppo_record_blocks(N))
     partial = e(T, nb, d=f64)
@@ -380,13 +384,11 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
                 N, dp, dv, pol_in.data_ptr(), val_in.data_ptr(), ctypes.byref(np_c),
                 ctypes.byref(nv_c), ptr(None if raw_p is None else raw_p[t]),
                 ptr(None if raw_v is None else raw_v[t]), p_obs[t].data_ptr(), v_obs[t].data_ptr(),
-                vin.data_ptr(), st()))
-            if pair:  # policy and value of this step's observations in one launch
-                mean, v = forward_pair(policy.mlp, p_obs[t], value.mlp, vin)
-                log_std = policy.module.log_std.expand_as(mean)
-                v = v.squeeze(-1)
-            else:
-                mean, log_std = policy(p_obs[t])
+                ptr(vin), st()))
+            # (pair: the value of this step's inputs is evaluated with the whole
+            # phase's after it, in one launch: rows are independent, the
+            # normaliser is constant within the phase, so the values are the same)
+            mean, log_std = policy(p_obs[t])
             eps = noise[t].to(mean.dtype) if noise is not None else torch.randn(
                 mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
             _sample(mean, log_std, eps, nan_flag, out=(pres[t], act, lps[t]))
@@ -401,19 +403,28 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
             # terminal values: the compacted boot rows only (tensor-core MLP with a
             # device-side row count), else the whole buffer (rows past the count unread)
             vt = value_count(vterm, count) if value_count is not None else value(vterm)
-            v, vt = (x if x.dtype == f32 and x.is_contiguous() else x.to(f32).contiguous()
-                     for x in (v, vt))
+            v = None if pair else v if v.dtype == f32 and v.is_contiguous() else v.to(f32).contiguous()
+            vt = vt if vt.dtype == f32 and vt.is_contiguous() else vt.to(f32).contiguous()
             _check(lib.dk_ppo_step_record(
-                N, A, step["reward"].data_ptr(), pos.data_ptr(), v.data_ptr(), vt.data_ptr(),
+                N, A, step["reward"].data_ptr(), pos.data_ptr(), ptr(v), vt.data_ptr(),
                 act.data_ptr(), float(cfg.reward_scaling), float(cfg.discounting),
-                rews[t].data_ptr(), vals[t].data_ptr(), acts[t].data_ptr(),
+                rews[t].data_ptr(), None if pair else vals[t].data_ptr(), acts[t].data_ptr(),
                 partial[t].data_ptr(), st()))
             # read by the next step's inputs kernel before the env overwrites them
             obs = _next_obs(step)
         if T > 0:
             obs = _next_obs(step, clone=True)  # the phase's last observations, kept
         _, val_in = _route(obs, cfg)
-        bootstrap = value(vn.apply(val_in).to(f32) if vn is not None else val_in).to(f64)
+        boot_in = vn.apply(val_in).to(f32) if vn is not None else val_in
+        if pair and T > 0:
+            # the phase's values and the bootstrap values in one launch
+            # (T * N rows fill every SM; per step they were 64 of 148)
+            v_all, v_boot = forward_pair(value.mlp, v_obs.view(T * N, dv), value.mlp,
+                                         boot_in.to(f32).contiguous())
+            vals.copy_(v_all.view(T, N))
+            bootstrap = v_boot.squeeze(-1).to(f64)
+        else:
+            bootstrap = value(boot_in).to(f64)
     batch = DeviceRolloutBatch(p_obs, v_obs, acts, pres, lps, rews, dns, vals, bootstrap)
     batch.raw_policy_obs = raw_p.reshape(T * N, dp) if raw_p is not None else None
     batch.raw_value_obs = raw_v.reshape(T * N, dv) if raw_v is not None else None
