@@ -52,9 +52,10 @@ int mlp_args(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const flo
     a.y_stride = y_stride;
     a.desc_swap = desc_swap;
     a.rows_dev = rows_dev;
-    smem = dk::mlp::mlp_smem_bytes(H, net->d_in, net->n_tc, net->n_out);
-    if (smem > 227 * 1024)
+    a.ns = dk::mlp::mlp_stages(H, net->d_in, net->n_out);
+    if (a.ns < 2)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_mlp_forward: network too large");
+    smem = dk::mlp::mlp_smem_bytes(H, net->d_in, net->n_out, a.ns);
     return DK_OK;
 }
 

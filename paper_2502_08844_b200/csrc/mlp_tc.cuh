@@ -15,8 +15,9 @@
 // SWIZZLE_NONE: 8-row x 16-byte core matrices, LBO = core-matrix stride along K,
 // SBO = along M); weights are pre-split and pre-packed in the same layout in HBM
 // (pack_weights_kernel) and streamed per 32-column K chunk by 1-D bulk copies
-// (cp.async.bulk, the TMA engine) into a two-stage ring; one thread issues the
-// MMAs and commits them to mbarriers; in the epilogue each warp reads its 32
+// (cp.async.bulk, the TMA engine) by a loader warp into a 2-4 stage ring (as
+// deep as shared memory allows); one thread of another warp issues the MMAs and
+// commits them to mbarriers; in the epilogue each warp reads its 32
 // TMEM lanes x its column quarter (tcgen05.ld 32x32b): bias, SiLU, split, store;
 // the output layer's four partial sums per row are added in quarter order.
 #pragma once
@@ -30,7 +31,8 @@ namespace mlp {
 
 constexpr int M = 128;          // rows per CTA (= TMEM lanes)
 constexpr int EPI_WARPS = 16;   // warp w < 16 -> TMEM lanes 32 (w % 4), column quarter w / 4
-constexpr int THREADS = 32 * (EPI_WARPS + 1);  // + warp 16: weight copies and MMA issue
+constexpr int THREADS = 32 * (EPI_WARPS + 2);  // + warp 16: MMA issue, warp 17: weight copies
+constexpr int MAXNS = 4;        // weight ring stages (runtime: as many as fit, >= 2)
 constexpr int MAXCH = 8;        // K chunks of a hidden layer (H / KC)
 constexpr int MAXOUT = 16;      // output-layer width
 constexpr int MAXDIN = 128;     // input width (> 16: layer 0 on the tensor cores)
@@ -57,6 +59,7 @@ struct MlpArgs {
     int desc_swap;                    // debug: swap LBO / SBO
     const int64_t *rows_dev;          // nullable: the row count, read on the device
                                       // (<= rows; tiles past it exit at once)
+    int ns;                           // weight ring stages (2..MAXNS, mlp_stages)
 };
 
 // ------------------------------------------------------------------ PTX glue
@@ -165,6 +168,9 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float *v) {
 // range fix-ups of __expf / __fdividef (x -> -inf: e = inf, rcp = 0, -0; x -> +inf:
 // e = 0, x; NaN propagates)
 __device__ __forceinline__ float silu(float x) {
+#ifdef DK_MLP_EXP_NOSILU
+    return x;
+#endif
     float e, r;
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(x * -1.4426950408889634f));
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.0f + e));
@@ -214,8 +220,8 @@ __global__ void pack_weights_kernel(const float *w, int N, int K, __nv_bfloat16 
     lo[e] = l;
 }
 
-// Warp-specialised and pipelined across layers: warp 16 streams the weights and
-// issues the MMAs; warps 0-15 run layer 0 and the epilogues.  Two TMEM
+// Warp-specialised and pipelined across layers: warp 17 streams the weights,
+// warp 16 issues the MMAs; warps 0-15 run layer 0 and the epilogues.  Two TMEM
 // accumulators alternate between layers, and the activations of layer l + 1
 // are handed to the MMA warp K-chunk by K-chunk (an mbarrier per 32-column
 // chunk): layer l + 1's MMAs start on the first chunks while layer l's
@@ -246,23 +252,28 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
     const uint32_t b_chunk = (uint32_t)H * KC * 2;          // one B chunk (hi or lo)
     unsigned char *A_hi = smem;
     unsigned char *A_lo = smem + a_bytes;
-    unsigned char *Bst = smem + 2 * a_bytes;                // [2 stages][hi, lo][b_chunk]
-    // full[2] empty[2] (weight ring), done[2] (accumulator of layer l: done[l & 1]),
-    // achunk[MAXCH] (K chunk c of the current layer's input written)
-    uint64_t *bars = reinterpret_cast<uint64_t *>(Bst + 4 * b_chunk);
-    uint64_t *full = bars, *empty = bars + 2, *done = bars + 4, *achunk = bars + 6;
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 6 + MAXCH);
+    const int ns = a.ns;
+    unsigned char *Bst = smem + 2 * a_bytes;                // [ns stages][hi, lo][b_chunk]
+    // full[ns] empty[ns] (weight ring), done[2] (accumulator of layer l: done[l & 1]),
+    // achunk[MAXCH] (K chunk c of the current layer's input written), w0free (a
+    // CUDA-core layer 0 has read its weights)
+    uint64_t *bars = reinterpret_cast<uint64_t *>(Bst + 2 * ns * b_chunk);
+    uint64_t *full = bars, *empty = bars + MAXNS, *done = bars + 2 * MAXNS,
+             *achunk = bars + 2 * MAXNS + 2;
+    uint64_t *w0free = bars + 2 * MAXNS + 2 + MAXCH;
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * MAXNS + 3 + MAXCH);
     // the float32 parameters used on the CUDA cores, staged once; layer 0's weight
     // rows (CUDA-core layer 0 only) padded to DP columns (zeros past d_in) for
-    // 16-byte loads
+    // 16-byte loads, in the ring's last stage (the loader fills that stage once
+    // layer 0 is done).  (Biases are read from global memory: L1-resident.)
     const bool tc0 = tc_layer0(din);
     const int DP = tc0 ? 0 : din_pad(din);
     const int NO = nout <= 4 ? 4 : MAXOUT;                   // partial-sum slots per row
-    float *s_w0 = reinterpret_cast<float *>(bars + 8 + MAXCH);  // [H][DP]
-    float *s_b0 = s_w0 + H * DP;                             // [H]
-    float *s_bh = s_b0 + H;                                  // [n_tc][H]
-    float *s_wo = s_bh + a.n_tc * H;                         // [nout][H]
-    float *s_red = s_wo + nout * H;                          // [4 quarters][M][NO] partial outputs
+    float *s_w0 = reinterpret_cast<float *>(Bst + 2 * (ns - 1) * b_chunk);  // [H][DP]
+    float *s_wo = reinterpret_cast<float *>(bars + 2 * MAXNS + 4 + MAXCH);  // [nout][H]
+    // [4 quarters][M][NO] partial outputs: written after the last layer's MMAs
+    // completed, so they reuse the activation buffer
+    float *s_red = reinterpret_cast<float *>(A_hi);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int q = warp & 3, quarter = warp >> 2;            // TMEM lane group, column quarter
     const int row = 32 * q + lane;
@@ -274,8 +285,6 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
         const int j = i / DP, k = i - j * DP;
         s_w0[i] = k < din ? a.w0[j * din + k] : 0.0f;
     }
-    for (int i = tid; i < H; i += THREADS) s_b0[i] = a.b0[i];
-    for (int i = tid; i < a.n_tc * H; i += THREADS) s_bh[i] = a.bh[i];
     for (int i = tid; i < nout * H; i += THREADS) s_wo[i] = a.wout[i];
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
@@ -284,8 +293,9 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
     }
     if (tid == 0) {
-        for (int i = 0; i < 6; ++i) mbar_init(&bars[i], 1);
+        for (int i = 0; i < 2 * MAXNS + 2; ++i) mbar_init(&bars[i], 1);
         for (int c = 0; c < MAXCH; ++c) mbar_init(&achunk[c], 4);  // the 4 warps of a quarter
+        mbar_init(w0free, EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     tc_fence_before();
@@ -301,13 +311,16 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
     const int nch0 = tc0 ? k0_pad(din) / KC : nch;           // K chunks of layer 0
     auto layer_chunks = [&](int l) { return l == 0 ? nch0 : nch; };
 
-    if (warp == EPI_WARPS) {
-        // ---------------------------------------------- weights and MMA issue
+    const uint32_t total = (uint32_t)(nch0 + (nl - 1) * nch);  // weight chunks
+    if (warp == EPI_WARPS + 1) {
+        // ---------------------------------------------- weight loader: runs ahead
+        // of the MMAs by up to ns chunks (its own warp: it never waits on the
+        // activations)
         if (lane == 0) {
-            const uint32_t total = (uint32_t)(nch0 + (nl - 1) * nch);
-            // global weight chunk gg -> (layer, K chunk, source)
-            auto load = [&](uint32_t gg) {
-                const int s = gg & 1;
+            for (uint32_t gg = 0; gg < total; ++gg) {
+                const int s = (int)(gg % (uint32_t)ns);
+                if (gg >= (uint32_t)ns) mbar_wait(&empty[s], ((gg / ns) - 1) & 1);  // stage free
+                else if (!tc0 && gg + 1 == (uint32_t)ns) mbar_wait(w0free, 0);  // holds W0
                 int ll, i;
                 if (gg < (uint32_t)nch0) {
                     ll = 0;
@@ -316,24 +329,29 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                     ll = 1 + (int)((gg - nch0) / nch);
                     i = (int)((gg - nch0) % nch);
                 }
-                if (gg >= 2) mbar_wait(&empty[s], ((gg - 2) >> 1) & 1);  // stage free
+#ifdef DK_MLP_EXP_NOLOAD
+                mbar_expect_tx(&full[s], 0);
+                continue;
+#endif
                 mbar_expect_tx(&full[s], 2 * b_chunk);
                 const __nv_bfloat16 *hi, *lo;
-                int c;
                 if (tc0 && ll == 0) {
-                    c = i;
-                    hi = a.w0hi + (size_t)c * H * KC;
-                    lo = a.w0lo + (size_t)c * H * KC;
+                    hi = a.w0hi + (size_t)i * H * KC;
+                    lo = a.w0lo + (size_t)i * H * KC;
                 } else {
-                    c = kchunk(i);
+                    const int c = kchunk(i);
                     const size_t off = (size_t)(ll - (tc0 ? 1 : 0)) * H * H + (size_t)c * H * KC;
                     hi = a.whi + off;
                     lo = a.wlo + off;
                 }
                 bulk_g2s(Bst + (2 * s) * b_chunk, hi, b_chunk, &full[s]);
                 bulk_g2s(Bst + (2 * s + 1) * b_chunk, lo, b_chunk, &full[s]);
-            };
-            load(0);
+            }
+        }
+        __syncwarp();
+    } else if (warp == EPI_WARPS) {
+        // ---------------------------------------------- MMA issue
+        if (lane == 0) {
             const uint32_t idesc = instr_desc_bf16(M, H);
             const uint32_t lbo = a.desc_swap ? 512u : 128u, sbo = a.desc_swap ? 128u : 512u;
             uint32_t gbase = 0;
@@ -343,13 +361,13 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                 for (int i = 0; i < lch; ++i) {
                     const int c = (tc0 && l == 0) ? i : kchunk(i);
                     const uint32_t gc = gbase + (uint32_t)i;
-                    const int s = gc & 1;
+                    const int s = (int)(gc % (uint32_t)ns);
                     // this layer's input, K chunk c: its barrier completed once per
                     // earlier layer whose input had chunk c (a tensor-core layer 0
                     // reads only x's nch0 chunks)
                     const int ph = (tc0 && l > 0 && c >= nch0) ? l - 1 : l;
                     mbar_wait(&achunk[c], ph & 1);
-                    mbar_wait(&full[s], (gc >> 1) & 1);  // its weights
+                    mbar_wait(&full[s], (gc / ns) & 1);  // its weights
                     tc_fence_after();
                     const uint32_t a_hi = smem_u32(A_hi) + c * (M * KC * 2);
                     const uint32_t a_lo = smem_u32(A_lo) + c * (M * KC * 2);
@@ -362,15 +380,16 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                         const uint64_t dal = smem_desc(a_lo + o, lbo, sbo);
                         const uint64_t dbh = smem_desc(b_hi + o, lbo, sbo);
                         const uint64_t dbl = smem_desc(b_lo + o, lbo, sbo);
+#ifndef DK_MLP_EXP_NOMMA
                         mma_bf16(tacc, dah, dbh, idesc, (i | ks) != 0);
                         mma_bf16(tacc, dah, dbl, idesc, 1);
                         mma_bf16(tacc, dal, dbh, idesc, 1);
+#else
+                        (void)dah; (void)dal; (void)dbh; (void)dbl;
+#endif
                     }
                     mma_commit(&empty[s]);  // stage s free once these MMAs complete
                     if (i + 1 == lch) mma_commit(&done[l & 1]);  // layer l's accumulator final
-                    // the next weight chunk after this chunk's MMAs are queued (its
-                    // stage-free wait is on the previous chunk's MMAs)
-                    if (gc + 1 < total) load(gc + 1);
                 }
                 gbase += (uint32_t)lch;
             }
@@ -381,7 +400,9 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
         // hand K chunk c of the next layer's input to the MMA warp: stores
         // visible to the tensor core (async proxy), TMEM reads ordered before
         auto publish = [&](int c) {
+#ifndef DK_MLP_EXP_NOFENCE
             fence_async_smem();
+#endif
             tc_fence_before();
             __syncwarp();
             if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
@@ -401,7 +422,7 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
 #pragma unroll
                 for (int jj = 0; jj < 8; ++jj) {
                     const int j = j0 + jj;
-                    float s = s_b0[j];
+                    float s = __ldg(a.b0 + j);
                     const float4 *w = reinterpret_cast<const float4 *>(s_w0 + j * DPC);
 #pragma unroll
                     for (int i4 = 0; i4 < DPC / 4; ++i4) {
@@ -433,9 +454,17 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                 }
                 publish(quarter);
             }
-        } else if (DP == 4) layer0(std::integral_constant<int, 4>{});
-        else if (DP == 8) layer0(std::integral_constant<int, 8>{});
-        else layer0(std::integral_constant<int, 16>{});
+        } else {
+            if (DP == 4) layer0(std::integral_constant<int, 4>{});
+            else if (DP == 8) layer0(std::integral_constant<int, 8>{});
+            else layer0(std::integral_constant<int, 16>{});
+            // the weight ring's last stage (W0's home) may now be filled
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(
+                                            smem_u32(w0free))
+                                        : "memory");
+        }
         float out_acc[MO];
 #pragma unroll
         for (int o = 0; o < MO; ++o) out_acc[o] = 0.f;
@@ -445,12 +474,17 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
             // ---- epilogue (this thread's row and column quarter): bias, SiLU; split
             // into the next layer's input, or partial output-layer dot products
             const bool last = l + 1 == nl;
-            const float *bias = (tc0 && l == 0) ? s_b0 : s_bh + (size_t)(l - (tc0 ? 1 : 0)) * H;
+            const float *bias = (tc0 && l == 0) ? a.b0 : a.bh + (size_t)(l - (tc0 ? 1 : 0)) * H;
             const uint32_t tacc = tmem + (uint32_t)((l & 1) * H);
             for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
                 float v[32];
+#ifndef DK_MLP_EXP_NOLD
                 tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + cc * 32, v);
-                const float4 *b4 = reinterpret_cast<const float4 *>(bias + cc * 32);
+#else
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = (float)(i + row) * 0.01f;
+#endif
+                const float4 *b4 = reinterpret_cast<const float4 *>(bias + cc * 32);  // 16 B aligned
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
                     const float4 bb = b4[i4];
@@ -477,9 +511,13 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                         }
                     }
                 } else {
+#ifndef DK_MLP_EXP_NOSTORE
 #pragma unroll
                     for (int k8 = 0; k8 < 4; ++k8)
                         store_split8(A_hi, A_lo, row, cc * 32 + k8 * 8, v + 8 * k8);
+#else
+                    if (v[0] == 1234.5f) store_split8(A_hi, A_lo, row, cc * 32, v);
+#endif
                     publish(cc);
                 }
             }
@@ -502,11 +540,22 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
                      "r"(tcols));
 }
 
-inline size_t mlp_smem_bytes(int H, int d_in, int n_tc, int n_out) {
-    const size_t dp = tc_layer0(d_in) ? 0 : (size_t)din_pad(d_in);
-    const size_t no = n_out <= 4 ? 4 : MAXOUT;
-    return 2 * (size_t)M * H * 2 + 4 * (size_t)H * KC * 2 + 8 * (8 + MAXCH) +
-           4 * ((size_t)H * dp + H + (size_t)n_tc * H + (size_t)n_out * H + 4 * M * no);
+// dynamic shared memory of a call with an ns-stage weight ring
+inline size_t mlp_smem_bytes(int H, int d_in, int n_out, int ns) {
+    (void)d_in;  // a CUDA-core layer 0's weights live in the ring's last stage
+    return 2 * (size_t)M * H * 2 + 2 * (size_t)ns * H * KC * 2 + 8 * (2 * MAXNS + 4 + MAXCH) +
+           4 * (size_t)n_out * H;
+}
+
+// the deepest weight ring (<= MAXNS stages) that fits in 227 KB; 0 if none (>= 2)
+inline int mlp_stages(int H, int d_in, int n_out) {
+#ifdef DK_MLP_EXP_NS
+    for (int ns = DK_MLP_EXP_NS; ns >= 2; --ns)  // A/B: a shallower ring
+#else
+    for (int ns = MAXNS; ns >= 2; --ns)
+#endif
+        if (mlp_smem_bytes(H, d_in, n_out, ns) <= 227 * 1024) return ns;
+    return 0;
 }
 
 }  // namespace mlp

@@ -15,9 +15,10 @@ def main():
 
     torch.manual_seed(0)
     kind = os.environ.get("MLP_KIND", "value")
-    net = (R.make_value(5) if kind == "value" else R.make_policy(5, 1)).cuda()
+    din = int(os.environ.get("MLP_DIN", "5"))
+    net = (R.make_value(din) if kind == "value" else R.make_policy(din, 1)).cuda()
     tc = M.tc_value(net) if kind == "value" else M.tc_policy(net)
-    x = torch.randn(int(os.environ.get("MLP_ROWS", "8192")), 5, device="cuda")
+    x = torch.randn(int(os.environ.get("MLP_ROWS", "8192")), din, device="cuda")
     with torch.no_grad():
         for _ in range(5):
             tc(x)
@@ -40,7 +41,7 @@ def main():
             g.replay()
         e1.record()
         torch.cuda.synchronize()
-    print(kind, x.shape[0], "rows: %.1f us per call (graph)" % (e0.elapsed_time(e1) / 100 * 1e3))
+    print(kind, "d_in", din, x.shape[0], "rows: %.1f us per call (graph)" % (e0.elapsed_time(e1) / 100 * 1e3))
 
 
 if __name__ == "__main__":
