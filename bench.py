@@ -78,7 +78,7 @@ def parse():
     if a.unroll <= 0:
         a.unroll = 50 if a.task == GO1 else 1000
     if a.e2e_steps <= 0:
-        a.e2e_steps = 1000 if a.task == GO1 else 20_000
+        a.e2e_steps = 200 if a.task == GO1 else 20_000
     return a
 
 
