@@ -94,10 +94,15 @@ def test_tc_mlp_pair_launch_equals_separate_calls(M):
     (56, 128, 4, 12, 8192),   # a Go1 joystick policy: noisy observation -> 12 joint means
     (75, 256, 5, 1, 3000),    # its critic on the privileged observation
     (17, 128, 3, 16, 129),
+    # H = 256 with 16 outputs: a two-stage weight ring (the deepest that fits), with
+    # a CUDA-core layer 0 (its weights in the ring's last stage) and a tensor-core one
+    (3, 256, 3, 16, 1000),
+    (100, 256, 4, 16, 257),
 ])
 def test_tc_mlp_wide_inputs_and_outputs(M, d_in, hidden, n_layers, n_out, rows):
     """d_in > 16 runs layer 0 on the tensor cores too (K padded to 32); up to 16
-    outputs: against a float64 evaluation."""
+    outputs; 2-, 3- and 4-stage weight rings (csrc/mlp_tc.cuh mlp_stages): against
+    a float64 evaluation."""
     import torch.nn as nn
 
     torch.manual_seed(d_in)
