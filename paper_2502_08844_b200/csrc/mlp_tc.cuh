@@ -476,14 +476,10 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
             const bool last = l + 1 == nl;
             const float *bias = (tc0 && l == 0) ? a.b0 : a.bh + (size_t)(l - (tc0 ? 1 : 0)) * H;
             const uint32_t tacc = tmem + (uint32_t)((l & 1) * H);
-            for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
-                float v[32];
-#ifndef DK_MLP_EXP_NOLD
-                tmem_ld32(tacc + ((uint32_t)(q * 32) << 16) + cc * 32, v);
-#else
-#pragma unroll
-                for (int i = 0; i < 32; ++i) v[i] = (float)(i + row) * 0.01f;
-#endif
+            // one 32-column chunk of this thread's row, loaded from TMEM: bias, SiLU,
+            // then the next layer's input (split, stored, published) or the output
+            // layer's partial dot products
+            auto chunk = [&](int cc, float *v) {
                 const float4 *b4 = reinterpret_cast<const float4 *>(bias + cc * 32);  // 16 B aligned
 #pragma unroll
                 for (int i4 = 0; i4 < 8; ++i4) {
@@ -520,6 +516,17 @@ __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs 
 #endif
                     publish(cc);
                 }
+            };
+            const uint32_t trow = tacc + ((uint32_t)(q * 32) << 16);
+            for (int cc = quarter * HQ / 32; cc < (quarter + 1) * HQ / 32; ++cc) {
+                float v[32];
+#ifndef DK_MLP_EXP_NOLD
+                tmem_ld32(trow + cc * 32, v);
+#else
+#pragma unroll
+                for (int i = 0; i < 32; ++i) v[i] = (float)(i + row) * 0.01f;
+#endif
+                chunk(cc, v);
             }
         }
         // output layer: the four column quarters' partial sums, in quarter order
