@@ -552,9 +552,10 @@ class RolloutGraph:
         if restorable:
             env.set_state(state=snap[0], target=snap[1], steps=snap[2], episode=snap[3],
                           needs_reset=snap[4])
+            torch.cuda.set_rng_state(gen_state, env.device)
         else:
+            # the env moved on: so does the noise (no phase repeats the warm-up's draws)
             self._copy_obs(warm_obs)
-        torch.cuda.set_rng_state(gen_state, env.device)
         self.graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(self.graph):
             self.batch, self.obs_out, self.reward_out = collect_rollout_device(
