@@ -319,19 +319,33 @@ int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t 
                           const uint8_t *terminal_mask, const float *terminal_obs,
                           const dk_ppo_norm *norm_v, float *val_term, int64_t *count,
                           int32_t *pos, double *dones, void *stream);
+/* the same without resetting *count: slots keep counting across the steps of a
+ * phase (val_term holds the whole phase's terminal rows), for one value call
+ * and dk_ppo_boot_fixup after the phase */
+int dk_ppo_step_bootstrap_acc(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
+                              const uint8_t *terminal_mask, const float *terminal_obs,
+                              const dk_ppo_norm *norm_v, float *val_term, int64_t *count,
+                              int32_t *pos, double *dones, void *stream);
 /* after the value calls (values [n] of the step's inputs, term_values[pos[i]]
  * of the compacted terminal rows): rewards_out = reward * reward_scaling +
  * discounting * (pos[i] >= 0 ? term_values[pos[i]] : 0), values_out =
  * float64(values) (values NULL: values_out not written -- the caller evaluates
  * the phase's values in one call after it), actions_out = float64(action)
  * [n, action_dim], and
- * reward_partial[dk_ppo_record_blocks(n)] = float64 reward sums per block. */
+ * reward_partial[dk_ppo_record_blocks(n)] = float64 reward sums per block.
+ * term_values NULL: the boot rows' rewards_out = reward * reward_scaling, their
+ * terminal values added by dk_ppo_boot_fixup after the phase. */
 int64_t dk_ppo_record_blocks(int64_t n);
 int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const int32_t *pos,
                        const float *values, const float *term_values, const float *action,
                        double reward_scaling, double discounting, double *rewards_out,
                        double *values_out, double *actions_out, double *reward_partial,
                        void *stream);
+/* rewards [tn] += discounting * term_values[pos[e]] where pos[e] >= 0 (pos [tn]:
+ * the phase's dk_ppo_step_bootstrap_acc slots): the reward targets of the boot
+ * rows, rounded as dk_ppo_step_record would */
+int dk_ppo_boot_fixup(int64_t tn, const int32_t *pos, const float *term_values,
+                      double discounting, double *rewards, void *stream);
 int dk_ppo_gae(int dtype, int64_t num_steps, int64_t num_worlds, const void *rewards,
                const void *values, const void *dones, const void *bootstrap, double gamma,
                double lam, void *advantages, void *returns, void *stream);

@@ -185,6 +185,9 @@ _SIGS = {
                                           _vp, _vp, _vp, _vp, _vp, _vp]),
     "dk_ppo_step_bootstrap": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp,
                                              _vp, _vp, _vp, _vp]),
+    "dk_ppo_step_bootstrap_acc": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
+                                                 _vp, _vp, _vp, _vp, _vp]),
+    "dk_ppo_boot_fixup": (ctypes.c_int, [_i64, _vp, _vp, ctypes.c_double, _vp, _vp]),
     "dk_ppo_record_blocks": (_i64, [_i64]),
     "dk_ppo_step_record": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
                                           ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp,

@@ -185,8 +185,14 @@ ppo_record_kernel(int64_t n, int A, const float *reward, const int32_t *pos, con
     if (i < n) {
         r = (double)reward[i];
         const int32_t p = pos[i];
-        const double tv = p >= 0 ? (double)term_values[p] : 0.0;
-        rew_out[i] = __dadd_rn(__dmul_rn(r, scale), __dmul_rn(discount, tv));
+        if (!term_values && p >= 0) {
+            // boot row, its terminal value added after the phase
+            // (ppo_boot_fixup_kernel: the same two roundings)
+            rew_out[i] = __dmul_rn(r, scale);
+        } else {
+            const double tv = p >= 0 ? (double)term_values[p] : 0.0;
+            rew_out[i] = __dadd_rn(__dmul_rn(r, scale), __dmul_rn(discount, tv));
+        }
         if (values) val_out[i] = (double)values[i];
         for (int a = 0; a < A; ++a) act_out[i * A + a] = (double)action[i * A + a];
     }
@@ -197,6 +203,16 @@ ppo_record_kernel(int64_t n, int A, const float *reward, const int32_t *pos, con
         __syncthreads();
     }
     if (threadIdx.x == 0) reward_partial[blockIdx.x] = red[0];
+}
+
+// after a phase whose terminal values were evaluated in one call: the boot
+// rows' reward targets get discount * term_values[pos] (pos [T * n])
+__global__ void ppo_boot_fixup_kernel(int64_t tn, const int32_t *pos, const float *term_values,
+                                      double discount, double *rew) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= tn) return;
+    const int32_t p = pos[e];
+    if (p >= 0) rew[e] = __dadd_rn(rew[e], __dmul_rn(discount, (double)term_values[p]));
 }
 
 extern "C" {
@@ -336,23 +352,54 @@ int dk_ppo_step_inputs(int64_t n, int dp, int dv, const float *obs_p, const floa
     return cuda_rc(cudaGetLastError(), "dk_ppo_step_inputs launch");
 }
 
-int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
-                          const uint8_t *terminal_mask, const float *terminal_obs,
-                          const dk_ppo_norm *norm_v, float *val_term, int64_t *count,
-                          int32_t *pos, double *dones, void *stream) {
+namespace {
+int step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
+                   const uint8_t *terminal_mask, const float *terminal_obs,
+                   const dk_ppo_norm *norm_v, float *val_term, int64_t *count, int32_t *pos,
+                   double *dones, bool accumulate, void *stream) {
     dk::PtrDeviceGuard dg_(done);
     if (n < 0 || dv < 1 || !done || !trunc || !terminal_mask || !terminal_obs || !val_term ||
         !count || !pos || !dones)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_bootstrap: bad arguments");
     cudaStream_t st = (cudaStream_t)stream;
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int64_t), st);
-    if (e != cudaSuccess) return cuda_rc(e, "dk_ppo_step_bootstrap count");
+    if (!accumulate) {
+        cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int64_t), st);
+        if (e != cudaSuccess) return cuda_rc(e, "dk_ppo_step_bootstrap count");
+    }
     if (n == 0) return DK_OK;
     dk_ppo_norm off = {};
     ppo_bootstrap_kernel<<<blocks(n, 256), 256, 0, st>>>(n, dv, done, trunc, terminal_mask,
                                                          terminal_obs, norm_v ? *norm_v : off,
                                                          val_term, count, pos, dones);
     return cuda_rc(cudaGetLastError(), "dk_ppo_step_bootstrap launch");
+}
+}  // namespace
+
+int dk_ppo_step_bootstrap(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
+                          const uint8_t *terminal_mask, const float *terminal_obs,
+                          const dk_ppo_norm *norm_v, float *val_term, int64_t *count,
+                          int32_t *pos, double *dones, void *stream) {
+    return step_bootstrap(n, dv, done, trunc, terminal_mask, terminal_obs, norm_v, val_term,
+                          count, pos, dones, false, stream);
+}
+
+int dk_ppo_step_bootstrap_acc(int64_t n, int dv, const uint8_t *done, const uint8_t *trunc,
+                              const uint8_t *terminal_mask, const float *terminal_obs,
+                              const dk_ppo_norm *norm_v, float *val_term, int64_t *count,
+                              int32_t *pos, double *dones, void *stream) {
+    return step_bootstrap(n, dv, done, trunc, terminal_mask, terminal_obs, norm_v, val_term,
+                          count, pos, dones, true, stream);
+}
+
+int dk_ppo_boot_fixup(int64_t tn, const int32_t *pos, const float *term_values,
+                      double discounting, double *rewards, void *stream) {
+    dk::PtrDeviceGuard dg_(pos);
+    if (tn < 0 || !pos || !term_values || !rewards)
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_boot_fixup: bad arguments");
+    if (tn == 0) return DK_OK;
+    ppo_boot_fixup_kernel<<<blocks(tn, 256), 256, 0, (cudaStream_t)stream>>>(
+        tn, pos, term_values, discounting, rewards);
+    return cuda_rc(cudaGetLastError(), "dk_ppo_boot_fixup launch");
 }
 
 int64_t dk_ppo_record_blocks(int64_t n) { return (n + kRecordThreads - 1) / kRecordThreads; }
@@ -363,7 +410,7 @@ int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const int
                        double *values_out, double *actions_out, double *reward_partial,
                        void *stream) {
     dk::PtrDeviceGuard dg_(reward);
-    if (n < 0 || action_dim < 1 || !reward || !pos || !term_values || !action ||
+    if (n < 0 || action_dim < 1 || !reward || !pos || !action ||
         !rewards_out || (values && !values_out) || !actions_out || !reward_partial)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_record: bad arguments");
     if (n == 0) return DK_OK;

@@ -343,8 +343,10 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     phase's [T, N, ...] batch buffers: eight launches per control step (inputs,
     policy, noise, sampling, env step, bootstrap, terminal value, record)
     instead of ~30.  With the tensor-core networks the step values of the whole
-    phase (and the bootstrap values) are one launch after it.  Same values as
-    the op-by-op path (tests/test_gpu_rollout.py)."""
+    phase (and the bootstrap values) are one launch after it, and so are the
+    terminal values of the truncated worlds (one count-limited launch and
+    dk_ppo_boot_fixup): six launches per step.  Same values as the op-by-op path
+    (tests/test_gpu_rollout.py)."""
     import torch
 
     T, N = int(cfg.unroll_length), env.num_envs
@@ -360,10 +362,6 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     raw_v = e(T, N, dv) if vn is not None else None
     acts, pres, lps = e(T, N, A, d=f64), e(T, N, A), e(T, N)
     rews, dns, vals = e(T, N, d=f64), e(T, N, d=f64), e(T, N, d=f64)
-    # the boot rows' terminal observations, compacted (count on the device)
-    vterm = torch.zeros((N, dv), dtype=f32, device=dev)
-    count = torch.zeros((1,), dtype=torch.int64, device=dev)
-    pos = torch.empty((N,), dtype=torch.int32, device=dev)
     value_count = getattr(value, "call_count", None)
     from .mlp import _TCPolicy, _TCValue, forward_pair
 
@@ -371,6 +369,13 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     # the per-step value call's rows (this step's normalised inputs); with the
     # tensor-core nets the values are evaluated after the phase from v_obs
     vin = None if pair else e(N, dv)
+    # the boot rows' terminal observations, compacted (count on the device): per
+    # step, or with the tensor-core nets over the whole phase (slots keep counting;
+    # one count-limited value call and dk_ppo_boot_fixup after the phase)
+    vterm = e(T * N, dv) if pair else torch.zeros((N, dv), dtype=f32, device=dev)
+    count = torch.zeros((1,), dtype=torch.int64, device=dev)
+    pos = torch.empty((T, N) if pair else (1, N), dtype=torch.int32, device=dev)
+    boot_fn = lib.dk_ppo_step_bootstrap_acc if pair else lib.dk_ppo_step_bootstrap
     act = e(N, A)
     nb = int(lib.dk_ppo_record_blocks(N))
     partial = e(T, nb, d=f64)
@@ -393,20 +398,23 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
                 mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
             _sample(mean, log_std, eps, nan_flag, out=(pres[t], act, lps[t]))
             step = env.step(act, autoreset=True, with_info=False, out=out)
-            _check(lib.dk_ppo_step_bootstrap(
+            pos_t = pos[t if pair else 0]
+            _check(boot_fn(
                 N, dv, step["done"].data_ptr(), step["trunc"].data_ptr(),
                 step["terminal_mask"].data_ptr(), step[_terminal_key(step, cfg)].data_ptr(),
-                ctypes.byref(nv_c), vterm.data_ptr(), count.data_ptr(), pos.data_ptr(),
+                ctypes.byref(nv_c), vterm.data_ptr(), count.data_ptr(), pos_t.data_ptr(),
                 dns[t].data_ptr(), st()))
-            if not pair:
+            if pair:
+                v = vt = None
+            else:
                 v = value(vin)
-            # terminal values: the compacted boot rows only (tensor-core MLP with a
-            # device-side row count), else the whole buffer (rows past the count unread)
-            vt = value_count(vterm, count) if value_count is not None else value(vterm)
-            v = None if pair else v if v.dtype == f32 and v.is_contiguous() else v.to(f32).contiguous()
-            vt = vt if vt.dtype == f32 and vt.is_contiguous() else vt.to(f32).contiguous()
+                # terminal values: the compacted boot rows only (tensor-core MLP with a
+                # device-side row count), else the whole buffer (rows past the count unread)
+                vt = value_count(vterm, count) if value_count is not None else value(vterm)
+                v, vt = (x if x.dtype == f32 and x.is_contiguous() else x.to(f32).contiguous()
+                         for x in (v, vt))
             _check(lib.dk_ppo_step_record(
-                N, A, step["reward"].data_ptr(), pos.data_ptr(), ptr(v), vt.data_ptr(),
+                N, A, step["reward"].data_ptr(), pos_t.data_ptr(), ptr(v), ptr(vt),
                 act.data_ptr(), float(cfg.reward_scaling), float(cfg.discounting),
                 rews[t].data_ptr(), None if pair else vals[t].data_ptr(), acts[t].data_ptr(),
                 partial[t].data_ptr(), st()))
@@ -423,6 +431,10 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
                                          boot_in.to(f32).contiguous())
             vals.copy_(v_all.view(T, N))
             bootstrap = v_boot.squeeze(-1).to(f64)
+            # the phase's terminal rows (count-limited), then their reward targets
+            vt_all = value_count(vterm, count)
+            _check(lib.dk_ppo_boot_fixup(T * N, pos.data_ptr(), vt_all.data_ptr(),
+                                         float(cfg.discounting), rews.data_ptr(), st()))
         else:
             bootstrap = value(boot_in).to(f64)
     batch = DeviceRolloutBatch(p_obs, v_obs, acts, pres, lps, rews, dns, vals, bootstrap)
