@@ -345,7 +345,7 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     instead of ~30.  With the tensor-core networks the step values of the whole
     phase (and the bootstrap values) are one launch after it, and so are the
     terminal values of the truncated worlds (one count-limited launch and
-    dk_ppo_boot_fixup): six launches per step.  Same values as the op-by-op path
+    dk_ppo_boot_fixup): seven launches per step.  Same values as the op-by-op path
     (tests/test_gpu_rollout.py)."""
     import torch
 
