@@ -341,6 +341,29 @@ int dk_ppo_step_record(int64_t n, int action_dim, const float *reward, const int
                        double reward_scaling, double discounting, double *rewards_out,
                        double *values_out, double *actions_out, double *reward_partial,
                        void *stream);
+/* one launch after the env step of a phase whose values and terminal values are
+ * evaluated after it: dk_ppo_step_bootstrap_acc + dk_ppo_step_record (values and
+ * term_values NULL) for this step, and dk_ppo_step_inputs for the next step's
+ * observations (next_obs_p NULL: the phase's last step) */
+typedef struct {
+    int64_t n;
+    int32_t dp, dv, action_dim, reserved;
+    /* this step: env outputs and the bootstrap / record buffers */
+    const uint8_t *done, *trunc, *terminal_mask;
+    const float *terminal_obs; /* [n, dv] the critic's terminal rows */
+    float *val_term;           /* compacted boot rows, slots from *count on */
+    int64_t *count;
+    int32_t *pos;              /* [n] slot or -1 */
+    double *dones;             /* [n] */
+    const float *reward, *action;
+    double reward_scaling, discounting;
+    double *rewards_out, *actions_out, *reward_partial;
+    /* the next step's inputs (dk_ppo_step_inputs), nullable */
+    const float *next_obs_p, *next_obs_v;
+    float *next_raw_p, *next_raw_v, *next_pol, *next_val;
+} dk_ppo_post;
+int dk_ppo_step_post(const dk_ppo_post *args, const dk_ppo_norm *norm_p,
+                     const dk_ppo_norm *norm_v, void *stream);
 /* rewards [tn] += discounting * term_values[pos[e]] where pos[e] >= 0 (pos [tn]:
  * the phase's dk_ppo_step_bootstrap_acc slots): the reward targets of the boot
  * rows, rounded as dk_ppo_step_record would */

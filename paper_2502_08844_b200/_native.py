@@ -59,6 +59,19 @@ class PpoNormC(ctypes.Structure):
                 ("copy", ctypes.c_int32), ("present", ctypes.c_int32)]
 
 
+class PpoPostC(ctypes.Structure):
+    """dk_ppo_post (include/deskrl_b200.h)"""
+    _fields_ = [("n", ctypes.c_int64), ("dp", ctypes.c_int32), ("dv", ctypes.c_int32),
+                ("action_dim", ctypes.c_int32), ("reserved", ctypes.c_int32)] + [
+        (f, ctypes.c_void_p) for f in ("done", "trunc", "terminal_mask", "terminal_obs",
+                                       "val_term", "count", "pos", "dones", "reward",
+                                       "action")] + [
+        ("reward_scaling", ctypes.c_double), ("discounting", ctypes.c_double)] + [
+        (f, ctypes.c_void_p) for f in ("rewards_out", "actions_out", "reward_partial",
+                                       "next_obs_p", "next_obs_v", "next_raw_p", "next_raw_v",
+                                       "next_pol", "next_val")]
+
+
 class RewardConfigC(ctypes.Structure):
     _fields_ = [(f, ctypes.c_double) for f in REWARD_FIELDS] + [
         ("standstill_gated", ctypes.c_int32), ("reserved", ctypes.c_int32)]
@@ -188,6 +201,7 @@ _SIGS = {
     "dk_ppo_step_bootstrap_acc": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
                                                  _vp, _vp, _vp, _vp, _vp]),
     "dk_ppo_boot_fixup": (ctypes.c_int, [_i64, _vp, _vp, ctypes.c_double, _vp, _vp]),
+    "dk_ppo_step_post": (ctypes.c_int, [_vp, _vp, _vp, _vp]),
     "dk_ppo_record_blocks": (_i64, [_i64]),
     "dk_ppo_step_record": (ctypes.c_int, [_i64, ctypes.c_int, _vp, _vp, _vp, _vp, _vp,
                                           ctypes.c_double, ctypes.c_double, _vp, _vp, _vp, _vp,

@@ -205,6 +205,60 @@ ppo_record_kernel(int64_t n, int A, const float *reward, const int32_t *pos, con
     if (threadIdx.x == 0) reward_partial[blockIdx.x] = red[0];
 }
 
+static_assert(sizeof(dk_ppo_post) == 192, "dk_ppo_post layout (paper_2502_08844_b200/_native.py PpoPostC)");
+
+// dk_ppo_step_post: one thread per element of the next step's inputs (the
+// first n threads also do world i's bootstrap and record; the first
+// dk_ppo_record_blocks(n) blocks hold the worlds, so the per-block reward sums
+// cover the same 256-world ranges as ppo_record_kernel's)
+__global__ void __launch_bounds__(kRecordThreads)
+ppo_post_kernel(dk_ppo_post a, dk_ppo_norm np_, dk_ppo_norm nv_) {
+    __shared__ double red[kRecordThreads];
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t n = a.n;
+    double r = 0.0;
+    if (e < n) {
+        const int64_t i = e;
+        // bootstrap (ppo_bootstrap_kernel, slots accumulating over the phase)
+        const bool b = a.trunc[i] && !a.done[i] && a.terminal_mask[i];
+        a.dones[i] = (a.done[i] || a.trunc[i]) ? 1.0 : 0.0;
+        int32_t slot = -1;
+        if (b) {
+            slot = (int32_t)atomicAdd(reinterpret_cast<unsigned long long *>(a.count), 1ull);
+            for (int j = 0; j < a.dv; ++j)
+                a.val_term[(int64_t)slot * a.dv + j] = norm_f32(a.terminal_obs[i * a.dv + j], nv_, j);
+        }
+        a.pos[i] = slot;
+        // record (ppo_record_kernel with values / term_values NULL)
+        r = (double)a.reward[i];
+        const double rs = __dmul_rn(r, a.reward_scaling);
+        a.rewards_out[i] = slot >= 0 ? rs : __dadd_rn(rs, __dmul_rn(a.discounting, 0.0));
+        for (int k = 0; k < a.action_dim; ++k)
+            a.actions_out[i * a.action_dim + k] = (double)a.action[i * a.action_dim + k];
+    }
+    if ((int64_t)blockIdx.x * blockDim.x < n) {  // block-uniform
+        red[threadIdx.x] = r;
+        __syncthreads();
+        for (int s2 = kRecordThreads / 2; s2 > 0; s2 >>= 1) {
+            if ((int)threadIdx.x < s2) red[threadIdx.x] = red[threadIdx.x] + red[threadIdx.x + s2];
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) a.reward_partial[blockIdx.x] = red[0];
+    }
+    if (a.next_obs_p) {  // the next step's inputs (ppo_inputs_kernel)
+        if (e < n * a.dp) {
+            const float x = a.next_obs_p[e];
+            if (a.next_raw_p) a.next_raw_p[e] = x;
+            a.next_pol[e] = norm_f32(x, np_, (int)(e % a.dp));
+        }
+        if (e < n * a.dv) {
+            const float x = a.next_obs_v[e];
+            if (a.next_raw_v) a.next_raw_v[e] = x;
+            a.next_val[e] = norm_f32(x, nv_, (int)(e % a.dv));
+        }
+    }
+}
+
 // after a phase whose terminal values were evaluated in one call: the boot
 // rows' reward targets get discount * term_values[pos] (pos [T * n])
 __global__ void ppo_boot_fixup_kernel(int64_t tn, const int32_t *pos, const float *term_values,
@@ -389,6 +443,28 @@ int dk_ppo_step_bootstrap_acc(int64_t n, int dv, const uint8_t *done, const uint
                               int32_t *pos, double *dones, void *stream) {
     return step_bootstrap(n, dv, done, trunc, terminal_mask, terminal_obs, norm_v, val_term,
                           count, pos, dones, true, stream);
+}
+
+int dk_ppo_step_post(const dk_ppo_post *a, const dk_ppo_norm *norm_p,
+                     const dk_ppo_norm *norm_v, void *stream) {
+    if (!a || !a->done) return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_post: null");
+    dk::PtrDeviceGuard dg_(a->done);
+    const bool next = a->next_obs_p != nullptr;
+    if (a->n < 0 || a->dv < 1 || a->action_dim < 1 || !a->trunc || !a->terminal_mask ||
+        !a->terminal_obs || !a->val_term || !a->count || !a->pos || !a->dones || !a->reward ||
+        !a->action || !a->rewards_out || !a->actions_out || !a->reward_partial ||
+        (next && (a->dp < 1 || !a->next_obs_v || !a->next_pol || !a->next_val)))
+        return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_step_post: bad arguments");
+    if (a->n == 0) return DK_OK;
+    dk_ppo_norm off = {};
+    int64_t tot = a->n;
+    if (next) {
+        const int64_t m = a->n * (a->dp > a->dv ? a->dp : a->dv);
+        tot = m > tot ? m : tot;
+    }
+    ppo_post_kernel<<<blocks(tot, kRecordThreads), kRecordThreads, 0, (cudaStream_t)stream>>>(
+        *a, norm_p ? *norm_p : off, norm_v ? *norm_v : off);
+    return cuda_rc(cudaGetLastError(), "dk_ppo_step_post launch");
 }
 
 int dk_ppo_boot_fixup(int64_t tn, const int32_t *pos, const float *term_values,

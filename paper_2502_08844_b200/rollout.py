@@ -345,7 +345,8 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     instead of ~30.  With the tensor-core networks the step values of the whole
     phase (and the bootstrap values) are one launch after it, and so are the
     terminal values of the truncated worlds (one count-limited launch and
-    dk_ppo_boot_fixup): seven launches per step.  Same values as the op-by-op path
+    dk_ppo_boot_fixup), and the bootstrap, record and next step's inputs are one
+    kernel (dk_ppo_step_post): five launches per step.  Same values as the op-by-op path
     (tests/test_gpu_rollout.py)."""
     import torch
 
@@ -375,21 +376,26 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     vterm = e(T * N, dv) if pair else torch.zeros((N, dv), dtype=f32, device=dev)
     count = torch.zeros((1,), dtype=torch.int64, device=dev)
     pos = torch.empty((T, N) if pair else (1, N), dtype=torch.int32, device=dev)
-    boot_fn = lib.dk_ppo_step_bootstrap_acc if pair else lib.dk_ppo_step_bootstrap
     act = e(N, A)
     nb = int(lib.dk_ppo_record_blocks(N))
     partial = e(T, nb, d=f64)
     np_c, nv_c = _norm_c(pn), _norm_c(vn)
     ptr = lambda x: None if x is None else x.data_ptr()  # noqa: E731
     with torch.no_grad():
-        for t in range(T):
-            pol_in, val_in = _route(obs, cfg)
+        def inputs(t, o):  # dk_ppo_step_inputs: step t's normalised inputs from obs o
+            pol_in, val_in = _route(o, cfg)
             pol_in, val_in = pol_in.contiguous(), val_in.contiguous()
             _check(lib.dk_ppo_step_inputs(
                 N, dp, dv, pol_in.data_ptr(), val_in.data_ptr(), ctypes.byref(np_c),
                 ctypes.byref(nv_c), ptr(None if raw_p is None else raw_p[t]),
                 ptr(None if raw_v is None else raw_v[t]), p_obs[t].data_ptr(), v_obs[t].data_ptr(),
                 ptr(vin), st()))
+
+        if pair and T > 0:
+            inputs(0, obs)
+        for t in range(T):
+            if not pair:
+                inputs(t, obs)
             # (pair: the value of this step's inputs is evaluated with the whole
             # phase's after it, in one launch: rows are independent, the
             # normaliser is constant within the phase, so the values are the same)
@@ -398,26 +404,49 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
                 mean.shape, generator=generator, device=mean.device, dtype=mean.dtype)
             _sample(mean, log_std, eps, nan_flag, out=(pres[t], act, lps[t]))
             step = env.step(act, autoreset=True, with_info=False, out=out)
-            pos_t = pos[t if pair else 0]
-            _check(boot_fn(
-                N, dv, step["done"].data_ptr(), step["trunc"].data_ptr(),
-                step["terminal_mask"].data_ptr(), step[_terminal_key(step, cfg)].data_ptr(),
-                ctypes.byref(nv_c), vterm.data_ptr(), count.data_ptr(), pos_t.data_ptr(),
-                dns[t].data_ptr(), st()))
             if pair:
-                v = vt = None
+                # bootstrap + record of this step and the next step's inputs: one launch
+                nxt = None
+                if t + 1 < T:
+                    np_in, nv_in = _route(_next_obs(step), cfg)
+                    if np_in.is_contiguous() and nv_in.is_contiguous():
+                        nxt = (np_in, nv_in)
+                post = nat.PpoPostC(
+                    n=N, dp=dp, dv=dv, action_dim=A, done=step["done"].data_ptr(),
+                    trunc=step["trunc"].data_ptr(), terminal_mask=step["terminal_mask"].data_ptr(),
+                    terminal_obs=step[_terminal_key(step, cfg)].data_ptr(),
+                    val_term=vterm.data_ptr(), count=count.data_ptr(), pos=pos[t].data_ptr(),
+                    dones=dns[t].data_ptr(), reward=step["reward"].data_ptr(),
+                    action=act.data_ptr(), reward_scaling=float(cfg.reward_scaling),
+                    discounting=float(cfg.discounting), rewards_out=rews[t].data_ptr(),
+                    actions_out=acts[t].data_ptr(), reward_partial=partial[t].data_ptr(),
+                    next_obs_p=ptr(nxt[0]) if nxt else None,
+                    next_obs_v=ptr(nxt[1]) if nxt else None,
+                    next_raw_p=ptr(raw_p[t + 1]) if nxt and raw_p is not None else None,
+                    next_raw_v=ptr(raw_v[t + 1]) if nxt and raw_v is not None else None,
+                    next_pol=ptr(p_obs[t + 1]) if nxt else None,
+                    next_val=ptr(v_obs[t + 1]) if nxt else None)
+                _check(lib.dk_ppo_step_post(ctypes.byref(post), ctypes.byref(np_c),
+                                            ctypes.byref(nv_c), st()))
+                if t + 1 < T and nxt is None:  # (strided observations: separately)
+                    inputs(t + 1, _next_obs(step))
             else:
+                _check(lib.dk_ppo_step_bootstrap(
+                    N, dv, step["done"].data_ptr(), step["trunc"].data_ptr(),
+                    step["terminal_mask"].data_ptr(), step[_terminal_key(step, cfg)].data_ptr(),
+                    ctypes.byref(nv_c), vterm.data_ptr(), count.data_ptr(), pos[0].data_ptr(),
+                    dns[t].data_ptr(), st()))
                 v = value(vin)
                 # terminal values: the compacted boot rows only (tensor-core MLP with a
                 # device-side row count), else the whole buffer (rows past the count unread)
                 vt = value_count(vterm, count) if value_count is not None else value(vterm)
                 v, vt = (x if x.dtype == f32 and x.is_contiguous() else x.to(f32).contiguous()
                          for x in (v, vt))
-            _check(lib.dk_ppo_step_record(
-                N, A, step["reward"].data_ptr(), pos_t.data_ptr(), ptr(v), ptr(vt),
-                act.data_ptr(), float(cfg.reward_scaling), float(cfg.discounting),
-                rews[t].data_ptr(), None if pair else vals[t].data_ptr(), acts[t].data_ptr(),
-                partial[t].data_ptr(), st()))
+                _check(lib.dk_ppo_step_record(
+                    N, A, step["reward"].data_ptr(), pos[0].data_ptr(), v.data_ptr(),
+                    vt.data_ptr(), act.data_ptr(), float(cfg.reward_scaling),
+                    float(cfg.discounting), rews[t].data_ptr(), vals[t].data_ptr(),
+                    acts[t].data_ptr(), partial[t].data_ptr(), st()))
             # read by the next step's inputs kernel before the env overwrites them
             obs = _next_obs(step)
         if T > 0:
