@@ -116,3 +116,17 @@ def test_infos_view():
     assert set(infos[1]) == {"upright", "centered", "still", "terminal_observation"}
     assert set(infos[-1]["terminal_observation"]) == {"state", "privileged_state"}
     assert [d.get("terminal_observation") is None for d in infos] == [True, False]
+
+
+def test_ppo_struct_layouts_match_the_header():
+    """ctypes mirrors of the PPO structs: sizes as the C compiler lays them out
+    (capi_ppo.cu static_asserts sizeof(dk_ppo_post) == 192) and field offsets at
+    natural alignment."""
+    import ctypes
+
+    from paper_2502_08844_b200 import _native as nat
+
+    assert ctypes.sizeof(nat.PpoPostC) == 192
+    assert nat.PpoPostC.reward_scaling.offset == 104
+    assert nat.PpoPostC.next_val.offset == 184
+    assert ctypes.sizeof(nat.PpoNormC) == 32
