@@ -129,3 +129,81 @@ def test_gae_ragged_vs_oracle(P, dt, T, N):
     ra, rr = orc.gae(r, v, b, d, 0.99, 0.95)
     np.testing.assert_array_equal(adv.cpu().numpy(), ra.astype(npdt))
     np.testing.assert_array_equal(ret.cpu().numpy(), rr.astype(npdt))
+
+
+def test_step_post_equals_separate_kernels():
+    """dk_ppo_step_post == dk_ppo_step_bootstrap_acc + dk_ppo_step_record (values /
+    term_values NULL) + dk_ppo_step_inputs, and the deferred reward targets
+    (record without term_values, then dk_ppo_boot_fixup) == the direct ones,
+    bit for bit; slots keep counting across calls (the boot rows' slot order
+    follows the atomics, so rows are compared through pos)."""
+    import ctypes
+
+    from paper_2502_08844_b200 import _native as nat
+
+    lib = nat.lib()
+    g = torch.Generator(device="cuda").manual_seed(3)
+    N, dp, dv, A = 1000, 7, 9, 3
+    u8 = lambda p: (torch.rand(N, device="cuda", generator=g) < p).to(torch.uint8)  # noqa: E731
+    rn = lambda *s: torch.randn(*s, device="cuda", generator=g)  # noqa: E731
+    done, trunc, tmask = u8(0.1), u8(0.3), u8(0.8)
+    term_obs, reward, action = rn(N, dv), rn(N), rn(N, A)
+    obs_p, obs_v = rn(N, dp), rn(N, dv)
+    mk = lambda d: (torch.rand(d, device="cuda", dtype=torch.float64, generator=g),  # noqa: E731
+                    torch.rand(d, device="cuda", dtype=torch.float64, generator=g) + 0.5)
+    (mp, vp), (mv, vv) = mk(dp), mk(dv)
+    norm_p = nat.PpoNormC(mp.data_ptr(), vp.data_ptr(), 1e-8, 0, 1)
+    norm_v = nat.PpoNormC(mv.data_ptr(), vv.data_ptr(), 1e-8, 0, 1)
+    scale, disc = 0.3, 0.97
+    nb = int(lib.dk_ppo_record_blocks(N))
+
+    def bufs():
+        z = lambda *s, d=torch.float32: torch.zeros(*s, dtype=d, device="cuda")  # noqa: E731
+        return dict(vterm=z(2 * N, dv), count=z(1, d=torch.int64), pos=z(N, d=torch.int32),
+                    dones=z(N, d=torch.float64), rew=z(N, d=torch.float64),
+                    acts=z(N, A, d=torch.float64), part=z(nb, d=torch.float64),
+                    rawp=z(N, dp), rawv=z(N, dv), pol=z(N, dp), val=z(N, dv))
+
+    a, b = bufs(), bufs()
+    for x in (a, b):
+        x["count"].fill_(5)  # slots continue from earlier steps of the phase
+    P = lambda t: t.data_ptr()  # noqa: E731
+    assert lib.dk_ppo_step_bootstrap_acc(
+        N, dv, P(done), P(trunc), P(tmask), P(term_obs), ctypes.byref(norm_v), P(a["vterm"]),
+        P(a["count"]), P(a["pos"]), P(a["dones"]), None) == 0
+    assert lib.dk_ppo_step_record(
+        N, A, P(reward), P(a["pos"]), None, None, P(action), scale, disc, P(a["rew"]), None,
+        P(a["acts"]), P(a["part"]), None) == 0
+    assert lib.dk_ppo_step_inputs(
+        N, dp, dv, P(obs_p), P(obs_v), ctypes.byref(norm_p), ctypes.byref(norm_v), P(a["rawp"]),
+        P(a["rawv"]), P(a["pol"]), P(a["val"]), None, None) == 0
+    post = nat.PpoPostC(
+        n=N, dp=dp, dv=dv, action_dim=A, done=P(done), trunc=P(trunc), terminal_mask=P(tmask),
+        terminal_obs=P(term_obs), val_term=P(b["vterm"]), count=P(b["count"]), pos=P(b["pos"]),
+        dones=P(b["dones"]), reward=P(reward), action=P(action), reward_scaling=scale,
+        discounting=disc, rewards_out=P(b["rew"]), actions_out=P(b["acts"]),
+        reward_partial=P(b["part"]), next_obs_p=P(obs_p), next_obs_v=P(obs_v),
+        next_raw_p=P(b["rawp"]), next_raw_v=P(b["rawv"]), next_pol=P(b["pol"]),
+        next_val=P(b["val"]))
+    assert lib.dk_ppo_step_post(ctypes.byref(post), ctypes.byref(norm_p), ctypes.byref(norm_v),
+                                None) == 0
+    torch.cuda.synchronize()
+    boot = (trunc.bool() & ~done.bool() & tmask.bool())
+    assert int(a["count"]) == int(b["count"]) == 5 + int(boot.sum()) and boot.sum() > 10
+    for k in ("dones", "rew", "acts", "part", "rawp", "rawv", "pol", "val"):
+        assert torch.equal(a[k], b[k]), k
+    assert torch.equal(a["pos"] >= 0, boot) and torch.equal(b["pos"] >= 0, boot)
+    ia, ib = a["pos"][boot].long(), b["pos"][boot].long()
+    assert torch.equal(a["vterm"][ia], b["vterm"][ib]) and int(ia.min()) >= 5
+
+    # deferred reward targets == direct ones
+    tv = rn(2 * N)
+    direct = torch.zeros(N, dtype=torch.float64, device="cuda")
+    part = torch.zeros(nb, dtype=torch.float64, device="cuda")
+    acts = torch.zeros(N, A, dtype=torch.float64, device="cuda")
+    assert lib.dk_ppo_step_record(
+        N, A, P(reward), P(a["pos"]), None, P(tv), P(action), scale, disc, P(direct), None,
+        P(acts), P(part), None) == 0
+    assert lib.dk_ppo_boot_fixup(N, P(a["pos"]), P(tv), disc, P(a["rew"]), None) == 0
+    torch.cuda.synchronize()
+    assert torch.equal(direct, a["rew"])
