@@ -918,6 +918,114 @@ rollout_kernel(const T *__restrict__ actions, int64_t K, EnvScalars sc, Params<T
 }
 
 // ---------------------------------------------------------------------------
+// One control step (K = 1: BatchEnv.step, the PPO rollout's per-step env call)
+// without the rollout kernel's staging ring: its fixed cost (action staging, the
+// producer / consumer hand-off, the drain: ~6 us at 8192 worlds) is most of a
+// single step.  One thread per world does what the stager, the producer and a
+// consumer do for that world in rollout_kernel, in the same order and with the
+// same arithmetic: validate / clip / control the action (envkit.py:529-532),
+// step (action_repeat loop, reward averaged), count, truncate, reward /
+// observation / info of the post-step state, terminal observation and Philox
+// auto-reset, state into the other buffer; the last block commits the buffer
+// flip unless an error was recorded (batch-atomic, as rollout_kernel).
+template <class Task, typename T, bool R1>
+__global__ void __launch_bounds__(64)
+step1_kernel(const T *__restrict__ actions, EnvScalars sc, Params<T> p, Worlds<T> w,
+             StepOut<T> out, unsigned long long *err) {
+    constexpr int A = Task::A, O = Task::O, I = Task::I;
+    __shared__ int ctrl[2];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) {
+        ctrl[0] = *(volatile const unsigned long long *)err != kNoError;
+        ctrl[1] = *w.cur;
+    }
+    __syncthreads();
+    const bool blocked = ctrl[0] != 0;
+    const int src = ctrl[1];
+    const int64_t n = sc.n;
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (!blocked && i < n) {
+        const T *st_src = src ? w.state[1] : w.state[0];
+        T *st_dst = src ? w.state[0] : w.state[1];
+        const int32_t *steps_src = src ? w.steps[1] : w.steps[0];
+        int32_t *steps_dst = src ? w.steps[0] : w.steps[1];
+        const uint32_t *ep_src = src ? w.episode[1] : w.episode[0];
+        uint32_t *ep_dst = src ? w.episode[0] : w.episode[1];
+        const uint8_t *nr_src = src ? w.needs_reset[1] : w.needs_reset[0];
+        uint8_t *nr_dst = src ? w.needs_reset[0] : w.needs_reset[1];
+        typename Task::W wd;
+        Task::load(wd, st_src, i, n);
+        int32_t steps = steps_src[i];
+        uint32_t episode = ep_src[i];
+        // step at which the world would need a reset (UsageError, envkit.py:527-528)
+        int ku = 1;
+        if (nr_src[i]) ku = 0;
+        else if (!sc.autoreset && (int64_t)sc.episode_length - steps < 1)
+            ku = (int)((int64_t)sc.episode_length - steps);
+        if (ku < 1) record_error(err, ku, n, i, kErrUsage);
+        Task::refresh(wd);
+        // the stager's validation, clip and control
+        bool fin = true;
+        T a[A], u[A];
+#pragma unroll
+        for (int j = 0; j < A; ++j) {
+            const T v = actions[i * A + j];
+            fin &= RealOps<T>::finite_(v);
+            a[j] = fmin(fmax(v, T(-1)), T(1));  // envkit.py:532
+        }
+        Task::control(a, p, u);
+        if (!fin && 0 < ku) record_error(err, 0, n, i, kErrInvalid);  // envkit.py:529-531
+        // the producer's step
+        T rp = T(0);
+        Task::step_u(wd, u, p);
+        if (!R1) {
+            for (int rep = 1; rep < sc.action_repeat; ++rep) {
+                T inf[I];
+                rp += Task::reward(wd, p, inf);
+                Task::step_u(wd, u, p);
+            }
+        }
+        steps += 1;
+        const bool truncated = steps >= sc.episode_length;
+        const bool reset = truncated && sc.autoreset;
+        // the consumer's outputs of the post-step state
+        T info[I];
+        const T r = R1 ? (T(0) + Task::reward(wd, p, info))
+                       : (rp + Task::reward(wd, p, info)) / T(sc.action_repeat);
+        T o[O];
+        Task::obs(wd, p, o);
+        if (reset && out.term_obs) {
+#pragma unroll
+            for (int j = 0; j < O; ++j) out.term_obs[i * O + j] = o[j];
+        }
+        if (!reset) {
+#pragma unroll
+            for (int j = 0; j < O; ++j) out.obs[i * O + j] = o[j];
+        }
+        if (out.info) {
+#pragma unroll
+            for (int j = 0; j < I; ++j) out.info[i * I + j] = info[j];
+        }
+        out.reward[i] = r;
+        out.done[i] = 0;
+        out.trunc[i] = truncated ? 1 : 0;
+        if (out.term_mask) out.term_mask[i] = reset ? 1 : 0;
+        if (__builtin_expect(reset, 0)) {
+            episode += 1;
+            steps = 0;
+            wd = autoreset_world<Task, T>(sc.seed, (uint64_t)(sc.env_offset + i), episode, p,
+                                          sc.wide_init, out.obs + i * O);
+        }
+        Task::store(wd, st_dst, i, n);
+        steps_dst[i] = steps;
+        ep_dst[i] = episode;
+        nr_dst[i] = (!sc.autoreset && steps >= sc.episode_length) ? 1 : 0;
+    }
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    finish_launch(w.cur, w.blocks_done, err, !blocked);
+}
+
+// ---------------------------------------------------------------------------
 // BatchEnv.reset (envkit.py:616-623): rewind -> episode := -1 first.  Writes
 // the live buffer in place (a reset cannot fail).
 

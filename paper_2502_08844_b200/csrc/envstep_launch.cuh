@@ -84,12 +84,35 @@ inline cudaError_t launch_task_rollout_tl(const T *actions, int64_t K, const Env
     return cudaLaunchKernelEx(&cfg, kern, actions, K, scl, p, w, out, err);
 }
 
+// K = 1: one thread per world (step1_kernel), 64-thread blocks so that even a
+// few thousand worlds spread over the SMs; programmatic dependent launch as
+// the rollout kernel
+template <class Task, typename T>
+inline cudaError_t launch_task_step1(const T *actions, const EnvScalars &sc, const Params<T> &p,
+                                     const Worlds<T> &w, const StepOut<T> &out,
+                                     unsigned long long *err, cudaStream_t st) {
+    auto kern = sc.action_repeat == 1 ? step1_kernel<Task, T, true> : step1_kernel<Task, T, false>;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)((sc.n + 63) / 64));
+    cfg.blockDim = dim3(64);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = kUsePdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, actions, sc, p, w, out, err);
+}
+
 template <class Task, typename T>
 inline cudaError_t launch_task_rollout(const T *actions, int64_t K, const EnvScalars &sc,
                                        const Params<T> &p, const Worlds<T> &w,
                                        const StepOut<T> &out, unsigned long long *err,
                                        cudaStream_t st, int64_t *launches) {
     *launches += 1;
+#ifndef DK_NO_STEP1
+    if (K == 1 && sc.n > 0) return launch_task_step1<Task, T>(actions, sc, p, w, out, err, st);
+#endif
     return launch_task_rollout_tl<Task, T, 1>(actions, K, sc, p, w, out, err, st);
 }
 
