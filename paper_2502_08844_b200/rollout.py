@@ -358,23 +358,33 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
     pol_in, val_in = _route(obs, cfg)
     dp, dv, A = pol_in.shape[1], val_in.shape[1], env.action_dim
     e = lambda *s_, d=f32: torch.empty(s_, dtype=d, device=dev)  # noqa: E731
-    p_obs, v_obs = e(T, N, dp), e(T, N, dv)
+    p_obs = e(T, N, dp)
     raw_p = e(T, N, dp) if pn is not None else None
     raw_v = e(T, N, dv) if vn is not None else None
     acts, pres, lps = e(T, N, A, d=f64), e(T, N, A), e(T, N)
     rews, dns, vals = e(T, N, d=f64), e(T, N, d=f64), e(T, N, d=f64)
     value_count = getattr(value, "call_count", None)
-    from .mlp import _TCPolicy, _TCValue, forward_pair
+    from .mlp import _TCPolicy, _TCValue
 
     pair = isinstance(policy, _TCPolicy) and isinstance(value, _TCValue)
     # the per-step value call's rows (this step's normalised inputs); with the
     # tensor-core nets the values are evaluated after the phase from v_obs
     vin = None if pair else e(N, dv)
     # the boot rows' terminal observations, compacted (count on the device): per
-    # step, or with the tensor-core nets over the whole phase (slots keep counting;
-    # one count-limited value call and dk_ppo_boot_fixup after the phase)
-    vterm = e(T * N, dv) if pair else torch.zeros((N, dv), dtype=f32, device=dev)
-    count = torch.zeros((1,), dtype=torch.int64, device=dev)
+    # step; or, with the tensor-core nets, over the whole phase into one value
+    # input buffer -- rows [0, T N) the step inputs (the batch's value_obs),
+    # [T N, T N + N) the final observations' (bootstrap), then the terminal rows
+    # (slots counted from T N + N): one count-limited value call after the phase
+    # and dk_ppo_boot_fixup
+    if pair:
+        vbuf = e((2 * T + 1) * N, dv)
+        v_obs = vbuf[:T * N].view(T, N, dv)
+        vterm = vbuf
+        count = torch.full((1,), T * N + N, dtype=torch.int64, device=dev)
+    else:
+        v_obs = e(T, N, dv)
+        vterm = torch.zeros((N, dv), dtype=f32, device=dev)
+        count = torch.zeros((1,), dtype=torch.int64, device=dev)
     pos = torch.empty((T, N) if pair else (1, N), dtype=torch.int32, device=dev)
     act = e(N, A)
     nb = int(lib.dk_ppo_record_blocks(N))
@@ -454,15 +464,14 @@ def _collect_fused(env, policy, value, cfg, obs, pn, vn, noise, generator, updat
         _, val_in = _route(obs, cfg)
         boot_in = vn.apply(val_in).to(f32) if vn is not None else val_in
         if pair and T > 0:
-            # the phase's values and the bootstrap values in one launch
-            # (T * N rows fill every SM; per step they were 64 of 148)
-            v_all, v_boot = forward_pair(value.mlp, v_obs.view(T * N, dv), value.mlp,
-                                         boot_in.to(f32).contiguous())
-            vals.copy_(v_all.view(T, N))
-            bootstrap = v_boot.squeeze(-1).to(f64)
-            # the phase's terminal rows (count-limited), then their reward targets
-            vt_all = value_count(vterm, count)
-            _check(lib.dk_ppo_boot_fixup(T * N, pos.data_ptr(), vt_all.data_ptr(),
+            # the phase's values, the bootstrap values and the terminal rows' values
+            # in one count-limited launch (T N rows fill every SM; per step they
+            # were 64 of 148), then the boot rows' reward targets
+            vbuf[T * N:T * N + N].copy_(boot_in)
+            y = value_count(vbuf, count)
+            vals.copy_(y[:T * N].view(T, N))
+            bootstrap = y[T * N:T * N + N].to(f64)
+            _check(lib.dk_ppo_boot_fixup(T * N, pos.data_ptr(), y.data_ptr(),
                                          float(cfg.discounting), rews.data_ptr(), st()))
         else:
             bootstrap = value(boot_in).to(f64)
