@@ -201,20 +201,25 @@ __device__ __noinline__ void go1_noise_quad(T *row, uint64_t seed, uint64_t env,
                                             uint32_t episode, uint64_t step,
                                             const double *noise, int l) {
     const int start[5] = {0, 3, 6, 9, 9 + NJ}, len[5] = {3, 3, 3, NJ, NJ};
-    uint64_t q = 0;
-    Philox4x64 r;
-    int64_t have = -1;  // block held in r.buf
-    for (int gi = 0; gi < 5; ++gi) {
-        const double sc = noise[gi];
-        if (!(sc > 0)) continue;
-        for (int e = 0; e < len[gi]; ++e, ++q) {
-            const uint64_t blk = q >> 2;
-            if ((int)(blk & 3) != l) continue;
-            if ((int64_t)blk != have) {
-                philox_seek(r, seed, env, episode, step, blk << 2);
-                have = (int64_t)blk;
+    int total = 0;  // words drawn: the enabled groups' elements
+#pragma unroll
+    for (int gi = 0; gi < 5; ++gi)
+        if (noise[gi] > 0) total += len[gi];
+    // the lanes' blocks side by side (block b on lane b % 4; a block-at-a-time
+    // walk over the words made the quad's lanes take turns)
+    for (int b = l; 4 * b < total; b += 4) {
+        Philox4x64 r;
+        philox_seek(r, seed, env, episode, step, (uint64_t)b << 2);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int q = 4 * b + j;
+            if (q >= total) break;
+            int gi = 0, e = q;  // word q -> element e of enabled group gi
+            while (!(noise[gi] > 0) || e >= len[gi]) {
+                if (noise[gi] > 0) e -= len[gi];
+                ++gi;
             }
-            const int j = (int)(q & 3);
+            const double sc = noise[gi];
             const uint64_t w = j == 0 ? r.buf[0] : j == 1 ? r.buf[1] : j == 2 ? r.buf[2] : r.buf[3];
             const double range = __dsub_rn(sc, -sc);
             const double u = __dmul_rn((double)(w >> 11), 1.0 / 9007199254740992.0);
