@@ -214,16 +214,25 @@ __device__ __noinline__ void go1_noise_quad(T *row, uint64_t seed, uint64_t env,
         for (int j = 0; j < 4; ++j) {
             const int q = 4 * b + j;
             if (q >= total) break;
-            int gi = 0, e = q;  // word q -> element e of enabled group gi
-            while (!(noise[gi] > 0) || e >= len[gi]) {
-                if (noise[gi] > 0) e -= len[gi];
-                ++gi;
+            // word q -> row slot of its element and its group's scale (unrolled:
+            // the group tables stay in registers)
+            int slot = 0, f = 0;
+            double sc = 0.0;
+#pragma unroll
+            for (int gi = 0; gi < 5; ++gi) {
+                const double g_sc = noise[gi];
+                if (g_sc > 0) {
+                    if (q >= f && q < f + len[gi]) {
+                        slot = start[gi] + (q - f);
+                        sc = g_sc;
+                    }
+                    f += len[gi];
+                }
             }
-            const double sc = noise[gi];
             const uint64_t w = j == 0 ? r.buf[0] : j == 1 ? r.buf[1] : j == 2 ? r.buf[2] : r.buf[3];
             const double range = __dsub_rn(sc, -sc);
             const double u = __dmul_rn((double)(w >> 11), 1.0 / 9007199254740992.0);
-            row[start[gi] + e] = row[start[gi] + e] + (T)__dadd_rn(-sc, __dmul_rn(range, u));
+            row[slot] = row[slot] + (T)__dadd_rn(-sc, __dmul_rn(range, u));
         }
     }
 }
