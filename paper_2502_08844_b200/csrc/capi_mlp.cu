@@ -4,6 +4,7 @@
 
 #include "../../include/deskrl_b200.h"
 #include "devguard.h"
+#include "pdl.h"
 #include "mlp_tc.cuh"
 
 extern "C" int dk_internal_fail(int code, const char *msg);  // capi.cu
@@ -70,13 +71,12 @@ int mlp_launch(const dk::mlp::MlpArgs &a0, int64_t t0, const dk::mlp::MlpArgs &a
     static dk::SmemOptIn optin[2];
     cudaError_t e = optin[wide ? 1 : 0].ensure(fn, smem);
     if (e != cudaSuccess) return cuda_rc(e, "dk_mlp_forward attribute");
-    if (wide)
-        dk::mlp::mlp_tc_kernel<dk::mlp::MAXOUT>
-            <<<(unsigned)(t0 + t1), dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(a0, a1, t0);
-    else
-        dk::mlp::mlp_tc_kernel<4>
-            <<<(unsigned)(t0 + t1), dk::mlp::THREADS, smem, (cudaStream_t)stream>>>(a0, a1, t0);
-    return cuda_rc(cudaGetLastError(), "mlp_tc_kernel");
+    // programmatic dependent launch: the grid is placed while the previous kernel
+    // of the PPO step drains (the kernel waits before touching its data)
+    e = dk::launch_pdl(wide ? dk::mlp::mlp_tc_kernel<dk::mlp::MAXOUT> : dk::mlp::mlp_tc_kernel<4>,
+                       dim3((unsigned)(t0 + t1)), dim3(dk::mlp::THREADS), smem,
+                       (cudaStream_t)stream, a0, a1, t0);
+    return cuda_rc(e != cudaSuccess ? e : cudaGetLastError(), "mlp_tc_kernel");
 }
 
 int mlp_forward(const dk_mlp *net, int64_t rows, const int64_t *rows_dev, const float *x,

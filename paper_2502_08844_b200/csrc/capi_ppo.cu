@@ -7,6 +7,7 @@
 #include "ppo_kernels.cuh"
 
 #include "devguard.h"
+#include "pdl.h"
 
 extern "C" int dk_internal_fail(int code, const char *msg);  // capi.cu
 
@@ -84,6 +85,7 @@ int norm_update(int64_t rows, int dim, const T *batch, double count, double *mea
 __global__ void ppo_sample_kernel(int64_t n, int A, const float *mean, const float *log_std,
                                   int64_t ls_stride, const float *eps, float *pre, float *act,
                                   float *lp, int *nan_flag) {
+    dk::pdl_wait();
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= n) return;
     const float kHalfLog2Pi = 0.91893853320467274178f;  // 0.5 * log(2 pi) as float32
@@ -129,6 +131,7 @@ __device__ __forceinline__ float norm_f32(float x, const dk_ppo_norm &nm, int j)
 __global__ void ppo_inputs_kernel(int64_t n, int dp, int dv, const float *obs_p,
                                   const float *obs_v, dk_ppo_norm np_, dk_ppo_norm nv_,
                                   float *raw_p, float *raw_v, float *pol, float *val, float *val2) {
+    dk::pdl_wait();
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t tp = n * dp;
     if (e < tp) {
@@ -213,6 +216,7 @@ static_assert(sizeof(dk_ppo_post) == 192, "dk_ppo_post layout (paper_2502_08844_
 // cover the same 256-world ranges as ppo_record_kernel's)
 __global__ void __launch_bounds__(kRecordThreads)
 ppo_post_kernel(dk_ppo_post a, dk_ppo_norm np_, dk_ppo_norm nv_) {
+    dk::pdl_wait();
     __shared__ double red[kRecordThreads];
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t n = a.n;
@@ -263,6 +267,7 @@ ppo_post_kernel(dk_ppo_post a, dk_ppo_norm np_, dk_ppo_norm nv_) {
 // rows' reward targets get discount * term_values[pos] (pos [T * n])
 __global__ void ppo_boot_fixup_kernel(int64_t tn, const int32_t *pos, const float *term_values,
                                       double discount, double *rew) {
+    dk::pdl_wait();
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= tn) return;
     const int32_t p = pos[e];
@@ -279,9 +284,10 @@ int dk_ppo_sample(int64_t n, int action_dim, const float *mean, const float *log
         !log_prob || !nan_flag)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_sample: bad arguments");
     if (n == 0) return DK_OK;
-    ppo_sample_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-        n, action_dim, mean, log_std, log_std_stride, eps, pre_tanh, action, log_prob, nan_flag);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = dk::launch_pdl(ppo_sample_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256),
+                                   0, (cudaStream_t)stream, n, action_dim, mean, log_std,
+                                   log_std_stride, eps, pre_tanh, action, log_prob, nan_flag);
+    if (e == cudaSuccess) e = cudaGetLastError();
     return e == cudaSuccess ? DK_OK : dk_internal_fail(DK_ERR_CUDA, cudaGetErrorString(e));
 }
 
@@ -400,10 +406,10 @@ int dk_ppo_step_inputs(int64_t n, int dp, int dv, const float *obs_p, const floa
     if (n == 0) return DK_OK;
     dk_ppo_norm off = {};
     const int64_t tot = n * (dp > dv ? dp : dv);
-    ppo_inputs_kernel<<<blocks(tot, 256), 256, 0, (cudaStream_t)stream>>>(
-        n, dp, dv, obs_p, obs_v, norm_p ? *norm_p : off, norm_v ? *norm_v : off, raw_p, raw_v, pol,
-        val, val2);
-    return cuda_rc(cudaGetLastError(), "dk_ppo_step_inputs launch");
+    const cudaError_t e = dk::launch_pdl(
+        ppo_inputs_kernel, dim3(blocks(tot, 256)), dim3(256), 0, (cudaStream_t)stream, n, dp, dv,
+        obs_p, obs_v, norm_p ? *norm_p : off, norm_v ? *norm_v : off, raw_p, raw_v, pol, val, val2);
+    return cuda_rc(e != cudaSuccess ? e : cudaGetLastError(), "dk_ppo_step_inputs launch");
 }
 
 namespace {
@@ -462,9 +468,10 @@ int dk_ppo_step_post(const dk_ppo_post *a, const dk_ppo_norm *norm_p,
         const int64_t m = a->n * (a->dp > a->dv ? a->dp : a->dv);
         tot = m > tot ? m : tot;
     }
-    ppo_post_kernel<<<blocks(tot, kRecordThreads), kRecordThreads, 0, (cudaStream_t)stream>>>(
-        *a, norm_p ? *norm_p : off, norm_v ? *norm_v : off);
-    return cuda_rc(cudaGetLastError(), "dk_ppo_step_post launch");
+    const cudaError_t e = dk::launch_pdl(ppo_post_kernel, dim3(blocks(tot, kRecordThreads)),
+                                         dim3(kRecordThreads), 0, (cudaStream_t)stream, *a,
+                                         norm_p ? *norm_p : off, norm_v ? *norm_v : off);
+    return cuda_rc(e != cudaSuccess ? e : cudaGetLastError(), "dk_ppo_step_post launch");
 }
 
 int dk_ppo_boot_fixup(int64_t tn, const int32_t *pos, const float *term_values,
@@ -473,9 +480,10 @@ int dk_ppo_boot_fixup(int64_t tn, const int32_t *pos, const float *term_values,
     if (tn < 0 || !pos || !term_values || !rewards)
         return dk_internal_fail(DK_ERR_INVALID_INPUT, "dk_ppo_boot_fixup: bad arguments");
     if (tn == 0) return DK_OK;
-    ppo_boot_fixup_kernel<<<blocks(tn, 256), 256, 0, (cudaStream_t)stream>>>(
-        tn, pos, term_values, discounting, rewards);
-    return cuda_rc(cudaGetLastError(), "dk_ppo_boot_fixup launch");
+    const cudaError_t e = dk::launch_pdl(ppo_boot_fixup_kernel, dim3(blocks(tn, 256)), dim3(256),
+                                         0, (cudaStream_t)stream, tn, pos, term_values,
+                                         discounting, rewards);
+    return cuda_rc(e != cudaSuccess ? e : cudaGetLastError(), "dk_ppo_boot_fixup launch");
 }
 
 int64_t dk_ppo_record_blocks(int64_t n) { return (n + kRecordThreads - 1) / kRecordThreads; }

@@ -238,6 +238,9 @@ template <int MO>
 __global__ void __launch_bounds__(THREADS, 1) mlp_tc_kernel(MlpArgs a0, MlpArgs a1,
                                                             int64_t tiles0) {
     extern __shared__ __align__(1024) unsigned char smem[];
+    // programmatic dependent launch (capi_mlp.cu): nothing of the previous
+    // kernel's (inputs, row count, outputs) is touched before this
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const bool second = (int64_t)blockIdx.x >= tiles0;
     MlpArgs a = second ? a1 : a0;
     const int64_t tile = second ? (int64_t)blockIdx.x - tiles0 : (int64_t)blockIdx.x;
